@@ -1,0 +1,436 @@
+#!/usr/bin/env python3
+"""Benchmark of the raycasting-RMP hot path (BASELINE.json ``metric``).
+
+Workload (one "step"): config C4's shape on the C1 headline map -- P = 4096
+robot poses (bench_states, seed 123) x 65536 Halton rays each, 200x200x100
+node map @0.1 m (200 random boxes, f32-exact values), 10 m range, preset
+``static_map`` -- evaluated as ONE fused launch (trace + per-ray policy +
+reduction + 3x3 pinv per pose).  ``value`` is whole-job rays/s with inputs
+resident in HBM (CUDA events around each step, L2 flushed between steps);
+``hz`` is the matching 65536-ray policy-evaluation rate.  Under torchrun
+each rank evaluates its own block of P poses (weak scaling, no collective on
+the data path).
+
+``e2e`` is the same metric through the public host API
+(``ray_policy_batch`` with host arrays: pose upload + result download inside
+the timed region).  ``latency_hz`` is the single-pose ``ray_policy`` call
+rate (the paper's load -> execute -> readback window).
+
+``--impl reference`` times the reference's own compiled CPU kernels
+(oracle/_ref, built from /root/reference) on the box's host cores on the
+same workload, a bounded sample of poses per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = ("rays/sec and RMP evaluation rate (Hz) at 65536 rays; "
+          "voxel-steps/s vs L2/HBM BW")
+N_RAYS = 65536
+MAX_RANGE = 10.0
+PARAMS = (88.0, 1.4, 140.0, 1.2, 1e-6, 2.4, 0.2)  # static_map, kernel order
+BYTES_PER_STEP = 32  # 8 corner reads x f32 storage
+
+
+def _env_int(k, d):
+    try:
+        return int(os.environ.get(k, d))
+    except ValueError:
+        return d
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu: int):
+        self.gpu = gpu
+        self.proc = None
+        self.lines: list[str] = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.t.join(timeout=2)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = float(parts[1])
+            except ValueError:
+                continue
+            for nm, val in zip(names, parts[3:7]):
+                if val.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def build_world(backend_bake=None, distance=None, total_poses=4096):
+    from paper_2301_08068_b200 import synth
+
+    scene = synth.c1_scene()
+    grid = synth.c1_grid(scene, bake=backend_bake)
+    states = synth.bench_states(scene, count=total_poses, seed=123, distance=distance)
+    return scene, grid, states
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh), "measured"
+    except Exception:
+        return {"hbm_gbs": 6650.0}, "fallback"
+
+
+# ----------------------------------------------------------------------------
+# our arm
+
+def run_b200(args):
+    import torch
+    import torch.distributed as dist
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    os.environ["RMPNAV_DEVICE"] = str(local)
+
+    from paper_2301_08068_b200 import _lib, synth
+    from paper_2301_08068_b200._kernels import b200
+    from paper_2301_08068_b200.device import RayPolicyEngine
+    from paper_2301_08068_b200.policies import ObstacleParams, ray_policy, ray_policy_batch
+    from paper_2301_08068_b200.rays import sample_directions
+
+    b200.set_device(local)
+    P = args.poses
+    scene, grid, states_all = build_world(total_poses=P * world)
+    states = states_all[rank * P:(rank + 1) * P]
+    x_h, v_h = synth.states_arrays(states)
+    bundle = sample_directions(N_RAYS)  # Halton bundle generated on device
+    params = ObstacleParams(88.0, 1.4, 140.0, 1.2, 2.4, 0.2)
+    eng = RayPolicyEngine(grid, bundle, params.as_tuple(), MAX_RANGE, device=local)
+    dev = torch.device("cuda", local)
+    x = torch.from_numpy(x_h).to(dev)
+    v = torch.from_numpy(v_h).to(dev)
+    slots = torch.empty((P, 13), dtype=torch.float64, device=dev)
+    accels = torch.empty((P, 3), dtype=torch.float64, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    # calibration (untimed): voxel-steps per step, for the roofline numerator
+    steps_ctr = torch.zeros(1, dtype=torch.int64, device=dev)
+    eng.evaluate(x, v, slots, accels, step_counter=steps_ctr)
+    torch.cuda.synchronize()
+    vox_steps = int(steps_ctr.item())
+
+    stream = torch.cuda.current_stream()
+    for _ in range(args.warmup):
+        flush.zero_()
+        eng.evaluate(x, v, slots, accels)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    clocks = ClockSampler(local)
+    clocks.start()
+    n0 = _lib.launch_count()
+    total_ms = 0.0
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush between timed steps (256 MiB > 126 MB L2)
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng.evaluate(x, v, slots, accels)
+        e1.record(stream)
+        e1.synchronize()
+        total_ms += e0.elapsed_time(e1)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - n0
+    if world > 1:
+        dist.barrier()
+    clk = clocks.stop()
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    total_ms = float(t.item())
+    ms_per_step = total_ms / args.steps
+    rays_per_step = P * N_RAYS * world
+    value = rays_per_step / (ms_per_step * 1e-3)
+    hz = P * world / (ms_per_step * 1e-3)
+
+    # e2e: public host API, host arrays in, host results out, every step
+    for _ in range(2):
+        ray_policy_batch((x_h, v_h), grid, bundle, params, MAX_RANGE)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e2e_s = 0.0
+    for _ in range(args.steps):
+        flush.zero_()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        acc_h, met_h, nh = ray_policy_batch((x_h, v_h), grid, bundle, params, MAX_RANGE)
+        e2e_s += time.perf_counter() - t0
+    t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    e2e_s = float(t.item())
+    e2e_value = rays_per_step * args.steps / e2e_s
+
+    # single-pose latency through ray_policy (paper's window), rank-local
+    lat = []
+    for i in range(args.latency_calls + 20):
+        st = states[i % len(states)]
+        t0 = time.perf_counter()
+        ray_policy(st, grid, bundle, params, MAX_RANGE)
+        if i >= 20:
+            lat.append(time.perf_counter() - t0)
+    lat_med = statistics.median(lat)
+
+    # live kernel duration = step time (one k_ray_policy launch per step)
+    kern_ms = ms_per_step
+    peaks, peak_src = measured_peaks()
+    algo_bytes = vox_steps * BYTES_PER_STEP
+    achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
+    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+            "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
+            "traffic": args.ncu_traffic, "peak_source": peak_src,
+            "kernel": "k_ray_policy<QuadGridF32>",
+            "algorithmic_bytes_per_launch": algo_bytes,
+            "voxel_steps_per_launch": vox_steps,
+            "note": "bytes = voxel-steps x 8 corners x 4 B (f32 map); map is L2-resident"}
+
+    out = None
+    if rank == 0:
+        cpu = None
+        if world == 1 and not args.no_cpu_baseline:
+            cpu = cpu_baseline(grid, states, args.cpu_seconds)
+        out = {
+            "metric": METRIC, "value": round(value, 1), "unit": "rays/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_per_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic",
+            "config": {"workload": "C4-shape batch on the C1 headline map: "
+                                   f"{P} poses/rank x {N_RAYS} Halton rays, 200x200x100 "
+                                   "@0.1 m (200 boxes), max range 10 m, static_map",
+                       "poses_per_rank": P, "rays_per_pose": N_RAYS, "max_range_m": MAX_RANGE,
+                       "map": "C1 200x200x100 @0.1m f32-exact, QUAD layout",
+                       "l2": "flushed (256 MiB write) between timed steps",
+                       "parallelism": f"pose-sharded x{world}"},
+            "hz": round(hz, 1),
+            "voxel_steps_per_s": round(vox_steps * world / (ms_per_step * 1e-3), 1),
+            "latency_hz": round(1.0 / lat_med, 1),
+            "latency_us_median": round(lat_med * 1e6, 2),
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "e2e": {"value": round(e2e_value, 1), "unit": "rays/s",
+                    "h2d_bytes_per_step": int(P * 6 * 8), "d2h_bytes_per_step": int(P * 16 * 8),
+                    "api": "paper_2301_08068_b200.ray_policy_batch (host arrays)"},
+            "gpu_launches": int(launches),
+            "clocks": clk,
+        }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+# ----------------------------------------------------------------------------
+# CPU legs (reference kernels from oracle/_ref; C port fallback)
+
+def _cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(grid, states, seconds=10.0, threads=None):
+    """Times the reference's CPU path (oracle/_ref compiled kernels driven as
+    rmpnav's ckern.py/_pool.py do) on a bounded sample of this workload."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    threads = threads or _cpu_threads()
+    dirs = O.sample_directions(N_RAYS)
+    vals = grid.values
+    kind = "reference" if O.ref_available() else "port"
+    pool = O.RefPool(threads)
+    done, t0 = 0, time.perf_counter()
+    try:
+        while True:
+            st = states[done % len(states)]
+            if kind == "reference":
+                O.ref_ray_policy(vals, grid.origin, grid.resolution, st.position, st.velocity,
+                                 dirs, PARAMS, MAX_RANGE, pool)
+            else:
+                O.ray_policy(vals, grid.origin, grid.resolution, st.position, st.velocity, dirs,
+                             PARAMS, MAX_RANGE, workers=threads)
+            done += 1
+            el = time.perf_counter() - t0
+            if (el >= seconds and done >= 3) or done >= 100000:
+                break
+    finally:
+        pool.close()
+    rays_s = done * N_RAYS / el
+    return {"value": round(rays_s, 1), "unit": "rays/s", "cores": threads, "kind": kind,
+            "hz": round(done / el, 2),
+            "sample": f"{done} poses x {N_RAYS} rays of the same workload in {el:.1f} s "
+                      f"({threads} threads, reference chunk pool, CHUNK=2048)"}
+
+
+def run_reference(args):
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    if rank != 0:
+        return None
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    threads = _cpu_threads()
+    kind = "reference" if O.ref_available() else "port"
+    if kind == "reference":
+        K = O.ref()
+
+        def bake(pack, origin, res, dims):
+            out = np.empty(tuple(dims))
+            nx = dims[0]
+            pool = O.RefPool(threads)
+            args_ = (pack["kinds"], pack["ops"], pack["centers"], pack["sizes"],
+                     pack["velocities"], pack["empty_dist"])
+            pool.run(lambda i, s, e: K.bake_chunk(*args_, origin[0], origin[1], origin[2], res,
+                                                  s, e, out), nx, chunk=max(1, nx // (4 * threads)))
+            pool.close()
+            return out
+
+        def distance_factory(scene):
+            pk = scene.packed()
+            a = (pk["kinds"], pk["ops"], pk["centers"], pk["sizes"], pk["velocities"],
+                 pk["empty_dist"])
+
+            def d(x):
+                out = np.empty(1)
+                K.scene_distance_chunk(*a, 0.0, np.ascontiguousarray(x.reshape(1, 3)), 0, 1, out)
+                return float(out[0])
+            return d
+    else:
+        bake = O.bake_values
+
+        def distance_factory(scene):
+            return lambda x: float(O.scene_distance_many(scene.packed(), x.reshape(1, 3), 0.0)[0])
+
+    from paper_2301_08068_b200 import synth
+
+    scene = synth.c1_scene()
+    grid = synth.c1_grid(scene, bake=bake)
+    states = synth.bench_states(scene, count=args.poses, seed=123,
+                                distance=distance_factory(scene))
+    dirs = O.sample_directions(N_RAYS)
+    pool = O.RefPool(threads)
+    sample = args.ref_poses_per_step
+
+    def one_step(base):
+        for j in range(sample):
+            st = states[(base + j) % len(states)]
+            if kind == "reference":
+                O.ref_ray_policy(grid.values, grid.origin, grid.resolution, st.position,
+                                 st.velocity, dirs, PARAMS, MAX_RANGE, pool)
+            else:
+                O.ray_policy(grid.values, grid.origin, grid.resolution, st.position, st.velocity,
+                             dirs, PARAMS, MAX_RANGE, workers=threads)
+
+    for w in range(args.warmup):
+        one_step(w * sample)
+    t0 = time.perf_counter()
+    for k in range(args.steps):
+        one_step((args.warmup + k) * sample)
+    el = time.perf_counter() - t0
+    pool.close()
+    rays = args.steps * sample * N_RAYS
+    value = rays / el
+    ms = el / args.steps * 1e3
+    return {
+        "impl": "reference", "metric": METRIC, "value": round(value, 1), "unit": "rays/s",
+        "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 3),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic",
+        "config": {"workload": "C4-shape batch on the C1 headline map (CPU: bounded sample of "
+                               f"{sample} poses per step) x {N_RAYS} Halton rays, 200x200x100 "
+                               "@0.1 m (200 boxes), max range 10 m, static_map",
+                   "poses_per_step": sample, "rays_per_pose": N_RAYS, "max_range_m": MAX_RANGE},
+        "hz": round(args.steps * sample / el, 2),
+        "cpu_baseline": {"value": round(value, 1), "unit": "rays/s", "cores": threads,
+                         "kind": kind,
+                         "sample": f"{sample} poses x {N_RAYS} rays per step, {threads} threads"},
+        "e2e": {"value": round(value, 1), "unit": "rays/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+
+
+def main(argv=None):
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--poses", type=int, default=4096, help="poses per rank per step")
+    ap.add_argument("--latency-calls", type=int, default=200)
+    ap.add_argument("--cpu-seconds", type=float, default=10.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-poses-per-step", type=int, default=8)
+    ap.add_argument("--ncu-traffic", type=float, default=None,
+                    help="dram bytes per launch from an ncu --set full capture")
+    args = ap.parse_args(argv)
+    if args.warmup < 3 and args.impl == "b200":
+        print("warning: fewer than 3 warm-up steps", file=sys.stderr)
+    out = run_reference(args) if args.impl == "reference" else run_b200(args)
+    if out is not None:
+        print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,215 @@
+/*
+ * rmpb.h -- C ABI of the B200-native raycasting-RMP evaluator (librmpb.so).
+ *
+ * This is the drop-in boundary for the reference's kernel-backend protocol
+ * (rmpnav/_kernels/__init__.py:17-59; the "compiled" backend
+ * rmpnav/_kernels/ckern.py:19-93 and its NumPy twin npkern.py:21-221).  A
+ * backend there is a module with 7 functions; each is served here by one
+ * or more entry points (paths relative to /root/reference/pkg/src/):
+ *
+ *   grid_trace        (ckern.py:49-62)  -> rmpb_grid_trace            [unfused parity]
+ *   policy_reduce     (ckern.py:80-93)  -> rmpb_policy_reduce         [unfused parity]
+ *   ray_policy        (policies.py:182-192: grid_trace+policy_reduce+pinv_psd)
+ *                                       -> rmpb_ray_policy            [fused K1]
+ *   lidar_policy      (policies.py:195-205) -> rmpb_lidar_policy      [K2]
+ *   pinv_psd          (core.py:103-115) -> rmpb_pinv_psd
+ *   bake_values       (ckern.py:25-35)  -> rmpb_bake / rmpb_bake_grid [row f2]
+ *   scene_distance_many (ckern.py:19-23)-> rmpb_scene_distance        [row f3]
+ *   scene_trace       (ckern.py:65-77)  -> rmpb_scene_trace           [row f3]
+ *   esdf_sample_many  (ckern.py:38-46)  -> rmpb_esdf_sample           [row f4]
+ *
+ * plus batched / device-resident entries the reference does not have
+ * (multi-pose K3, ray-range partials + fixed-order fold for GPU splits,
+ * LiDAR from raw points, device-side Halton bundles).
+ *
+ * Conventions
+ *   - Plain C: pointers, sizes, doubles.  No C++ or torch types.
+ *   - Every function returns int status: RMPB_OK (0) or a negative code;
+ *     rmpb_last_error() gives a thread-local message.  The reference raises
+ *     ValueError for bad arguments (rmpnav/_kernels/__init__.py:45-48 and
+ *     Cython buffer checks); the Python host layer maps RMPB_ERR_INVALID to
+ *     ValueError and everything else to RuntimeError.
+ *   - Host-buffer entries copy inputs in, run, copy results out and return
+ *     when results are on the host (the caller owns all host buffers).
+ *   - *_device entries take device pointers (e.g. torch tensors' data_ptr)
+ *     and are asynchronous on `stream`.
+ *   - `stream` is a cudaStream_t (NULL = legacy default stream).  Calls on
+ *     distinct streams are thread-safe.
+ *   - Handles (grid, bundle, scene) are library-owned device objects bound
+ *     to one CUDA device.
+ *   - Params are the reference kernel argument order (policies.py:80-83):
+ *     {eta_rep, nu_rep, eta_damp, nu_damp, epsilon, radius, c}.
+ *   - Slots are the reference's 13-double layout (ckern.py:91-93, before
+ *     reshaping): [A (3x3 row-major, symmetric), A f (3), n_hits].
+ */
+#ifndef RMPB_H
+#define RMPB_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#if defined(__GNUC__)
+#define RMPB_EXPORT __attribute__((visibility("default")))
+#else
+#define RMPB_EXPORT
+#endif
+
+#define RMPB_API_VERSION 1
+
+enum {
+  RMPB_OK = 0,
+  RMPB_ERR_INVALID = -1,     /* bad argument (ValueError in the reference) */
+  RMPB_ERR_CUDA = -2,        /* CUDA runtime / launch failure */
+  RMPB_ERR_NOMEM = -3,       /* device or pinned allocation failed */
+  RMPB_ERR_UNSUPPORTED = -4  /* option not available for this handle */
+};
+
+enum { RMPB_F32 = 0, RMPB_F64 = 1 };                              /* value dtypes */
+enum { RMPB_STORE_AUTO = 0, RMPB_STORE_F32 = 1, RMPB_STORE_F64 = 2 }; /* grid storage */
+enum { RMPB_LAYOUT_LINEAR = 0, RMPB_LAYOUT_QUAD = 1, RMPB_LAYOUT_BRICK = 2,
+       RMPB_LAYOUT_AUTO = -1 };
+enum { RMPB_ORDER_IDENTITY = 0, RMPB_ORDER_MORTON = 1 };          /* bundle evaluation order */
+
+typedef struct rmpb_grid rmpb_grid;
+typedef struct rmpb_bundle rmpb_bundle;
+typedef struct rmpb_scene rmpb_scene;
+
+/* ---- library ---------------------------------------------------------- */
+RMPB_EXPORT const char* rmpb_last_error(void);
+RMPB_EXPORT int rmpb_api_version(void);
+RMPB_EXPORT int rmpb_device_count(int* n);
+/* Number of kernels this library has launched (all devices, since load). */
+RMPB_EXPORT uint64_t rmpb_launch_count(void);
+/* Tuning knobs ("seg_rays": rays per CTA unit, 0 = heuristic). */
+RMPB_EXPORT int rmpb_set_option(const char* name, int64_t value);
+
+/* ---- maps (EsdfGrid, rmpnav/geometry.py:215-255) ------------------------ */
+/* values: nx*ny*nz C-order (z fastest), dtype RMPB_F32/RMPB_F64, host memory.
+ * STORE_AUTO keeps f32 iff every value is exactly f32-representable (so the
+ * trace stays bit-identical to the f64 reference); STORE_F32 on values that
+ * are not f32-exact fails with RMPB_ERR_INVALID.  BRICK layout allocates
+ * only 8^3 bricks containing a value != `fill` (see rmpb_grid_create_brick). */
+RMPB_EXPORT int rmpb_grid_create(const void* values, int dtype, int64_t nx, int64_t ny, int64_t nz,
+                     double ox, double oy, double oz, double res,
+                     int storage, int layout, int device, rmpb_grid** out);
+/* Same, values already in device memory (e.g. a torch tensor) on `device`. */
+RMPB_EXPORT int rmpb_grid_create_device(const void* d_values, int dtype, int64_t nx, int64_t ny, int64_t nz,
+                            double ox, double oy, double oz, double res,
+                            int storage, int layout, int device, rmpb_grid** out);
+/* Block-hashed (BRICK) map: bricks whose 8^3 nodes all equal `fill` (the
+ * TSDF truncation value for unobserved space) are not stored. */
+RMPB_EXPORT int rmpb_grid_create_brick(const void* values, int dtype, int64_t nx, int64_t ny, int64_t nz,
+                           double ox, double oy, double oz, double res, double fill,
+                           int storage, int device, rmpb_grid** out);
+/* Re-upload values into an existing grid (same shape); invalidates caches. */
+RMPB_EXPORT int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype);
+RMPB_EXPORT int rmpb_grid_info(const rmpb_grid* g, int* storage, int* layout, int64_t* device_bytes,
+                   int64_t* allocated_bricks);
+RMPB_EXPORT int rmpb_grid_destroy(rmpb_grid* g);
+
+/* ---- ray bundles (RayBundle / sample_directions, rmpnav/rays.py:63-96) -- */
+RMPB_EXPORT int rmpb_bundle_create(const double* dirs, int64_t n, int order, int device, rmpb_bundle** out);
+/* Halton bundle generated on device: i = 1..n, polar = acos(1-2 h2), az = 2 pi h3. */
+RMPB_EXPORT int rmpb_bundle_halton(int64_t n, int order, int device, rmpb_bundle** out);
+RMPB_EXPORT int64_t rmpb_bundle_size(const rmpb_bundle* b);
+/* Directions back to host in ORIGINAL order (n x 3). */
+RMPB_EXPORT int rmpb_bundle_directions(const rmpb_bundle* b, double* out);
+RMPB_EXPORT int rmpb_bundle_destroy(rmpb_bundle* b);
+
+/* ---- fused map-based policy (K1/K3) ------------------------------------- */
+/* ray_policy (policies.py:182-192): trace + per-ray policy + reduce + pinv in
+ * one launch.  eps / step_scale as rays.py:117-120 (0.5*res, 0.9).  Optional
+ * per-ray outputs in ORIGINAL ray order: t (+inf = miss), hit cell (3 int32,
+ * -1 on miss), interpolation steps. */
+RMPB_EXPORT int rmpb_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, const double x[3], const double v[3],
+                    const double params[7], double max_range, double eps, double step_scale,
+                    double out_slot[13], double out_accel[3],
+                    double* opt_t, int32_t* opt_cell, int32_t* opt_steps, void* stream);
+/* P poses against one map and bundle (config C4); host buffers x, v: P x 3;
+ * out_slot: P x 13; out_accel: P x 3. */
+RMPB_EXPORT int rmpb_ray_policy_batch(const rmpb_grid* g, const rmpb_bundle* b, const double* x,
+                          const double* v, int64_t P, const double params[7], double max_range,
+                          double eps, double step_scale, double* out_slot, double* out_accel,
+                          void* stream);
+/* Same with device pointers; asynchronous.  opt_step_total (device u64, may
+ * be NULL) accumulates the number of voxel-steps executed. */
+RMPB_EXPORT int rmpb_ray_policy_batch_device(const rmpb_grid* g, const rmpb_bundle* b, const double* d_x,
+                                 const double* d_v, int64_t P, const double params[7],
+                                 double max_range, double eps, double step_scale, double* d_slot,
+                                 double* d_accel, uint64_t* opt_step_total, void* stream);
+/* Partial slot of stored rays [ray_begin, ray_end) of one pose (no pinv):
+ * the per-GPU share of a ray-split pose (config C5).  Device pointers. */
+RMPB_EXPORT int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bundle* b, const double* d_x,
+                                 const double* d_v, int64_t ray_begin, int64_t ray_end,
+                                 const double params[7], double max_range, double eps,
+                                 double step_scale, double* d_slot, void* stream);
+/* Fixed-order pairwise fold (rmpnav/_kernels/_pool.py:61-72 shape) of n
+ * 13-slots + pinv.  Device pointers (n <= 64). */
+RMPB_EXPORT int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double* d_slot, double* d_accel,
+                             void* stream);
+
+/* ---- LiDAR-direct policy (K2; policies.py:195-205) ----------------------- */
+/* dirs: n x 3 sensor-frame directions (world when R == NULL); R: 3x3
+ * row-major sensor orientation (world = dirs @ R^T, rays.py:172-173);
+ * valid: n bytes or NULL; min_range default 0.3 (policies.py:39). */
+RMPB_EXPORT int rmpb_lidar_policy(const double* dirs, const double* R, const double* ranges,
+                      const uint8_t* valid, int64_t n, const double v[3], const double params[7],
+                      double min_range, double out_slot[13], double out_accel[3], void* stream);
+/* Same with the sensor lattice kept on device as a bundle (IDENTITY order). */
+RMPB_EXPORT int rmpb_lidar_policy_bundle(const rmpb_bundle* pattern, const double* R, const double* ranges,
+                             const uint8_t* valid, const double v[3], const double params[7],
+                             double min_range, double out_slot[13], double out_accel[3],
+                             void* stream);
+/* S scans per launch, device pointers: dirs n x 3 (shared), R S x 9 (or
+ * NULL), ranges S x n, valid S x n (or NULL), v S x 3. */
+RMPB_EXPORT int rmpb_lidar_policy_batch_device(const double* d_dirs, const double* d_R, const double* d_ranges,
+                                   const uint8_t* d_valid, int64_t n, int64_t S, const double* d_v,
+                                   const double params[7], double min_range, double* d_slot,
+                                   double* d_accel, void* stream);
+/* Raw sensor-frame points (f32 xyz, S x n x 3): dir = p/|p|, range = |p|;
+ * zero or non-finite points are invalid. */
+RMPB_EXPORT int rmpb_lidar_points(const float* xyz, const double* R, int64_t n, const double v[3],
+                      const double params[7], double min_range, double out_slot[13],
+                      double out_accel[3], void* stream);
+RMPB_EXPORT int rmpb_lidar_points_batch_device(const float* d_xyz, const double* d_R, int64_t n, int64_t S,
+                                   const double* d_v, const double params[7], double min_range,
+                                   double* d_slot, double* d_accel, void* stream);
+
+/* ---- unfused protocol entries (parity) ---------------------------------- */
+RMPB_EXPORT int rmpb_grid_trace(const rmpb_grid* g, const double* dirs, int64_t n, const double start[3],
+                    double max_range, double eps, double step_scale, double* out_t,
+                    int32_t* out_cell, int32_t* out_steps, void* stream);
+RMPB_EXPORT int rmpb_policy_reduce(const double* dirs, const double* dists, int64_t n, const double v[3],
+                       const double params[7], double min_range, double out_slot[13],
+                       void* stream);
+/* n symmetric 3x3 matrices (row-major) -> their PSD pseudo-inverses. */
+RMPB_EXPORT int rmpb_pinv_psd(const double* a, int64_t n, double* out, void* stream);
+
+/* ---- analytic scene + map construction (rows f2-f4) --------------------- */
+/* Scene pack as rmpnav/geometry.py:177-197: kinds (0 sphere, 1 box), ops
+ * (0 union, 1 subtract), centers/sizes/velocities P x 3, empty distance. */
+RMPB_EXPORT int rmpb_scene_create(const int8_t* kinds, const int8_t* ops, const double* centers,
+                      const double* sizes, const double* velocities, int64_t n, double empty,
+                      int device, rmpb_scene** out);
+RMPB_EXPORT int rmpb_scene_destroy(rmpb_scene* s);
+RMPB_EXPORT int rmpb_scene_distance(const rmpb_scene* s, const double* pts, int64_t n, double t, double* out,
+                        void* stream);
+RMPB_EXPORT int rmpb_scene_trace(const rmpb_scene* s, const double start[3], const double* dirs, int64_t n,
+                     double max_range, double eps, double t, double step_scale, double* out,
+                     void* stream);
+/* bake_values (_ckern.pyx:71-87) into a host f64 array nx*ny*nz. */
+RMPB_EXPORT int rmpb_bake(const rmpb_scene* s, double ox, double oy, double oz, double res, int64_t nx,
+              int64_t ny, int64_t nz, double* out_values, void* stream);
+/* Bake straight into a device grid; storage RMPB_STORE_F32 ROUNDS to f32. */
+RMPB_EXPORT int rmpb_bake_grid(const rmpb_scene* s, double ox, double oy, double oz, double res, int64_t nx,
+                   int64_t ny, int64_t nz, int storage, int layout, int device, rmpb_grid** out);
+RMPB_EXPORT int rmpb_esdf_sample(const rmpb_grid* g, const double* pts, int64_t n, double* out_d,
+                     double* out_g, uint8_t* out_flag, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* RMPB_H */

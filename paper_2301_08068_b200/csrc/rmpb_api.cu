@@ -1,0 +1,1267 @@
+// rmpb_api.cu -- the C ABI (include/rmpb.h) over the sm_100a kernels.
+//
+// Handles own device memory; per-(device, stream) workspaces hold scratch
+// buffers and pinned/mapped host staging so host-buffer calls need no
+// allocation on the hot path.  Compiled with -fmad=false (see Makefile).
+#include <cuda_runtime.h>
+#include <cub/device/device_radix_sort.cuh>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "../../include/rmpb.h"
+#include "rmpb_aux.cuh"
+#include "rmpb_kernels.cuh"
+
+using namespace rmpb;
+
+// ---------------------------------------------------------------------------
+// errors
+
+static thread_local std::string g_err;
+static std::atomic<uint64_t> g_launches{0};
+static std::atomic<int64_t> g_opt_seg_rays{0};
+
+static int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return fail(e_ == cudaErrorMemoryAllocation ? RMPB_ERR_NOMEM : RMPB_ERR_CUDA,   \
+                  "%s: %s (%s:%d)", #call, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+
+#define CKL()                                                                        \
+  do {                                                                               \
+    g_launches.fetch_add(1, std::memory_order_relaxed);                              \
+    cudaError_t e_ = cudaGetLastError();                                             \
+    if (e_ != cudaSuccess)                                                           \
+      return fail(RMPB_ERR_CUDA, "kernel launch: %s (%s:%d)", cudaGetErrorString(e_), \
+                  __FILE__, __LINE__);                                               \
+  } while (0)
+
+#define TRY(expr)          \
+  do {                     \
+    int r_ = (expr);       \
+    if (r_ != RMPB_OK) return r_; \
+  } while (0)
+
+struct DeviceGuard {
+  int prev = -1;
+  bool ok = true;
+  cudaError_t err = cudaSuccess;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+    if (prev != dev) {
+      err = cudaSetDevice(dev);
+      ok = err == cudaSuccess;
+    }
+  }
+  ~DeviceGuard() {
+    int cur;
+    if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+static int current_device(int* dev) {
+  CK(cudaGetDevice(dev));
+  return RMPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// workspaces: one per (device, stream), grown on demand, never shrunk.
+
+struct DevBuf {
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return RMPB_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 256 ? 256 : bytes + bytes / 4;
+    CK(cudaMalloc(&p, want));
+    cap = want;
+    return RMPB_OK;
+  }
+};
+
+struct HostBuf {  // pinned + mapped (device-visible under UVA)
+  void* p = nullptr;
+  size_t cap = 0;
+  int ensure(size_t bytes) {
+    if (bytes <= cap) return RMPB_OK;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    cap = 0;
+    size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
+    CK(cudaHostAlloc(&p, want, cudaHostAllocMapped | cudaHostAllocPortable));
+    cap = want;
+    return RMPB_OK;
+  }
+};
+
+struct Workspace {
+  std::mutex mu;
+  DevBuf in, in2, in3, out, out2, out3, partials;
+  DevBuf tickets;  // zeroed on growth
+  size_t tickets_n = 0;
+  HostBuf hres;    // mapped small results (slots / accels)
+  int ensure_tickets(size_t n) {
+    if (n <= tickets_n) return RMPB_OK;
+    TRY(tickets.ensure(n * sizeof(unsigned)));
+    CK(cudaMemset(tickets.p, 0, tickets.cap));
+    tickets_n = tickets.cap / sizeof(unsigned);
+    return RMPB_OK;
+  }
+};
+
+static std::mutex g_ws_mu;
+static std::map<std::pair<int, void*>, std::unique_ptr<Workspace>> g_ws;
+
+static Workspace* workspace(int dev, void* stream) {
+  std::lock_guard<std::mutex> lk(g_ws_mu);
+  auto& w = g_ws[{dev, stream}];
+  if (!w) w.reset(new Workspace());
+  return w.get();
+}
+
+// ---------------------------------------------------------------------------
+// handles
+
+struct rmpb_grid {
+  int device;
+  int64_t nx, ny, nz;
+  GridGeom geom;
+  int storage;  // RMPB_STORE_F32 / RMPB_STORE_F64
+  int layout;   // LAYOUT_*
+  void* d_values = nullptr;  // linear / quad array or brick pool
+  int32_t* d_table = nullptr;
+  int bnx = 0, bny = 0, bnz = 0;
+  double fill = 0.0;
+  int64_t bricks = 0;
+  int64_t bytes = 0;
+};
+
+struct rmpb_bundle {
+  int device;
+  int64_t n;
+  int order;
+  double* d_dx = nullptr;  // stored order, SoA
+  double* d_dy = nullptr;
+  double* d_dz = nullptr;
+  int* d_perm = nullptr;   // stored -> original (null when identity)
+  double* d_aos = nullptr; // original order AoS (for LiDAR use / download)
+};
+
+struct rmpb_scene {
+  int device;
+  int64_t n;
+  double empty;
+  void* d_mem = nullptr;
+  ScenePack pack;
+};
+
+template <class F>
+static int with_grid(const rmpb_grid* g, F&& f) {
+  const GridGeom& G = g->geom;
+  if (g->layout == LAYOUT_LINEAR) {
+    if (g->storage == RMPB_STORE_F32) {
+      LinearGrid<float> a{(const float*)g->d_values, G.nz, G.ny * G.nz};
+      return f(a);
+    }
+    LinearGrid<double> a{(const double*)g->d_values, G.nz, G.ny * G.nz};
+    return f(a);
+  }
+  if (g->layout == LAYOUT_QUAD) {
+    if (g->storage == RMPB_STORE_F32) {
+      QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1)};
+      return f(a);
+    }
+    QuadGridF64 a{(const double2*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1)};
+    return f(a);
+  }
+  if (g->storage == RMPB_STORE_F32) {
+    BrickGrid<float> a{(const float*)g->d_values, g->d_table, g->bny, g->bnz, (float)g->fill};
+    return f(a);
+  }
+  BrickGrid<double> a{(const double*)g->d_values, g->d_table, g->bny, g->bnz, g->fill};
+  return f(a);
+}
+
+static inline int grid_blocks(long long n, int threads = 256) {
+  long long b = (n + threads - 1) / threads;
+  if (b > 148LL * 64) b = 148LL * 64;
+  return (int)(b < 1 ? 1 : b);
+}
+
+static PolicyParams make_params(const double p[7], double min_range) {
+  PolicyParams q;
+  q.eta_rep = p[0]; q.nu_rep = p[1]; q.eta_damp = p[2]; q.nu_damp = p[3];
+  q.eps_p = p[4]; q.radius = p[5]; q.c = p[6]; q.min_range = min_range;
+  return q;
+}
+
+static int check_params(const double* p) {
+  if (!p) return fail(RMPB_ERR_INVALID, "params is NULL");
+  for (int i = 0; i < 7; ++i)
+    if (!(p[i] == p[i])) return fail(RMPB_ERR_INVALID, "params[%d] is NaN", i);
+  return RMPB_OK;
+}
+
+// Segmentation of a pose's rays over CTAs.  Small launches (single pose):
+// one 256-ray segment per CTA for latency; large batches: whole poses per
+// CTA (no cross-CTA fold, no partial traffic).
+static void choose_segments(int64_t P, int64_t n, int* segs, int* seg_rays) {
+  int64_t sr = g_opt_seg_rays.load();
+  if (sr <= 0) {
+    const int64_t target_units = 148LL * 8 * 2;
+    sr = kBlock;
+    while (sr < n && P * ((n + sr * 2 - 1) / (sr * 2)) >= target_units) sr *= 2;
+  }
+  if (sr % kBlock) sr = (sr / kBlock + 1) * kBlock;
+  if (sr > n) sr = ((n + kBlock - 1) / kBlock) * kBlock;
+  if (sr < kBlock) sr = kBlock;
+  *seg_rays = (int)sr;
+  *segs = (int)((n + sr - 1) / sr);
+  if (*segs < 1) *segs = 1;
+}
+
+// ---------------------------------------------------------------------------
+// library
+
+extern "C" const char* rmpb_last_error(void) { return g_err.c_str(); }
+extern "C" int rmpb_api_version(void) { return RMPB_API_VERSION; }
+extern "C" uint64_t rmpb_launch_count(void) { return g_launches.load(); }
+
+extern "C" int rmpb_device_count(int* n) {
+  if (!n) return fail(RMPB_ERR_INVALID, "n is NULL");
+  CK(cudaGetDeviceCount(n));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_set_option(const char* name, int64_t value) {
+  if (!name) return fail(RMPB_ERR_INVALID, "name is NULL");
+  if (!strcmp(name, "seg_rays")) {
+    g_opt_seg_rays.store(value);
+    return RMPB_OK;
+  }
+  return fail(RMPB_ERR_INVALID, "unknown option '%s'", name);
+}
+
+// ---------------------------------------------------------------------------
+// grids
+
+static int grid_check_dims(int64_t nx, int64_t ny, int64_t nz, double res) {
+  if (nx < 2 || ny < 2 || nz < 2)
+    return fail(RMPB_ERR_INVALID, "grid needs at least 2 nodes per axis");
+  if (!(res > 0.0)) return fail(RMPB_ERR_INVALID, "resolution must be positive");
+  if (nx * ny * nz >= (1LL << 31) || nx >= (1 << 30) || ny >= (1 << 30) || nz >= (1 << 30))
+    return fail(RMPB_ERR_INVALID, "grid of %lld nodes exceeds 2^31", (long long)(nx * ny * nz));
+  return RMPB_OK;
+}
+
+// Builds the device representation from f64/f32 values already on device
+// (d_src, dtype).  Consumes nothing; caller frees d_src.
+static int grid_build(rmpb_grid* g, const void* d_src, int dtype, int storage, int layout,
+                      cudaStream_t st) {
+  const long long n = g->nx * g->ny * g->nz;
+  // resolve storage
+  int store = storage;
+  if (dtype == RMPB_F32) {
+    store = (storage == RMPB_STORE_F64) ? RMPB_STORE_F64 : RMPB_STORE_F32;
+  } else if (storage != RMPB_STORE_F64) {
+    int* d_bad;
+    int bad = 0;
+    CK(cudaMallocAsync((void**)&d_bad, sizeof(int), st));
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    k_check_f32<<<grid_blocks(n), 256, 0, st>>>(n, (const double*)d_src, d_bad);
+    CKL();
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d_bad, st));
+    CK(cudaStreamSynchronize(st));
+    if (bad && storage == RMPB_STORE_F32)
+      return fail(RMPB_ERR_INVALID,
+                  "STORE_F32 requested but values are not exactly representable in f32");
+    store = bad ? RMPB_STORE_F64 : RMPB_STORE_F32;
+  }
+  g->storage = store;
+  const size_t esz = store == RMPB_STORE_F32 ? 4 : 8;
+  // linear copy in the storage dtype
+  void* lin = nullptr;
+  CK(cudaMalloc(&lin, n * esz));
+  if (store == RMPB_STORE_F32 && dtype == RMPB_F64) {
+    k_to_f32<<<grid_blocks(n), 256, 0, st>>>(n, (const double*)d_src, (float*)lin);
+    CKL();
+  } else if (store == RMPB_STORE_F64 && dtype == RMPB_F32) {
+    return fail(RMPB_ERR_UNSUPPORTED, "f32 input with f64 storage is not supported");
+  } else {
+    CK(cudaMemcpyAsync(lin, d_src, n * esz, cudaMemcpyDeviceToDevice, st));
+  }
+  if (layout == LAYOUT_LINEAR) {
+    g->d_values = lin;
+    g->bytes = n * esz;
+  } else if (layout == LAYOUT_QUAD) {
+    long long nq = g->nx * (g->ny - 1) * (g->nz - 1);
+    void* q = nullptr;
+    CK(cudaMalloc(&q, nq * 4 * esz));
+    if (store == RMPB_STORE_F32)
+      k_build_quad<float, float4><<<grid_blocks(nq), 256, 0, st>>>(
+          (int)g->nx, (int)g->ny, (int)g->nz, (const float*)lin, (float4*)q);
+    else
+      k_build_quad<double, double2><<<grid_blocks(nq), 256, 0, st>>>(
+          (int)g->nx, (int)g->ny, (int)g->nz, (const double*)lin, (double2*)q);
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    cudaFree(lin);
+    g->d_values = q;
+    g->bytes = nq * 4 * esz;
+  } else {
+    return fail(RMPB_ERR_INVALID, "unknown layout %d", layout);
+  }
+  g->layout = layout;
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+static int grid_new(const void* values, bool on_device, int dtype, int64_t nx, int64_t ny,
+                    int64_t nz, double ox, double oy, double oz, double res, int storage,
+                    int layout, int device, rmpb_grid** out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!values) return fail(RMPB_ERR_INVALID, "values is NULL");
+  if (dtype != RMPB_F32 && dtype != RMPB_F64) return fail(RMPB_ERR_INVALID, "bad dtype %d", dtype);
+  TRY(grid_check_dims(nx, ny, nz, res));
+  if (layout == RMPB_LAYOUT_AUTO) layout = LAYOUT_QUAD;
+  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD)
+    return fail(RMPB_ERR_INVALID, "layout %d not valid here (use rmpb_grid_create_brick)", layout);
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
+  std::unique_ptr<rmpb_grid> g(new rmpb_grid());
+  g->device = device;
+  g->nx = nx; g->ny = ny; g->nz = nz;
+  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  const size_t bytes = (size_t)(nx * ny * nz) * (dtype == RMPB_F32 ? 4 : 8);
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  const void* src = values;
+  void* tmp = nullptr;
+  int rc = RMPB_OK;
+  if (!on_device) {
+    if (cudaMalloc(&tmp, bytes) != cudaSuccess) {
+      cudaStreamDestroy(st);
+      return fail(RMPB_ERR_NOMEM, "cudaMalloc(%zu) for grid upload failed", bytes);
+    }
+    cudaMemcpyAsync(tmp, values, bytes, cudaMemcpyHostToDevice, st);
+    src = tmp;
+  }
+  rc = grid_build(g.get(), src, dtype, storage, layout, st);
+  cudaStreamSynchronize(st);
+  if (tmp) cudaFree(tmp);
+  cudaStreamDestroy(st);
+  if (rc != RMPB_OK) return rc;
+  *out = g.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_grid_create(const void* values, int dtype, int64_t nx, int64_t ny, int64_t nz,
+                                double ox, double oy, double oz, double res, int storage,
+                                int layout, int device, rmpb_grid** out) {
+  return grid_new(values, false, dtype, nx, ny, nz, ox, oy, oz, res, storage, layout, device, out);
+}
+
+extern "C" int rmpb_grid_create_device(const void* d_values, int dtype, int64_t nx, int64_t ny,
+                                       int64_t nz, double ox, double oy, double oz, double res,
+                                       int storage, int layout, int device, rmpb_grid** out) {
+  return grid_new(d_values, true, dtype, nx, ny, nz, ox, oy, oz, res, storage, layout, device, out);
+}
+
+extern "C" int rmpb_grid_create_brick(const void* values, int dtype, int64_t nx, int64_t ny,
+                                      int64_t nz, double ox, double oy, double oz, double res,
+                                      double fill, int storage, int device, rmpb_grid** out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (!values) return fail(RMPB_ERR_INVALID, "values is NULL");
+  if (dtype != RMPB_F32 && dtype != RMPB_F64) return fail(RMPB_ERR_INVALID, "bad dtype %d", dtype);
+  TRY(grid_check_dims(nx, ny, nz, res));
+  // Brick construction happens on the host side of the API (a one-off map
+  // ingestion step, like the reference's ESDF load, geometry.py:472-488):
+  // scan bricks, allocate the non-uniform ones, upload pool + table.
+  const int B = 8;
+  const int bnx = (int)((nx + B - 1) / B), bny = (int)((ny + B - 1) / B), bnz = (int)((nz + B - 1) / B);
+  const bool f32in = dtype == RMPB_F32;
+  auto val = [&](int64_t i, int64_t j, int64_t k) -> double {
+    int64_t idx = (i * ny + j) * nz + k;
+    return f32in ? (double)((const float*)values)[idx] : ((const double*)values)[idx];
+  };
+  // storage resolution
+  int store = storage;
+  if (f32in) store = RMPB_STORE_F32;
+  else if (storage != RMPB_STORE_F64) {
+    bool exact = (double)(float)fill == fill;
+    const double* v = (const double*)values;
+    for (int64_t i = 0; exact && i < nx * ny * nz; ++i) exact = ((double)(float)v[i] == v[i]) || v[i] != v[i];
+    if (!exact && storage == RMPB_STORE_F32)
+      return fail(RMPB_ERR_INVALID, "STORE_F32 requested but values are not f32-exact");
+    store = exact ? RMPB_STORE_F32 : RMPB_STORE_F64;
+  }
+  std::vector<int32_t> table((size_t)bnx * bny * bnz, -1);
+  int64_t nb = 0;
+  for (int bi = 0; bi < bnx; ++bi)
+    for (int bj = 0; bj < bny; ++bj)
+      for (int bk = 0; bk < bnz; ++bk) {
+        bool uniform = true;
+        for (int li = 0; li < B && uniform; ++li)
+          for (int lj = 0; lj < B && uniform; ++lj)
+            for (int lk = 0; lk < B && uniform; ++lk) {
+              int64_t i = bi * B + li, j = bj * B + lj, k = bk * B + lk;
+              if (i >= nx || j >= ny || k >= nz) continue;
+              if (!(val(i, j, k) == fill)) uniform = false;
+            }
+        if (!uniform) table[((size_t)bi * bny + bj) * bnz + bk] = (int32_t)nb++;
+      }
+  const size_t esz = store == RMPB_STORE_F32 ? 4 : 8;
+  std::vector<unsigned char> pool((size_t)(nb > 0 ? nb : 1) * 512 * esz);
+  for (int bi = 0; bi < bnx; ++bi)
+    for (int bj = 0; bj < bny; ++bj)
+      for (int bk = 0; bk < bnz; ++bk) {
+        int32_t s = table[((size_t)bi * bny + bj) * bnz + bk];
+        if (s < 0) continue;
+        for (int li = 0; li < B; ++li)
+          for (int lj = 0; lj < B; ++lj)
+            for (int lk = 0; lk < B; ++lk) {
+              int64_t i = bi * B + li, j = bj * B + lj, k = bk * B + lk;
+              double x = (i < nx && j < ny && k < nz) ? val(i, j, k) : fill;
+              size_t o = (size_t)s * 512 + (li << 6 | lj << 3 | lk);
+              if (store == RMPB_STORE_F32) ((float*)pool.data())[o] = (float)x;
+              else ((double*)pool.data())[o] = x;
+            }
+      }
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
+  std::unique_ptr<rmpb_grid> g(new rmpb_grid());
+  g->device = device;
+  g->nx = nx; g->ny = ny; g->nz = nz;
+  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  g->storage = store;
+  g->layout = LAYOUT_BRICK;
+  g->bnx = bnx; g->bny = bny; g->bnz = bnz;
+  g->fill = fill;
+  g->bricks = nb;
+  CK(cudaMalloc(&g->d_values, pool.size()));
+  CK(cudaMemcpy(g->d_values, pool.data(), pool.size(), cudaMemcpyHostToDevice));
+  CK(cudaMalloc((void**)&g->d_table, table.size() * sizeof(int32_t)));
+  CK(cudaMemcpy(g->d_table, table.data(), table.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
+  g->bytes = (int64_t)(pool.size() + table.size() * sizeof(int32_t));
+  *out = g.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype) {
+  if (!g || !values) return fail(RMPB_ERR_INVALID, "NULL argument");
+  if (g->layout == LAYOUT_BRICK)
+    return fail(RMPB_ERR_UNSUPPORTED, "update of a BRICK grid: recreate it");
+  rmpb_grid* fresh = nullptr;
+  TRY(grid_new(values, false, dtype, g->nx, g->ny, g->nz, g->geom.ox, g->geom.oy, g->geom.oz,
+               g->geom.res, RMPB_STORE_AUTO, g->layout, g->device, &fresh));
+  DeviceGuard dg(g->device);
+  cudaFree(g->d_values);
+  g->d_values = fresh->d_values;
+  g->storage = fresh->storage;
+  g->bytes = fresh->bytes;
+  fresh->d_values = nullptr;
+  delete fresh;
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_grid_info(const rmpb_grid* g, int* storage, int* layout, int64_t* bytes,
+                              int64_t* bricks) {
+  if (!g) return fail(RMPB_ERR_INVALID, "grid is NULL");
+  if (storage) *storage = g->storage;
+  if (layout) *layout = g->layout;
+  if (bytes) *bytes = g->bytes;
+  if (bricks) *bricks = g->bricks;
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_grid_destroy(rmpb_grid* g) {
+  if (!g) return RMPB_OK;
+  DeviceGuard dg(g->device);
+  if (g->d_values) cudaFree(g->d_values);
+  if (g->d_table) cudaFree(g->d_table);
+  delete g;
+  return RMPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// bundles
+
+static int bundle_finish(rmpb_bundle* b, cudaStream_t st) {
+  // b->d_aos holds ORIGINAL-order AoS directions on device.
+  const int n = (int)b->n;
+  CK(cudaMalloc((void**)&b->d_dx, n * sizeof(double)));
+  CK(cudaMalloc((void**)&b->d_dy, n * sizeof(double)));
+  CK(cudaMalloc((void**)&b->d_dz, n * sizeof(double)));
+  if (b->order == RMPB_ORDER_MORTON) {
+    unsigned *k_in, *k_out;
+    int* i_in;
+    CK(cudaMalloc((void**)&k_in, n * sizeof(unsigned)));
+    CK(cudaMalloc((void**)&k_out, n * sizeof(unsigned)));
+    CK(cudaMalloc((void**)&i_in, n * sizeof(int)));
+    CK(cudaMalloc((void**)&b->d_perm, n * sizeof(int)));
+    k_morton_keys<<<grid_blocks(n), 256, 0, st>>>(n, b->d_aos, k_in, i_in);
+    CKL();
+    size_t tmp_bytes = 0;
+    CK(cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, k_in, k_out, i_in, b->d_perm, n, 0, 32, st));
+    void* tmp;
+    CK(cudaMalloc(&tmp, tmp_bytes));
+    CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, i_in, b->d_perm, n, 0, 32, st));
+    g_launches.fetch_add(1);
+    CK(cudaStreamSynchronize(st));
+    cudaFree(tmp); cudaFree(k_in); cudaFree(k_out); cudaFree(i_in);
+  }
+  k_gather_dirs<<<grid_blocks(n), 256, 0, st>>>(n, b->d_aos, b->d_perm, b->d_dx, b->d_dy, b->d_dz);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+static int bundle_new(const double* dirs, int64_t n, int order, int device, bool halton,
+                      rmpb_bundle** out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n < 1) return fail(RMPB_ERR_INVALID, "need at least one direction");
+  if (n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many directions");
+  if (!halton && !dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
+  if (order != RMPB_ORDER_IDENTITY && order != RMPB_ORDER_MORTON)
+    return fail(RMPB_ERR_INVALID, "bad order %d", order);
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
+  std::unique_ptr<rmpb_bundle> b(new rmpb_bundle());
+  b->device = device;
+  b->n = n;
+  b->order = order;
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  int rc = RMPB_OK;
+  if (cudaMalloc((void**)&b->d_aos, n * 3 * sizeof(double)) != cudaSuccess) {
+    cudaStreamDestroy(st);
+    return fail(RMPB_ERR_NOMEM, "bundle alloc failed");
+  }
+  if (halton) {
+    double *x, *y, *z;
+    cudaMalloc((void**)&x, n * sizeof(double));
+    cudaMalloc((void**)&y, n * sizeof(double));
+    cudaMalloc((void**)&z, n * sizeof(double));
+    k_halton<<<grid_blocks(n), 256, 0, st>>>((int)n, x, y, z);
+    g_launches.fetch_add(1);
+    k_soa_to_aos<<<grid_blocks(n), 256, 0, st>>>((int)n, x, y, z, b->d_aos);
+    g_launches.fetch_add(1);
+    cudaStreamSynchronize(st);
+    cudaFree(x); cudaFree(y); cudaFree(z);
+  } else {
+    cudaMemcpyAsync(b->d_aos, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st);
+  }
+  cudaError_t e = cudaStreamSynchronize(st);
+  if (e != cudaSuccess) rc = fail(RMPB_ERR_CUDA, "bundle setup: %s", cudaGetErrorString(e));
+  if (rc == RMPB_OK) rc = bundle_finish(b.get(), st);
+  cudaStreamDestroy(st);
+  if (rc != RMPB_OK) {
+    rmpb_bundle* p = b.release();
+    cudaFree(p->d_aos); cudaFree(p->d_dx); cudaFree(p->d_dy); cudaFree(p->d_dz); cudaFree(p->d_perm);
+    delete p;
+    return rc;
+  }
+  *out = b.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_bundle_create(const double* dirs, int64_t n, int order, int device,
+                                  rmpb_bundle** out) {
+  return bundle_new(dirs, n, order, device, false, out);
+}
+
+extern "C" int rmpb_bundle_halton(int64_t n, int order, int device, rmpb_bundle** out) {
+  return bundle_new(nullptr, n, order, device, true, out);
+}
+
+extern "C" int64_t rmpb_bundle_size(const rmpb_bundle* b) { return b ? b->n : -1; }
+
+extern "C" int rmpb_bundle_directions(const rmpb_bundle* b, double* out) {
+  if (!b || !out) return fail(RMPB_ERR_INVALID, "NULL argument");
+  DeviceGuard dg(b->device);
+  CK(cudaMemcpy(out, b->d_aos, b->n * 3 * sizeof(double), cudaMemcpyDeviceToHost));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_bundle_destroy(rmpb_bundle* b) {
+  if (!b) return RMPB_OK;
+  DeviceGuard dg(b->device);
+  cudaFree(b->d_aos); cudaFree(b->d_dx); cudaFree(b->d_dy); cudaFree(b->d_dz);
+  if (b->d_perm) cudaFree(b->d_perm);
+  delete b;
+  return RMPB_OK;
+}
+
+static Bundle bundle_view(const rmpb_bundle* b) {
+  Bundle v;
+  v.dx = b->d_dx; v.dy = b->d_dy; v.dz = b->d_dz; v.perm = b->d_perm; v.n = (int)b->n;
+  return v;
+}
+
+// ---------------------------------------------------------------------------
+// fused ray policy
+
+static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io, int64_t P,
+                             const PolicyParams& pp, double max_range, double eps,
+                             double step_scale, int segs, int seg_rays, RayOut ro,
+                             cudaStream_t st) {
+  Bundle bv = bundle_view(b);
+  const long long units = (long long)P * segs;
+  if (units >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many CTA units");
+  return with_grid(g, [&](auto acc) -> int {
+    k_ray_policy<<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
+                                                     step_scale, segs, seg_rays, ro);
+    CKL();
+    return RMPB_OK;
+  });
+}
+
+static int check_gb(const rmpb_grid* g, const rmpb_bundle* b) {
+  if (!g) return fail(RMPB_ERR_INVALID, "grid is NULL");
+  if (!b) return fail(RMPB_ERR_INVALID, "bundle is NULL");
+  if (g->device != b->device)
+    return fail(RMPB_ERR_INVALID, "grid (device %d) and bundle (device %d) differ", g->device,
+                b->device);
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, const double x[3],
+                               const double v[3], const double params[7], double max_range,
+                               double eps, double step_scale, double out_slot[13],
+                               double out_accel[3], double* opt_t, int32_t* opt_cell,
+                               int32_t* opt_steps, void* stream) {
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (!x || !v || !out_slot) return fail(RMPB_ERR_INVALID, "NULL x / v / out_slot");
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  const int64_t n = b->n;
+  int segs, seg_rays;
+  choose_segments(1, n, &segs, &seg_rays);
+  TRY(ws->hres.ensure(16 * sizeof(double)));
+  TRY(ws->partials.ensure((size_t)segs * kAcc * sizeof(double)));
+  TRY(ws->ensure_tickets(1));
+  double* h = (double*)ws->hres.p;
+  PoseIO io{};
+  io.x = nullptr; io.v = nullptr;
+  for (int k = 0; k < 3; ++k) { io.x0[k] = x[k]; io.v0[k] = v[k]; }
+  io.slot = h;
+  io.accel = h + 13;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  io.seg_out = nullptr;
+  RayOut ro{};
+  if (opt_t || opt_cell || opt_steps) {
+    TRY(ws->out.ensure(n * sizeof(double)));
+    TRY(ws->out2.ensure(n * 3 * sizeof(int32_t)));
+    TRY(ws->out3.ensure(n * sizeof(int32_t)));
+    ro.t = (double*)ws->out.p;
+    ro.cell = (int*)ws->out2.p;
+    ro.steps = (int*)ws->out3.p;
+  }
+  TRY(launch_ray_policy(g, b, io, 1, make_params(params, 0.0), max_range, eps, step_scale, segs,
+                        seg_rays, ro, st));
+  if (opt_t) CK(cudaMemcpyAsync(opt_t, ro.t, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (opt_cell)
+    CK(cudaMemcpyAsync(opt_cell, ro.cell, n * 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (opt_steps)
+    CK(cudaMemcpyAsync(opt_steps, ro.steps, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(out_slot, h, 13 * sizeof(double));
+  if (out_accel) memcpy(out_accel, h + 13, 3 * sizeof(double));
+  return RMPB_OK;
+}
+
+static int ray_policy_batch_impl(const rmpb_grid* g, const rmpb_bundle* b, const double* d_x,
+                                 const double* d_v, int64_t P, const double params[7],
+                                 double max_range, double eps, double step_scale, double* d_slot,
+                                 double* d_accel, uint64_t* step_total, Workspace* ws,
+                                 cudaStream_t st) {
+  int segs, seg_rays;
+  choose_segments(P, b->n, &segs, &seg_rays);
+  if (segs > 1) {
+    TRY(ws->partials.ensure((size_t)P * segs * kAcc * sizeof(double)));
+    TRY(ws->ensure_tickets((size_t)P));
+  }
+  PoseIO io{};
+  io.x = d_x; io.v = d_v; io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  RayOut ro{};
+  ro.step_total = (unsigned long long*)step_total;
+  return launch_ray_policy(g, b, io, P, make_params(params, 0.0), max_range, eps, step_scale, segs,
+                           seg_rays, ro, st);
+}
+
+extern "C" int rmpb_ray_policy_batch_device(const rmpb_grid* g, const rmpb_bundle* b,
+                                            const double* d_x, const double* d_v, int64_t P,
+                                            const double params[7], double max_range, double eps,
+                                            double step_scale, double* d_slot, double* d_accel,
+                                            uint64_t* opt_step_total, void* stream) {
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (P < 1) return fail(RMPB_ERR_INVALID, "P must be >= 1");
+  if (!d_x || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  return ray_policy_batch_impl(g, b, d_x, d_v, P, params, max_range, eps, step_scale, d_slot,
+                               d_accel, opt_step_total, ws, S(stream));
+}
+
+extern "C" int rmpb_ray_policy_batch(const rmpb_grid* g, const rmpb_bundle* b, const double* x,
+                                     const double* v, int64_t P, const double params[7],
+                                     double max_range, double eps, double step_scale,
+                                     double* out_slot, double* out_accel, void* stream) {
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (P < 1) return fail(RMPB_ERR_INVALID, "P must be >= 1");
+  if (!x || !v || !out_slot) return fail(RMPB_ERR_INVALID, "NULL x / v / out_slot");
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(P * 6 * sizeof(double)));
+  TRY(ws->out.ensure(P * 16 * sizeof(double)));
+  double* dx = (double*)ws->in.p;
+  double* dv = dx + 3 * P;
+  double* ds = (double*)ws->out.p;
+  double* da = ds + 13 * P;
+  CK(cudaMemcpyAsync(dx, x, P * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dv, v, P * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  TRY(ray_policy_batch_impl(g, b, dx, dv, P, params, max_range, eps, step_scale, ds,
+                            out_accel ? da : nullptr, nullptr, ws, st));
+  CK(cudaMemcpyAsync(out_slot, ds, P * 13 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out_accel) CK(cudaMemcpyAsync(out_accel, da, P * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bundle* b,
+                                            const double* d_x, const double* d_v,
+                                            int64_t ray_begin, int64_t ray_end,
+                                            const double params[7], double max_range, double eps,
+                                            double step_scale, double* d_slot, void* stream) {
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (!d_x || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
+  if (ray_begin < 0 || ray_end > b->n || ray_begin > ray_end)
+    return fail(RMPB_ERR_INVALID, "bad ray range [%lld, %lld) of %lld", (long long)ray_begin,
+                (long long)ray_end, (long long)b->n);
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  // A view of the bundle restricted to the range; one pose, no pinv.
+  rmpb_bundle sub = *b;
+  sub.d_dx = b->d_dx + ray_begin;
+  sub.d_dy = b->d_dy + ray_begin;
+  sub.d_dz = b->d_dz + ray_begin;
+  sub.d_perm = nullptr;
+  sub.n = ray_end - ray_begin;
+  if (sub.n == 0) {
+    CK(cudaMemsetAsync(d_slot, 0, 13 * sizeof(double), st));
+    return RMPB_OK;
+  }
+  int segs, seg_rays;
+  choose_segments(1, sub.n, &segs, &seg_rays);
+  TRY(ws->partials.ensure((size_t)segs * kAcc * sizeof(double)));
+  TRY(ws->ensure_tickets(1));
+  PoseIO io{};
+  io.x = d_x; io.v = d_v; io.slot = d_slot; io.accel = nullptr;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  RayOut ro{};
+  return launch_ray_policy(g, &sub, io, 1, make_params(params, 0.0), max_range, eps, step_scale,
+                           segs, seg_rays, ro, st);
+}
+
+extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double* d_slot,
+                                        double* d_accel, void* stream) {
+  if (!d_slots || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
+  if (n < 1 || n > 64) return fail(RMPB_ERR_INVALID, "fold of %lld slots (1..64)", (long long)n);
+  k_fold_resolve<<<1, 32, 0, S(stream)>>>(d_slots, (int)n, d_slot, d_accel);
+  CKL();
+  return RMPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// LiDAR
+
+static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
+                        const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
+                        cudaStream_t st) {
+  int segs, seg_rays;
+  choose_segments(S_, sc.n, &segs, &seg_rays);
+  if (segs > 1) {
+    TRY(ws->partials.ensure((size_t)S_ * segs * kAcc * sizeof(double)));
+    TRY(ws->ensure_tickets((size_t)S_));
+  }
+  PoseIO io{};
+  io.x = nullptr; io.v = d_v;
+  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
+  io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  const long long units = (long long)S_ * segs;
+  k_lidar_policy<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
+  CKL();
+  return RMPB_OK;
+}
+
+static int lidar_host(const double* d_dirs_or_null, const double* dirs, const double* R,
+                      const double* ranges, const uint8_t* valid, int64_t n, const double v[3],
+                      const double params[7], double min_range, double out_slot[13],
+                      double out_accel[3], void* stream, int device) {
+  TRY(check_params(params));
+  if (!ranges || !v || !out_slot) return fail(RMPB_ERR_INVALID, "NULL ranges / v / out_slot");
+  if (n < 0 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad beam count");
+  DeviceGuard dg(device);
+  Workspace* ws = workspace(device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->hres.ensure(16 * sizeof(double)));
+  double* h = (double*)ws->hres.p;
+  if (n == 0) {
+    memset(out_slot, 0, 13 * sizeof(double));
+    if (out_accel) memset(out_accel, 0, 3 * sizeof(double));
+    return RMPB_OK;
+  }
+  // staging: dirs (if not resident) | ranges | R | valid
+  size_t off_r = d_dirs_or_null ? 0 : (size_t)n * 3 * sizeof(double);
+  size_t off_R = off_r + (size_t)n * sizeof(double);
+  size_t off_v = off_R + 9 * sizeof(double);
+  size_t total = off_v + (valid ? (size_t)n : 0);
+  TRY(ws->in.ensure(total));
+  char* d = (char*)ws->in.p;
+  if (!d_dirs_or_null) {
+    if (!dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
+    CK(cudaMemcpyAsync(d, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  }
+  CK(cudaMemcpyAsync(d + off_r, ranges, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (R) CK(cudaMemcpyAsync(d + off_R, R, 9 * sizeof(double), cudaMemcpyHostToDevice, st));
+  if (valid) CK(cudaMemcpyAsync(d + off_v, valid, n, cudaMemcpyHostToDevice, st));
+  ScanIO sc;
+  sc.dirs = d_dirs_or_null ? d_dirs_or_null : (const double*)d;
+  sc.R = R ? (const double*)(d + off_R) : nullptr;
+  sc.ranges = (const double*)(d + off_r);
+  sc.valid = valid ? (const unsigned char*)(d + off_v) : nullptr;
+  sc.n = (int)n;
+  double v0[3] = {v[0], v[1], v[2]};
+  TRY(lidar_launch(sc, 1, nullptr, v0, make_params(params, min_range), h, h + 13, ws, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(out_slot, h, 13 * sizeof(double));
+  if (out_accel) memcpy(out_accel, h + 13, 3 * sizeof(double));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_lidar_policy(const double* dirs, const double* R, const double* ranges,
+                                 const uint8_t* valid, int64_t n, const double v[3],
+                                 const double params[7], double min_range, double out_slot[13],
+                                 double out_accel[3], void* stream) {
+  int dev;
+  TRY(current_device(&dev));
+  return lidar_host(nullptr, dirs, R, ranges, valid, n, v, params, min_range, out_slot, out_accel,
+                    stream, dev);
+}
+
+extern "C" int rmpb_lidar_policy_bundle(const rmpb_bundle* pattern, const double* R,
+                                        const double* ranges, const uint8_t* valid,
+                                        const double v[3], const double params[7],
+                                        double min_range, double out_slot[13],
+                                        double out_accel[3], void* stream) {
+  if (!pattern) return fail(RMPB_ERR_INVALID, "pattern is NULL");
+  return lidar_host(pattern->d_aos, nullptr, R, ranges, valid, pattern->n, v, params, min_range,
+                    out_slot, out_accel, stream, pattern->device);
+}
+
+extern "C" int rmpb_lidar_policy_batch_device(const double* d_dirs, const double* d_R,
+                                              const double* d_ranges, const uint8_t* d_valid,
+                                              int64_t n, int64_t S_, const double* d_v,
+                                              const double params[7], double min_range,
+                                              double* d_slot, double* d_accel, void* stream) {
+  TRY(check_params(params));
+  if (!d_dirs || !d_ranges || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
+  if (n < 1 || n >= (1LL << 31) || S_ < 1) return fail(RMPB_ERR_INVALID, "bad n / S");
+  int dev;
+  TRY(current_device(&dev));
+  Workspace* ws = workspace(dev, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  ScanIO sc{d_dirs, d_R, d_ranges, d_valid, (int)n};
+  return lidar_launch(sc, S_, d_v, nullptr, make_params(params, min_range), d_slot, d_accel, ws,
+                      S(stream));
+}
+
+static int points_launch(PointsIO pt, int64_t S_, const double* d_v, double v0[3],
+                         const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
+                         cudaStream_t st) {
+  int segs, seg_rays;
+  choose_segments(S_, pt.n, &segs, &seg_rays);
+  if (segs > 1) {
+    TRY(ws->partials.ensure((size_t)S_ * segs * kAcc * sizeof(double)));
+    TRY(ws->ensure_tickets((size_t)S_));
+  }
+  PoseIO io{};
+  io.x = nullptr; io.v = d_v;
+  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
+  io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  k_lidar_points<<<(unsigned)(S_ * segs), kBlock, 0, st>>>(pt, io, pp, segs, seg_rays);
+  CKL();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_lidar_points(const float* xyz, const double* R, int64_t n, const double v[3],
+                                 const double params[7], double min_range, double out_slot[13],
+                                 double out_accel[3], void* stream) {
+  TRY(check_params(params));
+  if (!xyz || !v || !out_slot) return fail(RMPB_ERR_INVALID, "NULL xyz / v / out_slot");
+  if (n < 1 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad point count");
+  int dev;
+  TRY(current_device(&dev));
+  Workspace* ws = workspace(dev, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->hres.ensure(16 * sizeof(double)));
+  TRY(ws->in.ensure(n * 3 * sizeof(float) + 16 * sizeof(double)));
+  char* d = (char*)ws->in.p;
+  double* dR = (double*)(d + ((n * 3 * sizeof(float) + 15) / 16) * 16);
+  CK(cudaMemcpyAsync(d, xyz, n * 3 * sizeof(float), cudaMemcpyHostToDevice, st));
+  if (R) CK(cudaMemcpyAsync(dR, R, 9 * sizeof(double), cudaMemcpyHostToDevice, st));
+  PointsIO pt{(const float*)d, R ? dR : nullptr, (int)n};
+  double* h = (double*)ws->hres.p;
+  double v0[3] = {v[0], v[1], v[2]};
+  TRY(points_launch(pt, 1, nullptr, v0, make_params(params, min_range), h, h + 13, ws, st));
+  CK(cudaStreamSynchronize(st));
+  memcpy(out_slot, h, 13 * sizeof(double));
+  if (out_accel) memcpy(out_accel, h + 13, 3 * sizeof(double));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_lidar_points_batch_device(const float* d_xyz, const double* d_R, int64_t n,
+                                              int64_t S_, const double* d_v,
+                                              const double params[7], double min_range,
+                                              double* d_slot, double* d_accel, void* stream) {
+  TRY(check_params(params));
+  if (!d_xyz || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
+  if (n < 1 || n >= (1LL << 31) || S_ < 1) return fail(RMPB_ERR_INVALID, "bad n / S");
+  int dev;
+  TRY(current_device(&dev));
+  Workspace* ws = workspace(dev, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  PointsIO pt{d_xyz, d_R, (int)n};
+  return points_launch(pt, S_, d_v, nullptr, make_params(params, min_range), d_slot, d_accel, ws,
+                       S(stream));
+}
+
+// ---------------------------------------------------------------------------
+// unfused protocol entries
+
+extern "C" int rmpb_grid_trace(const rmpb_grid* g, const double* dirs, int64_t n,
+                               const double start[3], double max_range, double eps,
+                               double step_scale, double* out_t, int32_t* out_cell,
+                               int32_t* out_steps, void* stream) {
+  if (!g || !start || !out_t) return fail(RMPB_ERR_INVALID, "NULL grid / start / out_t");
+  if (n < 0 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad ray count");
+  if (n == 0) return RMPB_OK;
+  if (!dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(n * 3 * sizeof(double)));
+  TRY(ws->out.ensure(n * sizeof(double)));
+  TRY(ws->out2.ensure(n * 3 * sizeof(int32_t)));
+  TRY(ws->out3.ensure(n * sizeof(int32_t)));
+  CK(cudaMemcpyAsync(ws->in.p, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  RayOut ro{};
+  ro.t = (double*)ws->out.p;
+  ro.cell = out_cell ? (int*)ws->out2.p : nullptr;
+  ro.steps = out_steps ? (int*)ws->out3.p : nullptr;
+  TRY(with_grid(g, [&](auto acc) -> int {
+    k_grid_trace<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, st>>>(
+        acc, g->geom, (const double*)ws->in.p, (int)n, start[0], start[1], start[2], max_range,
+        eps, step_scale, ro);
+    CKL();
+    return RMPB_OK;
+  }));
+  CK(cudaMemcpyAsync(out_t, ro.t, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  if (out_cell) CK(cudaMemcpyAsync(out_cell, ro.cell, n * 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (out_steps) CK(cudaMemcpyAsync(out_steps, ro.steps, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_policy_reduce(const double* dirs, const double* dists, int64_t n,
+                                  const double v[3], const double params[7], double min_range,
+                                  double out_slot[13], void* stream) {
+  TRY(check_params(params));
+  if (!v || !out_slot) return fail(RMPB_ERR_INVALID, "NULL v / out_slot");
+  if (n < 0 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad ray count");
+  if (n == 0) {
+    memset(out_slot, 0, 13 * sizeof(double));
+    return RMPB_OK;
+  }
+  if (!dirs || !dists) return fail(RMPB_ERR_INVALID, "NULL dirs / dists");
+  int dev;
+  TRY(current_device(&dev));
+  Workspace* ws = workspace(dev, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(n * 4 * sizeof(double)));
+  TRY(ws->hres.ensure(16 * sizeof(double)));
+  double* d = (double*)ws->in.p;
+  CK(cudaMemcpyAsync(d, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d + 3 * n, dists, n * sizeof(double), cudaMemcpyHostToDevice, st));
+  int segs, seg_rays;
+  choose_segments(1, n, &segs, &seg_rays);
+  TRY(ws->partials.ensure((size_t)segs * kAcc * sizeof(double)));
+  TRY(ws->ensure_tickets(1));
+  double* h = (double*)ws->hres.p;
+  PoseIO io{};
+  for (int k = 0; k < 3; ++k) io.v0[k] = v[k];
+  io.slot = h; io.accel = nullptr;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  k_policy_reduce<<<segs, kBlock, 0, st>>>(d, d + 3 * n, (int)n, io, make_params(params, min_range),
+                                           segs, seg_rays);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+  memcpy(out_slot, h, 13 * sizeof(double));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_pinv_psd(const double* a, int64_t n, double* out, void* stream) {
+  if (!a || !out) return fail(RMPB_ERR_INVALID, "NULL a / out");
+  if (n < 1) return RMPB_OK;
+  int dev;
+  TRY(current_device(&dev));
+  Workspace* ws = workspace(dev, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(n * 9 * sizeof(double)));
+  TRY(ws->out.ensure(n * 9 * sizeof(double)));
+  CK(cudaMemcpyAsync(ws->in.p, a, n * 9 * sizeof(double), cudaMemcpyHostToDevice, st));
+  k_pinv_psd<<<(unsigned)((n + 127) / 128), 128, 0, st>>>((const double*)ws->in.p, (int)n,
+                                                         (double*)ws->out.p);
+  CKL();
+  CK(cudaMemcpyAsync(out, ws->out.p, n * 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// scenes
+
+extern "C" int rmpb_scene_create(const int8_t* kinds, const int8_t* ops, const double* centers,
+                                 const double* sizes, const double* velocities, int64_t n,
+                                 double empty, int device, rmpb_scene** out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (n < 0 || n > (1 << 24)) return fail(RMPB_ERR_INVALID, "bad primitive count");
+  if (n > 0 && (!kinds || !ops || !centers || !sizes || !velocities))
+    return fail(RMPB_ERR_INVALID, "NULL scene array");
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
+  std::unique_ptr<rmpb_scene> s(new rmpb_scene());
+  s->device = device;
+  s->n = n;
+  s->empty = empty;
+  size_t nn = (size_t)(n > 0 ? n : 1);
+  size_t bytes = nn * 9 * sizeof(double) + 2 * ((nn + 15) / 16) * 16;
+  CK(cudaMalloc(&s->d_mem, bytes));
+  char* p = (char*)s->d_mem;
+  double* c = (double*)p;
+  double* z = c + 3 * nn;
+  double* v = z + 3 * nn;
+  signed char* k = (signed char*)(v + 3 * nn);
+  signed char* o = k + ((nn + 15) / 16) * 16;
+  if (n > 0) {
+    CK(cudaMemcpy(c, centers, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(z, sizes, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(v, velocities, n * 3 * sizeof(double), cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(k, kinds, n, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(o, ops, n, cudaMemcpyHostToDevice));
+  }
+  s->pack = ScenePack{k, o, c, z, v, (int)n, empty};
+  *out = s.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_scene_destroy(rmpb_scene* s) {
+  if (!s) return RMPB_OK;
+  DeviceGuard dg(s->device);
+  cudaFree(s->d_mem);
+  delete s;
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_scene_distance(const rmpb_scene* s, const double* pts, int64_t n, double t,
+                                   double* out, void* stream) {
+  if (!s || !out) return fail(RMPB_ERR_INVALID, "NULL scene / out");
+  if (n < 0 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad point count");
+  if (n == 0) return RMPB_OK;
+  if (!pts) return fail(RMPB_ERR_INVALID, "pts is NULL");
+  DeviceGuard dg(s->device);
+  Workspace* ws = workspace(s->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(n * 3 * sizeof(double)));
+  TRY(ws->out.ensure(n * sizeof(double)));
+  CK(cudaMemcpyAsync(ws->in.p, pts, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  k_scene_distance<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(s->pack, t, (const double*)ws->in.p,
+                                                                (int)n, (double*)ws->out.p);
+  CKL();
+  CK(cudaMemcpyAsync(out, ws->out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_scene_trace(const rmpb_scene* s, const double start[3], const double* dirs,
+                                int64_t n, double max_range, double eps, double t,
+                                double step_scale, double* out, void* stream) {
+  if (!s || !start || !out) return fail(RMPB_ERR_INVALID, "NULL scene / start / out");
+  if (n < 0 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad ray count");
+  if (n == 0) return RMPB_OK;
+  if (!dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
+  DeviceGuard dg(s->device);
+  Workspace* ws = workspace(s->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(n * 3 * sizeof(double)));
+  TRY(ws->out.ensure(n * sizeof(double)));
+  CK(cudaMemcpyAsync(ws->in.p, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  k_scene_trace<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+      s->pack, t, start[0], start[1], start[2], (const double*)ws->in.p, (int)n, max_range, eps,
+      step_scale, (double*)ws->out.p);
+  CKL();
+  CK(cudaMemcpyAsync(out, ws->out.p, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_bake(const rmpb_scene* s, double ox, double oy, double oz, double res,
+                         int64_t nx, int64_t ny, int64_t nz, double* out_values, void* stream) {
+  if (!s || !out_values) return fail(RMPB_ERR_INVALID, "NULL scene / out");
+  if (nx < 1 || ny < 1 || nz < 1) return fail(RMPB_ERR_INVALID, "bad dims");
+  const long long n = nx * ny * nz;
+  DeviceGuard dg(s->device);
+  cudaStream_t st = S(stream);
+  double* d;
+  CK(cudaMallocAsync((void**)&d, n * sizeof(double), st));
+  k_bake<double><<<grid_blocks(n), 256, 0, st>>>(s->pack, ox, oy, oz, res, (int)nx, (int)ny, (int)nz, d);
+  CKL();
+  CK(cudaMemcpyAsync(out_values, d, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaFreeAsync(d, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_bake_grid(const rmpb_scene* s, double ox, double oy, double oz, double res,
+                              int64_t nx, int64_t ny, int64_t nz, int storage, int layout,
+                              int device, rmpb_grid** out) {
+  if (!s || !out) return fail(RMPB_ERR_INVALID, "NULL scene / out");
+  *out = nullptr;
+  TRY(grid_check_dims(nx, ny, nz, res));
+  if (layout == RMPB_LAYOUT_AUTO) layout = LAYOUT_QUAD;
+  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD)
+    return fail(RMPB_ERR_INVALID, "bake_grid supports LINEAR / QUAD layouts");
+  if (device != s->device) return fail(RMPB_ERR_INVALID, "scene lives on device %d", s->device);
+  const long long n = nx * ny * nz;
+  DeviceGuard dg(device);
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::unique_ptr<rmpb_grid> g(new rmpb_grid());
+  g->device = device;
+  g->nx = nx; g->ny = ny; g->nz = nz;
+  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  void* tmp = nullptr;
+  int rc = RMPB_OK;
+  if (storage == RMPB_STORE_F32) {
+    // bake in f64, round once to f32 (the reference's ESDF file precision,
+    // geometry.py:466), then build the layout from f32 values.
+    if (cudaMalloc(&tmp, n * sizeof(float)) != cudaSuccess) rc = fail(RMPB_ERR_NOMEM, "bake alloc");
+    if (rc == RMPB_OK) {
+      k_bake<float><<<grid_blocks(n), 256, 0, st>>>(s->pack, ox, oy, oz, res, (int)nx, (int)ny,
+                                                    (int)nz, (float*)tmp);
+      g_launches.fetch_add(1);
+      rc = grid_build(g.get(), tmp, RMPB_F32, RMPB_STORE_F32, layout, st);
+    }
+  } else {
+    if (cudaMalloc(&tmp, n * sizeof(double)) != cudaSuccess) rc = fail(RMPB_ERR_NOMEM, "bake alloc");
+    if (rc == RMPB_OK) {
+      k_bake<double><<<grid_blocks(n), 256, 0, st>>>(s->pack, ox, oy, oz, res, (int)nx, (int)ny,
+                                                     (int)nz, (double*)tmp);
+      g_launches.fetch_add(1);
+      rc = grid_build(g.get(), tmp, RMPB_F64, storage, layout, st);
+    }
+  }
+  cudaStreamSynchronize(st);
+  if (tmp) cudaFree(tmp);
+  cudaStreamDestroy(st);
+  if (rc != RMPB_OK) return rc;
+  *out = g.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_esdf_sample(const rmpb_grid* g, const double* pts, int64_t n, double* out_d,
+                                double* out_g, uint8_t* out_flag, void* stream) {
+  if (!g || !out_d || !out_g || !out_flag) return fail(RMPB_ERR_INVALID, "NULL argument");
+  if (n < 0 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad point count");
+  if (n == 0) return RMPB_OK;
+  if (!pts) return fail(RMPB_ERR_INVALID, "pts is NULL");
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(n * 3 * sizeof(double)));
+  TRY(ws->out.ensure(n * 4 * sizeof(double) + n));
+  double* od = (double*)ws->out.p;
+  double* og = od + n;
+  unsigned char* of = (unsigned char*)(og + 3 * n);
+  CK(cudaMemcpyAsync(ws->in.p, pts, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  TRY(with_grid(g, [&](auto acc) -> int {
+    k_esdf_sample<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(acc, g->geom, (const double*)ws->in.p,
+                                                               (int)n, od, og, of);
+    CKL();
+    return RMPB_OK;
+  }));
+  CK(cudaMemcpyAsync(out_d, od, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out_g, og, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out_flag, of, n, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}

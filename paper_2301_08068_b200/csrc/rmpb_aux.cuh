@@ -1,0 +1,234 @@
+// rmpb_aux.cuh -- kernels around the hot path: device ray generation (Halton
+// bundle, rays.py:43-96), bundle reordering keys, map layout builders (QUAD,
+// BRICK), the analytic scene SDF / bake / scene trace (rows f2, f3;
+// _ckern.pyx:21-87, 251-273) and the ESDF single-lookup sample (row f4;
+// _ckern.pyx:138-166).  Same exactness rules as rmpb_device.cuh.
+#pragma once
+#include "rmpb_device.cuh"
+
+namespace rmpb {
+
+// Radical inverse with the reference's exact arithmetic (rays.py:43-51):
+// out += f * (i % b); i //= b; f /= b   (all fp64, left to right).
+__device__ __forceinline__ double radical_inverse(long long i, int base) {
+  double out = 0.0, f = 1.0 / (double)base;
+  while (i > 0) {
+    out += f * (double)(i % base);
+    i /= base;
+    f /= (double)base;
+  }
+  return out;
+}
+
+// Halton bundle, i = 1..N (rays.py:78-86):
+//   polar = arccos(1 - 2 h2), az = 2*pi*h3, dir = (sp cos az, sp sin az, cos polar)
+// Writes SoA directions in ORIGINAL order plus a reorder key per ray.
+__global__ void k_halton(int n, double* __restrict__ dx, double* __restrict__ dy,
+                         double* __restrict__ dz) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  long long idx = (long long)i + 1;
+  double h2 = radical_inverse(idx, 2), h3 = radical_inverse(idx, 3);
+  double polar = acos(1.0 - 2.0 * h2);
+  double az = (2.0 * CUDART_PI) * h3;
+  double sp = sin(polar);
+  dx[i] = sp * cos(az);
+  dy[i] = sp * sin(az);
+  dz[i] = cos(polar);
+}
+
+__device__ __forceinline__ unsigned part1by1(unsigned x) {
+  x &= 0x0000ffffu;
+  x = (x | (x << 8)) & 0x00ff00ffu;
+  x = (x | (x << 4)) & 0x0f0f0f0fu;
+  x = (x | (x << 2)) & 0x33333333u;
+  x = (x | (x << 1)) & 0x55555555u;
+  return x;
+}
+
+// Morton(polar, azimuth) key of each direction: rays adjacent in the key are
+// adjacent on the sphere, so a warp's 32 rays march through similar space
+// (SIMT efficiency).  Only the ORDER of evaluation
+// changes; t / mask / cell per ray are unaffected.
+__global__ void k_morton_keys(int n, const double* __restrict__ dirs_aos, unsigned* __restrict__ key,
+                              int* __restrict__ idx) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double x = dirs_aos[3 * i], y = dirs_aos[3 * i + 1], z = dirs_aos[3 * i + 2];
+  double c = fmin(fmax(z, -1.0), 1.0);
+  double pol = acos(c) * (1.0 / CUDART_PI);           // [0,1]
+  double az = atan2(y, x);
+  if (az < 0.0) az += 2.0 * CUDART_PI;
+  az *= 1.0 / (2.0 * CUDART_PI);                      // [0,1)
+  unsigned qp = (unsigned)fmin(pol * 65536.0, 65535.0);
+  unsigned qa = (unsigned)fmin(az * 65536.0, 65535.0);
+  if (!(pol == pol) || !(az == az)) qp = qa = 0;
+  key[i] = (part1by1(qp) << 1) | part1by1(qa);
+  idx[i] = i;
+}
+
+__global__ void k_gather_dirs(int n, const double* __restrict__ dirs_aos, const int* __restrict__ perm,
+                              double* __restrict__ dx, double* __restrict__ dy,
+                              double* __restrict__ dz) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  int o = perm ? perm[i] : i;
+  dx[i] = dirs_aos[3 * o];
+  dy[i] = dirs_aos[3 * o + 1];
+  dz[i] = dirs_aos[3 * o + 2];
+}
+
+__global__ void k_soa_to_aos(int n, const double* __restrict__ dx, const double* __restrict__ dy,
+                             const double* __restrict__ dz, double* __restrict__ aos) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  aos[3 * i] = dx[i];
+  aos[3 * i + 1] = dy[i];
+  aos[3 * i + 2] = dz[i];
+}
+
+// f64 -> f32 (exactness was checked by k_check_f32).
+__global__ void k_to_f32(long long n, const double* __restrict__ src, float* __restrict__ dst) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) dst[i] = (float)src[i];
+}
+
+// Flags any value that does not survive a round trip through f32.
+__global__ void k_check_f32(long long n, const double* __restrict__ src, int* __restrict__ bad) {
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  int b = 0;
+  for (; i < n; i += stride) {
+    double v = src[i];
+    double r = (double)(float)v;
+    if (!(r == v) && !(v != v)) b = 1;   // NaN stays NaN in f32
+  }
+  if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
+}
+
+// QUAD layout builder: quad[(i*(ny-1)+j)*(nz-1)+k] = {v[i,j,k], v[i,j,k+1], v[i,j+1,k], v[i,j+1,k+1]}.
+template <typename T, typename Q>
+__global__ void k_build_quad(int nx, int ny, int nz, const T* __restrict__ v, Q* __restrict__ q) {
+  long long n = (long long)nx * (ny - 1) * (nz - 1);
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    int k = (int)(i % (nz - 1));
+    long long r = i / (nz - 1);
+    int j = (int)(r % (ny - 1));
+    int ii = (int)(r / (ny - 1));
+    const T* b = v + ((long long)ii * ny + j) * nz + k;
+    T* o = reinterpret_cast<T*>(q) + 4 * i;
+    o[0] = b[0]; o[1] = b[1]; o[2] = b[nz]; o[3] = b[nz + 1];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Analytic scene (geometry.py:177-197 pack; _ckern.pyx:21-56 distance).
+struct ScenePack {
+  const signed char* kinds;
+  const signed char* ops;
+  const double* centers;  // [P][3]
+  const double* sizes;    // [P][3]
+  const double* vels;     // [P][3]
+  int n;
+  double empty;
+};
+
+__device__ __forceinline__ double scene_sd(const ScenePack& s, double t, double px, double py,
+                                           double pz) {
+  double d = s.empty;
+  for (int i = 0; i < s.n; ++i) {
+    double dx = px - (s.centers[3 * i] + s.vels[3 * i] * t);
+    double dy = py - (s.centers[3 * i + 1] + s.vels[3 * i + 1] * t);
+    double dz = pz - (s.centers[3 * i + 2] + s.vels[3 * i + 2] * t);
+    double dp;
+    if (s.kinds[i] == 0) {
+      dp = sqrt(dx * dx + dy * dy + dz * dz) - s.sizes[3 * i];
+    } else {
+      double qx = fabs(dx) - s.sizes[3 * i];
+      double qy = fabs(dy) - s.sizes[3 * i + 1];
+      double qz = fabs(dz) - s.sizes[3 * i + 2];
+      double ex = qx > 0.0 ? qx : 0.0, ey = qy > 0.0 ? qy : 0.0, ez = qz > 0.0 ? qz : 0.0;
+      double mx = qx;
+      if (qy > mx) mx = qy;
+      if (qz > mx) mx = qz;
+      dp = sqrt(ex * ex + ey * ey + ez * ez) + (mx < 0.0 ? mx : 0.0);
+    }
+    if (s.ops[i] == 0) { if (dp < d) d = dp; }
+    else { if (-dp > d) d = -dp; }
+  }
+  return d;
+}
+
+__global__ void k_scene_distance(ScenePack s, double t, const double* __restrict__ pts, int n,
+                                  double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  out[i] = scene_sd(s, t, pts[3 * i], pts[3 * i + 1], pts[3 * i + 2]);
+}
+
+// bake (_ckern.pyx:71-87): node (ix,iy,iz) at (ox + res*ix, ...), t = 0.
+template <typename T>
+__global__ void k_bake(ScenePack s, double ox, double oy, double oz, double res, int nx, int ny,
+                       int nz, T* __restrict__ out) {
+  long long n = (long long)nx * ny * nz;
+  long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    int iz = (int)(i % nz);
+    long long r = i / nz;
+    int iy = (int)(r % ny);
+    int ix = (int)(r / ny);
+    double px = ox + res * (double)ix, py = oy + res * (double)iy, pz = oz + res * (double)iz;
+    out[i] = (T)scene_sd(s, 0.0, px, py, pz);
+  }
+}
+
+// scene_trace (_ckern.pyx:251-273): from t = 0, no box clip.
+__global__ void k_scene_trace(ScenePack s, double tm, double sx, double sy, double sz,
+                              const double* __restrict__ dirs, int n, double max_range, double eps,
+                              double step_scale, double* __restrict__ out) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double dx = dirs[3 * i], dy = dirs[3 * i + 1], dz = dirs[3 * i + 2];
+  double t = 0.0, r = CUDART_INF;
+  while (true) {
+    double d = scene_sd(s, tm, sx + t * dx, sy + t * dy, sz + t * dz);
+    if (d < eps) { r = t; break; }
+    t += step_scale * d;
+    if (t > max_range) break;
+  }
+  out[i] = r;
+}
+
+// esdf_sample (_ckern.pyx:138-166): distance, normalised central-difference
+// gradient, out-of-domain flag.
+template <class G>
+__global__ void k_esdf_sample(G grid, GridGeom g, const double* __restrict__ pts, int n,
+                              double* __restrict__ out_d, double* __restrict__ out_g,
+                              unsigned char* __restrict__ out_flag) {
+  int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  double px = pts[3 * i], py = pts[3 * i + 1], pz = pts[3 * i + 2];
+  double ux = (px - g.ox) / g.res, uy = (py - g.oy) / g.res, uz = (pz - g.oz) / g.res;
+  out_flag[i] = (ux < 0.0 || ux > g.mx || uy < 0.0 || uy > g.my || uz < 0.0 || uz > g.mz);
+  int a, b, c;
+  out_d[i] = interp(grid, g, px, py, pz, a, b, c);
+  double r = g.res;
+  double gx = (interp(grid, g, px + r, py, pz, a, b, c) - interp(grid, g, px - r, py, pz, a, b, c)) /
+              (2.0 * r);
+  double gy = (interp(grid, g, px, py + r, pz, a, b, c) - interp(grid, g, px, py - r, pz, a, b, c)) /
+              (2.0 * r);
+  double gz = (interp(grid, g, px, py, pz + r, a, b, c) - interp(grid, g, px, py, pz - r, a, b, c)) /
+              (2.0 * r);
+  double nrm = sqrt(gx * gx + gy * gy + gz * gz);
+  if (nrm < 1e-9) {
+    out_g[3 * i] = 0.0; out_g[3 * i + 1] = 0.0; out_g[3 * i + 2] = 0.0;
+  } else {
+    out_g[3 * i] = gx / nrm; out_g[3 * i + 1] = gy / nrm; out_g[3 * i + 2] = gz / nrm;
+  }
+}
+
+}  // namespace rmpb

@@ -1,0 +1,376 @@
+// rmpb_device.cuh -- device-side building blocks of the raycasting-RMP path.
+//
+// Everything in the EXACT path is IEEE fp64 in the reference's operation
+// order and this translation unit family is compiled
+// with `-fmad=false`, so every a*b+c stays a separate DMUL/DADD exactly as
+// the reference's scalar SSE2 build (no FMA) computes it.  Division is the
+// IEEE correctly-rounded `/`.  Reference anchors (relative to
+// /root/reference/pkg/src/rmpnav/):
+//   interp ........ _kernels/_ckern.pyx:92-135
+//   box_span ...... _kernels/_ckern.pyx:171-212
+//   sphere trace .. _kernels/_ckern.pyx:217-248, rays.py:99-124
+//   ray policy .... _kernels/_ckern.pyx:278-321, policies.py:175-205
+//   pinv_psd ...... core.py:103-115
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+namespace rmpb {
+
+constexpr int kBlock = 256;       // threads per CTA for the policy kernels
+constexpr int kWarps = kBlock / 32;
+constexpr int kAcc = 10;          // a00 a01 a02 a11 a12 a22 b0 b1 b2 cnt
+
+// ---------------------------------------------------------------------------
+// Grid storage.  Node (i,j,k) sits at origin + (i,j,k)*res (geometry.py:215-221).
+//   LINEAR: values[(i*ny + j)*nz + k]                      (reference layout)
+//   QUAD  : quad[(i*(ny-1) + j)*(nz-1) + k] = {v[i,j,k], v[i,j,k+1],
+//           v[i,j+1,k], v[i,j+1,k+1]}: the 4 z/y corners of a cell column as
+//           one 16-B (f32) vector, so one trace step is 2 vector loads
+//           (x-planes i and i+1) instead of 8 scalar gathers.
+//   BRICK : 8^3 bricks behind a dense brick-index table (block-hashed TSDF,
+//           unallocated bricks read as `fill`).
+// Values are copied verbatim (f32 storage only when every value is exactly
+// representable in f32), so all layouts interpolate bit-identically.
+enum Layout : int { LAYOUT_LINEAR = 0, LAYOUT_QUAD = 1, LAYOUT_BRICK = 2 };
+
+struct GridGeom {
+  int nx, ny, nz;
+  double ox, oy, oz, res;
+  double mx, my, mz;     // n - 1.0 (the clamp bounds)
+  double hx, hy, hz;     // origin + (n-1)*res (the slab bounds)
+};
+
+__host__ inline GridGeom make_geom(int64_t nx, int64_t ny, int64_t nz, double ox, double oy,
+                                   double oz, double res) {
+  GridGeom g;
+  g.nx = (int)nx; g.ny = (int)ny; g.nz = (int)nz;
+  g.ox = ox; g.oy = oy; g.oz = oz; g.res = res;
+  g.mx = (double)nx - 1.0; g.my = (double)ny - 1.0; g.mz = (double)nz - 1.0;
+  // rmpnav/_kernels/_ckern.pyx:224-226: ox + (nx - 1) * res
+  g.hx = ox + (double)(nx - 1) * res;
+  g.hy = oy + (double)(ny - 1) * res;
+  g.hz = oz + (double)(nz - 1) * res;
+  return g;
+}
+
+// 8 corner values of cell (ix,iy,iz), in the reference's naming v{x}{y}{z}.
+struct Corners { double v000, v001, v010, v011, v100, v101, v110, v111; };
+
+template <typename T>
+struct LinearGrid {
+  const T* __restrict__ v;
+  int sy, sx;  // strides: nz, ny*nz (node counts < 2^31 checked at create)
+  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    const T* b = v + ((int64_t)ix * sx + (int64_t)iy * sy + iz);
+    Corners c;
+    c.v000 = (double)__ldg(b);           c.v001 = (double)__ldg(b + 1);
+    c.v010 = (double)__ldg(b + sy);      c.v011 = (double)__ldg(b + sy + 1);
+    c.v100 = (double)__ldg(b + sx);      c.v101 = (double)__ldg(b + sx + 1);
+    c.v110 = (double)__ldg(b + sx + sy); c.v111 = (double)__ldg(b + sx + sy + 1);
+    return c;
+  }
+};
+
+struct QuadGridF32 {
+  const float4* __restrict__ q;
+  int qy, qx;  // strides in quads: (nz-1), (ny-1)*(nz-1)
+  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    const float4* b = q + ((int64_t)ix * qx + (int64_t)iy * qy + iz);
+    float4 a = __ldg(b), c = __ldg(b + qx);
+    Corners k;
+    k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
+    k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;
+    return k;
+  }
+};
+
+struct QuadGridF64 {
+  const double2* __restrict__ q;  // 2 double2 per quad
+  int qy, qx;
+  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    const double2* b = q + 2 * ((int64_t)ix * qx + (int64_t)iy * qy + iz);
+    const double2* c = b + 2 * (int64_t)qx;
+    double2 a0 = __ldg(b), a1 = __ldg(b + 1), c0 = __ldg(c), c1 = __ldg(c + 1);
+    Corners k;
+    k.v000 = a0.x; k.v001 = a0.y; k.v010 = a1.x; k.v011 = a1.y;
+    k.v100 = c0.x; k.v101 = c0.y; k.v110 = c1.x; k.v111 = c1.y;
+    return k;
+  }
+};
+
+// Block-hashed sparse grid: bricks of B^3 nodes; brick (bi,bj,bk) ->
+// table[(bi*bny + bj)*bnz + bk] = brick slot or -1 (unallocated -> fill).
+template <typename T>
+struct BrickGrid {
+  const T* __restrict__ pool;          // slot * B^3 + ((li*B)+lj)*B + lk
+  const int32_t* __restrict__ table;
+  int bny, bnz;
+  T fill;
+  static constexpr int B = 8;
+  __device__ __forceinline__ double at(int i, int j, int k) const {
+    int s = __ldg(table + ((i >> 3) * bny + (j >> 3)) * bnz + (k >> 3));
+    if (s < 0) return (double)fill;
+    return (double)__ldg(pool + (int64_t)s * 512 + (((i & 7) << 6) | ((j & 7) << 3) | (k & 7)));
+  }
+  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    Corners c;
+    c.v000 = at(ix, iy, iz);         c.v001 = at(ix, iy, iz + 1);
+    c.v010 = at(ix, iy + 1, iz);     c.v011 = at(ix, iy + 1, iz + 1);
+    c.v100 = at(ix + 1, iy, iz);     c.v101 = at(ix + 1, iy, iz + 1);
+    c.v110 = at(ix + 1, iy + 1, iz); c.v111 = at(ix + 1, iy + 1, iz + 1);
+    return c;
+  }
+};
+
+// ---------------------------------------------------------------------------
+// Exact interpolation (rmpnav/_kernels/_ckern.pyx:92-135).
+template <class G>
+__device__ __forceinline__ double interp(const G& grid, const GridGeom& g, double px, double py,
+                                         double pz, int& ix, int& iy, int& iz) {
+  double ux = (px - g.ox) / g.res;
+  double uy = (py - g.oy) / g.res;
+  double uz = (pz - g.oz) / g.res;
+  if (ux < 0.0) ux = 0.0; else if (ux > g.mx) ux = g.mx;
+  if (uy < 0.0) uy = 0.0; else if (uy > g.my) uy = g.my;
+  if (uz < 0.0) uz = 0.0; else if (uz > g.mz) uz = g.mz;
+  // (uint) makes a NaN coordinate (undefined in the reference) a safe index.
+  ix = (int)floor(ux); iy = (int)floor(uy); iz = (int)floor(uz);
+  ix = min(max(ix, 0), g.nx - 2);
+  iy = min(max(iy, 0), g.ny - 2);
+  iz = min(max(iz, 0), g.nz - 2);
+  double fx = ux - (double)ix, fy = uy - (double)iy, fz = uz - (double)iz;
+  Corners c = grid.load(ix, iy, iz);
+  double c00 = c.v000 + fz * (c.v001 - c.v000);
+  double c01 = c.v010 + fz * (c.v011 - c.v010);
+  double c10 = c.v100 + fz * (c.v101 - c.v100);
+  double c11 = c.v110 + fz * (c.v111 - c.v110);
+  double c0 = c00 + fy * (c01 - c00);
+  double c1 = c10 + fy * (c11 - c10);
+  return c0 + fx * (c1 - c0);
+}
+
+// Slab interval against the node domain (rmpnav/_kernels/_ckern.pyx:171-212).
+__device__ __forceinline__ bool box_span(const GridGeom& g, double sx, double sy, double sz,
+                                         double dx, double dy, double dz, double& t0, double& t1) {
+  double tlo = -CUDART_INF, thi = CUDART_INF, ta, tb, tmp;
+  if (dx != 0.0) {
+    ta = (g.ox - sx) / dx; tb = (g.hx - sx) / dx;
+    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
+    if (ta > tlo) tlo = ta;
+    if (tb < thi) thi = tb;
+  } else if (sx < g.ox || sx > g.hx) {
+    return false;
+  }
+  if (dy != 0.0) {
+    ta = (g.oy - sy) / dy; tb = (g.hy - sy) / dy;
+    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
+    if (ta > tlo) tlo = ta;
+    if (tb < thi) thi = tb;
+  } else if (sy < g.oy || sy > g.hy) {
+    return false;
+  }
+  if (dz != 0.0) {
+    ta = (g.oz - sz) / dz; tb = (g.hz - sz) / dz;
+    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
+    if (ta > tlo) tlo = ta;
+    if (tb < thi) thi = tb;
+  } else if (sz < g.oz || sz > g.hz) {
+    return false;
+  }
+  t0 = tlo; t1 = thi;
+  return true;
+}
+
+struct TraceResult {
+  double t;     // hit distance, +inf on miss
+  int cx, cy, cz;  // cell of the terminating interpolation (valid on hit)
+  int steps;    // interpolation calls ("voxel-steps")
+};
+
+// Sphere trace (rmpnav/_kernels/_ckern.pyx:217-248).
+template <class G>
+__device__ __forceinline__ TraceResult trace_ray(const G& grid, const GridGeom& g, double sx,
+                                                 double sy, double sz, double dx, double dy,
+                                                 double dz, double max_range, double eps,
+                                                 double step_scale) {
+  TraceResult r;
+  r.t = CUDART_INF; r.cx = r.cy = r.cz = -1; r.steps = 0;
+  double t0, t1;
+  if (!box_span(g, sx, sy, sz, dx, dy, dz, t0, t1)) return r;
+  double t = t0 > 0.0 ? t0 : 0.0;
+  double t_end = t1 < max_range ? t1 : max_range;
+  if (t > t_end) return r;
+  int ix, iy, iz;
+  while (true) {
+    double d = interp(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
+    ++r.steps;
+    if (d < eps) { r.t = t; r.cx = ix; r.cy = iy; r.cz = iz; break; }
+    t += step_scale * d;
+    if (t > t_end) break;
+  }
+  return r;
+}
+
+// ---------------------------------------------------------------------------
+// Per-ray obstacle policy (rmpnav/_kernels/_ckern.pyx:290-316).  `dir` is the
+// cast direction; r = -dir points away from the obstacle (policies.py:550-552).
+struct PolicyParams {
+  double eta_rep, nu_rep, eta_damp, nu_damp, eps_p, radius, c;  // as_tuple order, policies.py:80-83
+  double min_range;
+};
+
+struct Acc {
+  double a00, a01, a02, a11, a12, a22, b0, b1, b2;
+  int cnt;
+  __device__ __forceinline__ void zero() {
+    a00 = a01 = a02 = a11 = a12 = a22 = b0 = b1 = b2 = 0.0;
+    cnt = 0;
+  }
+};
+
+// Adds ray (dir, dist) to `acc`.  Rays with a == 0 add nothing but the count
+// (x + 0 == x exactly), so the transcendental work is only done where the
+// metric weight can be nonzero: d < radius AND toward > 0 (w == 0 or g == 0
+// give fdamp*... == 0 and a == (w*smag)*smag == 0 exactly).
+__device__ __forceinline__ void policy_accumulate(Acc& acc, double dx, double dy, double dz,
+                                                  double d, double vx, double vy, double vz,
+                                                  const PolicyParams& p) {
+  if (d != d || d == CUDART_INF || d < p.min_range) return;
+  acc.cnt += 1;
+  double toward = dx * vx + dy * vy + dz * vz;
+  if (!(d < p.radius) || !(toward > 0.0)) return;
+  double rx = -dx, ry = -dy, rz = -dz;
+  double frep = p.eta_rep * exp(-d / p.nu_rep);
+  double g = toward;
+  double fdamp = p.eta_damp / (d / p.nu_damp + p.eps_p) * g * g;
+  double w = d * d / (p.radius * p.radius) - 2.0 * d / p.radius + 1.0;
+  double smag = fdamp / (fdamp + p.c * log1p(exp(-2.0 * p.c * fdamp)));
+  double a = w * smag * smag;
+  if (a != 0.0) {
+    acc.a00 += a * rx * rx; acc.a01 += a * rx * ry; acc.a02 += a * rx * rz;
+    acc.a11 += a * ry * ry; acc.a12 += a * ry * rz; acc.a22 += a * rz * rz;
+    double bf = a * (frep + fdamp);
+    acc.b0 += bf * rx; acc.b1 += bf * ry; acc.b2 += bf * rz;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Deterministic block reduction: butterfly shuffles inside each warp (fixed
+// pairing), then warp partials summed in warp order.  The result does not
+// depend on timing, so repeated launches are bitwise identical.
+__device__ __forceinline__ double warp_sum(double x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+__device__ __forceinline__ int warp_sum_i(int x) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+  return x;
+}
+
+// Returns the block total in thread 0 (other threads: undefined).
+// `sm` must hold kWarps*kAcc doubles.
+__device__ __forceinline__ void block_reduce(Acc& acc, double* sm) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  bool any = __any_sync(0xffffffffu, acc.a00 != 0.0 || acc.a11 != 0.0 || acc.a22 != 0.0 ||
+                                         acc.b0 != 0.0 || acc.b1 != 0.0 || acc.b2 != 0.0 ||
+                                         acc.a01 != 0.0 || acc.a02 != 0.0 || acc.a12 != 0.0);
+  double v[kAcc];
+  v[0] = acc.a00; v[1] = acc.a01; v[2] = acc.a02; v[3] = acc.a11; v[4] = acc.a12;
+  v[5] = acc.a22; v[6] = acc.b0; v[7] = acc.b1; v[8] = acc.b2;
+  if (any) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) v[k] = warp_sum(v[k]);
+  }
+  v[9] = (double)warp_sum_i(acc.cnt);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < kAcc; ++k) sm[warp * kAcc + k] = v[k];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s[kAcc];
+#pragma unroll
+    for (int k = 0; k < kAcc; ++k) s[k] = sm[k];
+    for (int w = 1; w < kWarps; ++w) {
+#pragma unroll
+      for (int k = 0; k < kAcc; ++k) s[k] += sm[w * kAcc + k];
+    }
+    acc.a00 = s[0]; acc.a01 = s[1]; acc.a02 = s[2]; acc.a11 = s[3]; acc.a12 = s[4];
+    acc.a22 = s[5]; acc.b0 = s[6]; acc.b1 = s[7]; acc.b2 = s[8]; acc.cnt = (int)s[9];
+  }
+  __syncthreads();
+}
+
+// ---------------------------------------------------------------------------
+// pinv_psd (rmpnav/core.py:103-115): eigen-decomposition of the symmetric 3x3
+// metric by cyclic Jacobi in fp64; eigenvalues <= 1e-8 * max(lambda_max, 0)
+// are dropped; accel = V diag(1/lambda) V^T Af.
+__device__ inline void jacobi3(double a[3][3], double V[3][3]) {
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0 : 0.0;
+  for (int sweep = 0; sweep < 32; ++sweep) {
+    double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
+    double diag = fabs(a[0][0]) + fabs(a[1][1]) + fabs(a[2][2]);
+    if (off == 0.0 || off <= 1e-300 || off < 1e-18 * diag) break;
+    for (int p = 0; p < 2; ++p) {
+      for (int q = p + 1; q < 3; ++q) {
+        double apq = a[p][q];
+        if (apq == 0.0) continue;
+        double theta = (a[q][q] - a[p][p]) / (2.0 * apq);
+        double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
+        if (!isfinite(theta)) t = 0.5 / theta;  // |theta| huge: t ~ 1/(2 theta)
+        double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+        for (int k = 0; k < 3; ++k) {  // A <- A J
+          double akp = a[k][p], akq = a[k][q];
+          a[k][p] = c * akp - s * akq;
+          a[k][q] = s * akp + c * akq;
+        }
+        for (int k = 0; k < 3; ++k) {  // A <- J^T A
+          double apk = a[p][k], aqk = a[q][k];
+          a[p][k] = c * apk - s * aqk;
+          a[q][k] = s * apk + c * aqk;
+        }
+        a[p][q] = a[q][p] = 0.0;
+        for (int k = 0; k < 3; ++k) {  // V <- V J
+          double vkp = V[k][p], vkq = V[k][q];
+          V[k][p] = c * vkp - s * vkq;
+          V[k][q] = s * vkp + c * vkq;
+        }
+      }
+    }
+  }
+}
+
+// m: symmetric metric (row-major 9), f: weighted sum (3) -> accel (3).
+__device__ inline void pinv_apply(const double m[9], const double f[3], double out[3]) {
+  double a[3][3], V[3][3];
+  for (int i = 0; i < 3; ++i)
+    for (int j = 0; j < 3; ++j) a[i][j] = 0.5 * (m[3 * i + j] + m[3 * j + i]);
+  jacobi3(a, V);
+  double lam[3] = {a[0][0], a[1][1], a[2][2]};
+  double lmax = fmax(fmax(lam[0], lam[1]), lam[2]);
+  double cut = 1e-8 * (lmax > 0.0 ? lmax : 0.0);
+  double y[3];
+  for (int k = 0; k < 3; ++k) {
+    double vf = V[0][k] * f[0] + V[1][k] * f[1] + V[2][k] * f[2];
+    y[k] = lam[k] > cut ? vf / lam[k] : 0.0;
+  }
+  for (int i = 0; i < 3; ++i) out[i] = V[i][0] * y[0] + V[i][1] * y[1] + V[i][2] * y[2];
+}
+
+// 13-slot layout of ckern.policy_reduce before reshaping (ckern.py:91-93):
+// [A (9, symmetric duplicated), Af (3), count].
+__device__ __forceinline__ void write_slot(const Acc& s, double* slot, double* accel) {
+  double m[9] = {s.a00, s.a01, s.a02, s.a01, s.a11, s.a12, s.a02, s.a12, s.a22};
+  double f[3] = {s.b0, s.b1, s.b2};
+  for (int k = 0; k < 9; ++k) slot[k] = m[k];
+  slot[9] = f[0]; slot[10] = f[1]; slot[11] = f[2];
+  slot[12] = (double)s.cnt;
+  if (accel) pinv_apply(m, f, accel);
+}
+
+}  // namespace rmpb

@@ -1,0 +1,182 @@
+"""Device-resident entry points for callers whose tensors already live on the
+GPU (the "PyTorch extension" side of the north star).  PyTorch is only the
+plumbing here: memory, the current stream, ``torch.distributed``; all
+compute is librmpb's sm_100a kernels, called through the C ABI with raw
+device pointers on ``torch.cuda.current_stream()``.
+
+* ``RayPolicyEngine`` -- one map + one bundle + params; ``evaluate(x, v)``
+  takes P x 3 f64 CUDA tensors and returns (slots P x 13, accels P x 3) CUDA
+  tensors asynchronously (K3, config C4).  ``partial(x, v, begin, end)``
+  returns the 13-slot of a ray range (config C5 ray split) and
+  ``resolve(slots)`` folds slots in fixed order and solves on device.
+* ``lidar_policy_batch_device`` / ``lidar_points_batch_device`` -- many scans
+  per launch (K2).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib as L
+from ._kernels import b200
+
+
+def _torch():
+    import torch
+
+    return torch
+
+
+def _stream_ptr(stream=None) -> int:
+    torch = _torch()
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return int(s.cuda_stream)
+
+
+def _check_tensor(t, shape_tail, dtype_name, name):
+    torch = _torch()
+    want = getattr(torch, dtype_name)
+    if not t.is_cuda:
+        raise ValueError(f"{name} must be a CUDA tensor")
+    if t.dtype != want:
+        raise ValueError(f"{name} must be {dtype_name}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    if shape_tail is not None and tuple(t.shape[1:]) != tuple(shape_tail):
+        raise ValueError(f"{name} must have shape (P, {', '.join(map(str, shape_tail))})")
+
+
+class RayPolicyEngine:
+    """Fused map-based policy evaluation with device-resident inputs."""
+
+    def __init__(self, grid, bundle, params, max_range: float = 20.0, device: int | None = None,
+                 eps: float | None = None, step_scale: float = 0.9):
+        dev = b200.get_device() if device is None else int(device)
+        if isinstance(grid, b200.DeviceGrid):
+            self.grid = grid
+        else:  # EsdfGrid
+            prev = b200.get_device()
+            b200._device = dev
+            try:
+                self.grid = b200.DeviceGrid(grid.values, grid.origin, grid.resolution, device=dev)
+            finally:
+                b200._device = prev
+        if isinstance(bundle, b200.DeviceBundle):
+            self.bundle = bundle
+        else:
+            dirs = getattr(bundle, "directions", bundle)
+            self.bundle = b200.DeviceBundle(dirs, device=dev)
+        self.device = dev
+        self.params = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
+        self.max_range = float(max_range)
+        self.eps = 0.5 * self.grid.res if eps is None else float(eps)
+        self.step_scale = float(step_scale)
+        self.n_rays = self.bundle.n
+
+    def evaluate(self, x, v, out_slot=None, out_accel=None, step_counter=None, stream=None):
+        torch = _torch()
+        _check_tensor(x, (3,), "float64", "x")
+        _check_tensor(v, (3,), "float64", "v")
+        P = x.shape[0]
+        if v.shape[0] != P:
+            raise ValueError("x and v must have the same number of poses")
+        if out_slot is None:
+            out_slot = torch.empty((P, 13), dtype=torch.float64, device=x.device)
+        if out_accel is None:
+            out_accel = torch.empty((P, 3), dtype=torch.float64, device=x.device)
+        cnt = 0 if step_counter is None else step_counter.data_ptr()
+        L.call("rmpb_ray_policy_batch_device", self.grid.handle, self.bundle.handle, x.data_ptr(),
+               v.data_ptr(), P, self.params.ctypes.data, self.max_range, self.eps,
+               self.step_scale, out_slot.data_ptr(), out_accel.data_ptr(), cnt or None,
+               _stream_ptr(stream))
+        return out_slot, out_accel
+
+    def partial(self, x, v, ray_begin: int, ray_end: int, out_slot=None, stream=None):
+        """13-slot of stored rays [ray_begin, ray_end) for one pose (no pinv)."""
+        torch = _torch()
+        _check_tensor(x, None, "float64", "x")
+        _check_tensor(v, None, "float64", "v")
+        if out_slot is None:
+            out_slot = torch.empty(13, dtype=torch.float64, device=x.device)
+        L.call("rmpb_ray_policy_range_device", self.grid.handle, self.bundle.handle, x.data_ptr(),
+               v.data_ptr(), int(ray_begin), int(ray_end), self.params.ctypes.data,
+               self.max_range, self.eps, self.step_scale, out_slot.data_ptr(),
+               _stream_ptr(stream))
+        return out_slot
+
+    @staticmethod
+    def resolve(slots, stream=None):
+        """Fixed-order pairwise fold of (n, 13) slots + pinv, on device."""
+        torch = _torch()
+        _check_tensor(slots, (13,), "float64", "slots")
+        out_slot = torch.empty(13, dtype=torch.float64, device=slots.device)
+        out_accel = torch.empty(3, dtype=torch.float64, device=slots.device)
+        L.call("rmpb_fold_resolve_device", slots.data_ptr(), slots.shape[0], out_slot.data_ptr(),
+               out_accel.data_ptr(), _stream_ptr(stream))
+        return out_slot, out_accel
+
+
+def lidar_policy_batch_device(dirs, R, ranges, valid, v, params, min_range=0.3, stream=None):
+    """S scans sharing the lattice ``dirs`` (n x 3 f64, CUDA): R (S x 9 or
+    None), ranges (S x n f64), valid (S x n uint8 / bool or None), v (S x 3).
+    Returns (slots S x 13, accels S x 3) CUDA tensors."""
+    torch = _torch()
+    _check_tensor(dirs, (3,), "float64", "dirs")
+    S, n = ranges.shape
+    _check_tensor(ranges, (n,), "float64", "ranges")
+    _check_tensor(v, (3,), "float64", "v")
+    if R is not None:
+        R = R.reshape(S, 9).contiguous()
+        _check_tensor(R, (9,), "float64", "R")
+    if valid is not None:
+        valid = valid.to(torch.uint8).contiguous()
+    p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
+    slots = torch.empty((S, 13), dtype=torch.float64, device=ranges.device)
+    accels = torch.empty((S, 3), dtype=torch.float64, device=ranges.device)
+    L.call("rmpb_lidar_policy_batch_device", dirs.data_ptr(), None if R is None else R.data_ptr(),
+           ranges.data_ptr(), None if valid is None else valid.data_ptr(), n, S, v.data_ptr(),
+           p.ctypes.data, float(min_range), slots.data_ptr(), accels.data_ptr(),
+           _stream_ptr(stream))
+    return slots, accels
+
+
+def lidar_points_batch_device(xyz, R, v, params, min_range=0.3, stream=None):
+    """Raw points: xyz (S x n x 3 f32 CUDA), R (S x 9 or None), v (S x 3)."""
+    torch = _torch()
+    if xyz.dtype != torch.float32 or not xyz.is_cuda or xyz.dim() != 3:
+        raise ValueError("xyz must be a (S, n, 3) float32 CUDA tensor")
+    xyz = xyz.contiguous()
+    S, n, _ = xyz.shape
+    _check_tensor(v, (3,), "float64", "v")
+    if R is not None:
+        R = R.reshape(S, 9).contiguous()
+    p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
+    slots = torch.empty((S, 13), dtype=torch.float64, device=xyz.device)
+    accels = torch.empty((S, 3), dtype=torch.float64, device=xyz.device)
+    L.call("rmpb_lidar_points_batch_device", xyz.data_ptr(), None if R is None else R.data_ptr(),
+           n, S, v.data_ptr(), p.ctypes.data, float(min_range), slots.data_ptr(),
+           accels.data_ptr(), _stream_ptr(stream))
+    return slots, accels
+
+
+def lidar_policy_batch_host(velocities, scans, p, min_range=0.3):
+    """Host-facing wrapper: scans share one lattice; uploads, runs, returns
+    (accels S x 3, metrics S x 3 x 3, n_hits S)."""
+    torch = _torch()
+    if not scans:
+        raise ValueError("need at least one scan")
+    dirs0 = scans[0].directions
+    for s in scans:
+        if s.directions.shape != dirs0.shape or not np.array_equal(s.directions, dirs0):
+            raise ValueError("lidar_policy_batch needs scans sharing one beam lattice")
+    dev = torch.device("cuda", b200.get_device())
+    d = torch.from_numpy(np.ascontiguousarray(dirs0)).to(dev)
+    R = torch.from_numpy(np.stack([s.orientation for s in scans]).reshape(-1, 9).copy()).to(dev)
+    rg = torch.from_numpy(np.stack([s.ranges for s in scans])).to(dev)
+    vl = torch.from_numpy(np.stack([s.valid for s in scans]).astype(np.uint8)).to(dev)
+    v = torch.from_numpy(np.asarray(velocities, dtype=np.float64).reshape(-1, 3).copy()).to(dev)
+    slots, accels = lidar_policy_batch_device(d, R, rg, vl, v, p.as_tuple(), min_range)
+    slots = slots.cpu().numpy()
+    return accels.cpu().numpy(), slots[:, 0:9].reshape(-1, 3, 3), slots[:, 12].astype(np.int64)

@@ -1,0 +1,390 @@
+"""GPU parity: the CUDA path through the C ABI vs the CPU oracle and the
+reference's golden vectors.
+
+Bars (BASELINE.json north_star):
+  * hit distance t, hit/miss mask, hit cell, step count: BIT-EXACT;
+  * n_hits: exact;
+  * summed metric / weighted force: within 1e-9 relative of the oracle (the
+    contract is 1e-5; only libm exp/log1p ulps and the reduction order
+    differ), resolved acceleration within 1e-6 relative (pinv amplifies
+    the sum error by cond(sum A) <= ~1e4 here).
+"""
+
+import numpy as np
+import pytest
+
+from conftest import LIDAR, STATIC_MAP, golden_pack, rel_err
+
+pytestmark = pytest.mark.gpu
+
+SUM_TOL = 1e-9
+ACC_TOL = 1e-6
+
+
+@pytest.fixture(scope="module")
+def be():
+    from paper_2301_08068_b200 import _lib
+    from paper_2301_08068_b200._kernels import b200
+
+    _lib.load()
+    assert _lib.device_count() >= 1, "no CUDA device visible"
+    return b200
+
+
+@pytest.fixture(scope="module")
+def gworld(be, golden):
+    g = golden
+    pack = golden_pack(g)
+    vals = be.bake_values(pack, g["grid_origin"], float(g["grid_res"]), tuple(g["grid_dims"]))
+    return pack, vals
+
+
+@pytest.fixture(scope="module")
+def c1(be, oracle):
+    from paper_2301_08068_b200 import synth
+
+    scene = synth.c1_scene()
+    grid = synth.c1_grid(scene)
+    states = synth.bench_states(scene, count=10, seed=123)
+    dirs = oracle.sample_directions(65536)
+    return scene, grid, states, dirs
+
+
+def check_policy(slot, acc, slot_ref, acc_ref):
+    assert slot[12] == slot_ref[12]
+    assert rel_err(slot[:9], slot_ref[:9]) <= SUM_TOL
+    assert rel_err(slot[9:12], slot_ref[9:12]) <= SUM_TOL
+    assert rel_err(acc, acc_ref) <= ACC_TOL
+
+
+# --- golden vectors (produced by running the reference) -----------------------
+
+def test_gpu_bake_bit_exact_vs_reference(gworld, golden):
+    import hashlib
+
+    _, vals = gworld
+    assert hashlib.sha256(vals.tobytes()).digest() == golden["grid_sha256_f64"].tobytes()
+
+
+def test_fused_ray_policy_vs_golden(be, gworld, golden):
+    g = golden
+    vals = gworld[1].astype(np.float32).astype(np.float64)
+    res = float(g["grid_res"])
+    for k in range(g["pose_x"].shape[0]):
+        slot, acc, t, cells, steps = be.ray_policy_fused(
+            vals, g["grid_origin"], res, g["pose_x"][k], g["pose_v"][k], g["dirs"], STATIC_MAP,
+            10.0, 0.5 * res, 0.9, with_rays=True)
+        assert np.array_equal(t, g["trace_t"][k]), f"pose {k}: t differs"
+        assert np.array_equal(np.isfinite(t), np.isfinite(g["trace_t"][k]))
+        check_policy(slot, acc, g["slots"][k], g["accels"][k])
+        assert rel_err(slot[:9].reshape(3, 3), g["metrics"][k]) <= SUM_TOL
+
+
+def test_unfused_protocol_vs_golden(be, gworld, golden):
+    g = golden
+    vals = gworld[1].astype(np.float32).astype(np.float64)
+    res = float(g["grid_res"])
+    for k in (0, 3):
+        t = be.grid_trace(vals, g["grid_origin"], res, g["pose_x"][k], g["dirs"], 10.0,
+                          0.5 * res, 0.9)
+        assert np.array_equal(t, g["trace_t"][k])
+        m, w, n = be.policy_reduce(g["dirs"], t, g["pose_v"][k], STATIC_MAP, 0.0)
+        assert n == int(g["slots"][k][12])
+        assert rel_err(m.ravel(), g["slots"][k][:9]) <= SUM_TOL
+        assert rel_err(w, g["slots"][k][9:12]) <= SUM_TOL
+
+
+def test_f64_grid_trace_vs_golden(be, gworld, golden):
+    g = golden
+    vals = gworld[1]  # not f32-exact -> f64 storage
+    res = float(g["grid_res"])
+    grid = be.DeviceGrid(vals, g["grid_origin"], res)
+    assert grid.storage == "f64"
+    t = be.grid_trace(vals, g["grid_origin"], res, g["pose_x"][0], g["dirs"], 10.0, 0.5 * res, 0.9)
+    assert np.array_equal(t, g["trace_t_f64grid"])
+
+
+def test_public_api_vs_golden(be, gworld, golden):
+    import paper_2301_08068_b200 as P
+
+    g = golden
+    vals = gworld[1].astype(np.float32).astype(np.float64)
+    grid = P.EsdfGrid(g["grid_origin"], float(g["grid_res"]), tuple(g["grid_dims"]), vals)
+    bundle = P.RayBundle(g["dirs"])
+    p = P.preset("static_map").obstacle
+    for k in range(g["pose_x"].shape[0]):
+        pol = P.ray_policy(P.RobotState(g["pose_x"][k], g["pose_v"][k]), grid, bundle, p, 10.0)
+        assert rel_err(pol.metric, g["metrics"][k]) <= SUM_TOL
+        assert rel_err(pol.accel, g["accels"][k]) <= ACC_TOL
+    acc, met, nh = P.ray_policy_batch((g["pose_x"], g["pose_v"]), grid, bundle, p, 10.0)
+    assert np.array_equal(nh, g["slots"][:, 12].astype(np.int64))
+    for k in range(len(nh)):
+        assert rel_err(met[k], g["metrics"][k]) <= SUM_TOL
+        assert rel_err(acc[k], g["accels"][k]) <= ACC_TOL
+
+
+def test_lidar_vs_golden(be, golden):
+    import paper_2301_08068_b200 as P
+
+    g = golden
+    lp = P.preset("lidar").obstacle
+    for i in range(g["lidar_ranges"].shape[0]):
+        R = g["lidar_rot"] if i == 1 else np.eye(3)
+        scan = P.RangeScan(g["lidar_dirs"], g["lidar_ranges"][i], g["lidar_valid"][i],
+                           g["pose_x"][i], R, 16, 128)
+        pol = P.lidar_policy(g["pose_v"][i], scan, lp)
+        assert rel_err(pol.metric, g["lidar_metrics"][i]) <= SUM_TOL
+        assert rel_err(pol.accel, g["lidar_accels"][i]) <= ACC_TOL
+
+
+def test_scene_esdf_pinv_vs_golden(be, gworld, golden):
+    g = golden
+    pack, vals = gworld
+    t = be.scene_trace(pack, g["pose_x"][1], g["scene_trace_dirs"], 20.0, 1e-4, 0.0)
+    assert np.array_equal(t, g["scene_trace_t"])
+    assert np.array_equal(be.scene_distance_many(pack, g["esdf_pts"], 0.0), g["scene_dist"])
+    d, gr, fl = be.esdf_sample_many(vals, g["grid_origin"], float(g["grid_res"]), g["esdf_pts"])
+    assert np.array_equal(d, g["esdf_d"])
+    assert np.allclose(gr, g["esdf_g"], rtol=0, atol=1e-15)
+    assert np.array_equal(fl, g["esdf_flag"])
+    out = be.pinv_psd(g["pinv_in"])
+    for a, b in zip(out, g["pinv_out"]):
+        assert rel_err(a, b) <= 1e-10 or np.abs(a - b).max() <= 1e-13
+
+
+def test_spec_kats(be, golden):
+    import paper_2301_08068_b200 as P
+
+    sph = P.Scene(P.Aabb([-6, -6, -6], [6, 6, 6]), [P.Primitive.sphere((0, 0, 0), 1.0)])
+    assert P.raycast(sph, (5, 0, 0), (-1, 0, 0)) == float(golden["kat_sphere_ray"]) == 4.0
+    empty = P.Scene(P.Aabb([-6, -6, -6], [6, 6, 6]), [])
+    assert np.isinf(P.raycast(empty, (0, 0, 0), (1, 0, 0)))
+    d1 = P.sample_directions(1).directions
+    assert np.allclose(d1, golden["kat_dir1"], rtol=0, atol=1e-15)
+
+
+# --- full-size C1 (headline config) --------------------------------------------
+
+def test_c1_full_size_bit_exact(be, oracle, c1):
+    from paper_2301_08068_b200 import synth
+
+    scene, grid, states, dirs = c1
+    assert synth.grid_sha_prefix(grid) == synth.C1_SHA_PREFIX
+    for st in states[:4]:
+        slot, acc, t, cells, steps = be.ray_policy_fused(
+            grid.values, grid.origin, grid.resolution, st.position, st.velocity, dirs, STATIC_MAP,
+            10.0, 0.05, 0.9, with_rays=True)
+        t_r, c_r, s_r = oracle.grid_trace(grid.values, grid.origin, grid.resolution, st.position,
+                                          dirs, 10.0, 0.05, 0.9, with_cells=True, with_steps=True,
+                                          workers=8)
+        assert np.array_equal(t, t_r)
+        assert np.array_equal(cells, c_r)
+        assert np.array_equal(steps, s_r)
+        slot_r = oracle.policy_slot(dirs, t_r, st.velocity, STATIC_MAP)
+        check_policy(slot, acc, slot_r, oracle.accel_from_slot(slot_r))
+
+
+def test_c1_batch_matches_single_and_oracle(be, oracle, c1):
+    from paper_2301_08068_b200 import synth
+
+    scene, grid, states, dirs = c1
+    x, v = synth.states_arrays(states)
+    slots, accs = be.ray_policy_batch(grid.values, grid.origin, grid.resolution, x, v, dirs,
+                                      STATIC_MAP, 10.0, 0.05, 0.9)
+    for k, st in enumerate(states):
+        slot_r, acc_r, _ = oracle.ray_policy(grid.values, grid.origin, grid.resolution,
+                                             st.position, st.velocity, dirs, STATIC_MAP, 10.0,
+                                             workers=8)
+        check_policy(slots[k], accs[k], slot_r, acc_r)
+    # pose with an all-zero metric (SURVEY.md App. B pose 3): accel exactly 0
+    assert slots[3][12] == 11597 and not slots[3][:12].any() and not accs[3].any()
+
+
+def test_determinism_bitwise(be, c1):
+    scene, grid, states, dirs = c1
+    st = states[0]
+    a = be.ray_policy_fused(grid.values, grid.origin, grid.resolution, st.position, st.velocity,
+                            dirs, STATIC_MAP, 10.0, 0.05, 0.9)
+    for _ in range(3):
+        b = be.ray_policy_fused(grid.values, grid.origin, grid.resolution, st.position,
+                                st.velocity, dirs, STATIC_MAP, 10.0, 0.05, 0.9)
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_layouts_and_storage_identical(be, oracle, c1):
+    from paper_2301_08068_b200 import _lib as L
+
+    scene, grid, states, dirs = c1
+    st = states[1]
+    sub = dirs[:8192]
+    t_ref = oracle.grid_trace(grid.values, grid.origin, grid.resolution, st.position, sub, 10.0,
+                              0.05, 0.9)
+    variants = [dict(storage=L.STORE_F32, layout=L.LAYOUT_LINEAR),
+                dict(storage=L.STORE_F32, layout=L.LAYOUT_QUAD),
+                dict(storage=L.STORE_F64, layout=L.LAYOUT_LINEAR),
+                dict(storage=L.STORE_F64, layout=L.LAYOUT_QUAD)]
+    for kw in variants:
+        dg = be.DeviceGrid(grid.values, grid.origin, grid.resolution, **kw)
+        t, _, _ = be.grid_trace_ex(dg, grid.origin, grid.resolution, st.position, sub, 10.0,
+                                   0.05, 0.9)
+        assert np.array_equal(t, t_ref), kw
+
+
+def test_brick_grid_identical_to_dense(be, oracle):
+    """Block-hashed TSDF: a truncated field whose far bricks are uniform +tau."""
+    rng = np.random.default_rng(3)
+    nx, ny, nz = 64, 48, 40
+    res, tau = 0.05, 0.2
+    ii, jj, kk = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    p = np.stack([ii, jj, kk], -1) * res
+    c = np.array([1.5, 1.2, 1.0])
+    sd = np.linalg.norm(p - c, axis=-1) - 0.6
+    vals = np.clip(sd, -tau, tau).astype(np.float32).astype(np.float64)
+    dg = be.DeviceGrid(vals, np.zeros(3), res, brick_fill=tau)
+    assert dg.layout == "brick" and 0 < dg.bricks < (8 * 6 * 5)
+    dirs = rng.normal(size=(4096, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    start = np.array([0.4, 0.4, 0.3])
+    t, cells, _ = be.grid_trace_ex(dg, np.zeros(3), res, start, dirs, 5.0, 0.5 * res, 0.9,
+                                   with_cells=True)
+    t_r, c_r = oracle.grid_trace(vals, np.zeros(3), res, start, dirs, 5.0, 0.5 * res, 0.9,
+                                 with_cells=True)
+    assert np.array_equal(t, t_r) and np.array_equal(cells, c_r)
+    assert np.isfinite(t).mean() > 0.05
+
+
+# --- edge cases -------------------------------------------------------------------
+
+def test_edge_cases(be, oracle):
+    rng = np.random.default_rng(5)
+    nx, ny, nz, res = 30, 20, 10, 0.1
+    o = np.array([0.0, 0.0, 0.0])
+    free = np.full((nx, ny, nz), 5.0)
+    dirs = rng.normal(size=(3000, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    dirs[:40, 0] = 0.0
+    dirs[40:80, 1] = 0.0
+    dirs[80:120, 2] = 0.0
+    dirs[120:130] = [1.0, 0.0, 0.0]
+    # all rays miss -> zero policy
+    slot, acc = be.ray_policy_fused(free, o, res, [1.0, 1.0, 0.5], [1, 0, 0], dirs, STATIC_MAP,
+                                    10.0, 0.05, 0.9)
+    assert not slot.any() and not acc.any()
+    # start inside an obstacle -> every in-domain ray hits at t = 0
+    solid = np.full((nx, ny, nz), -1.0)
+    t = be.grid_trace(solid, o, res, [1.0, 1.0, 0.5], dirs, 10.0, 0.05, 0.9)
+    assert (t == 0.0).all()
+    # start outside the domain, directions with zero components
+    vals = (rng.normal(size=(nx, ny, nz)) * 0.2 + 0.15).astype(np.float32).astype(np.float64)
+    for start in ([-1.0, 0.5, 0.5], [1.5, 0.9, 0.45], [1.5, 5.0, 0.2], [3.0, 1.0, 0.5]):
+        t, c, s = be.grid_trace_ex(vals, o, res, start, dirs, 10.0, 0.05, 0.9, True, True)
+        t_r, c_r, s_r = oracle.grid_trace(vals, o, res, start, dirs, 10.0, 0.05, 0.9, True, True)
+        assert np.array_equal(t, t_r) and np.array_equal(c, c_r) and np.array_equal(s, s_r)
+    # empty inputs
+    assert be.grid_trace(vals, o, res, [0.5, 0.5, 0.5], np.zeros((0, 3)), 10.0, 0.05, 0.9).size == 0
+    m, w, n = be.policy_reduce(np.zeros((0, 3)), np.zeros(0), [1, 0, 0], STATIC_MAP)
+    assert n == 0 and not m.any() and not w.any()
+    # NaN / inf / below-min-range distances are skipped (not counted)
+    d = np.array([np.nan, np.inf, 0.1, 0.5, 1.0])
+    dd = dirs[:5]
+    m, w, n = be.policy_reduce(dd, d, [0.3, 0.2, 0.1], LIDAR, 0.3)
+    m_r, w_r, n_r = oracle.policy_reduce(dd, d, [0.3, 0.2, 0.1], LIDAR, 0.3)
+    assert n == n_r == 2
+    assert rel_err(m, m_r) <= SUM_TOL and rel_err(w, w_r) <= SUM_TOL
+
+
+def test_odd_sizes_and_segmentation(be, oracle, c1):
+    """Ray counts that are not multiples of the CTA width, and forced
+    segmentation variants, give identical traces and equal sums."""
+    from paper_2301_08068_b200 import _lib
+
+    scene, grid, states, dirs = c1
+    st = states[2]
+    for n in (1, 31, 257, 5000):
+        sub = np.ascontiguousarray(dirs[:n])
+        slot, acc, t, _, _ = be.ray_policy_fused(grid.values, grid.origin, grid.resolution,
+                                                 st.position, st.velocity, sub, STATIC_MAP, 10.0,
+                                                 0.05, 0.9, with_rays=True)
+        t_r = oracle.grid_trace(grid.values, grid.origin, grid.resolution, st.position, sub, 10.0,
+                                0.05, 0.9)
+        assert np.array_equal(t, t_r)
+        slot_r = oracle.policy_slot(sub, t_r, st.velocity, STATIC_MAP)
+        check_policy(slot, acc, slot_r, oracle.accel_from_slot(slot_r))
+    base = be.ray_policy_fused(grid.values, grid.origin, grid.resolution, st.position,
+                               st.velocity, dirs, STATIC_MAP, 10.0, 0.05, 0.9)
+    try:
+        for sr in (256, 4096, 65536):
+            _lib.set_option("seg_rays", sr)
+            s2 = be.ray_policy_fused(grid.values, grid.origin, grid.resolution, st.position,
+                                     st.velocity, dirs, STATIC_MAP, 10.0, 0.05, 0.9)
+            check_policy(s2[0], s2[1], base[0], base[1])
+    finally:
+        _lib.set_option("seg_rays", 0)
+
+
+def test_lidar_points_and_batch(be, oracle, c1):
+    import paper_2301_08068_b200 as P
+    from paper_2301_08068_b200 import synth
+
+    scene, grid, states, dirs = c1
+    scans = synth.lidar_scans(scene, states[:3], 32, 256)
+    lp = P.preset("lidar").obstacle
+    for st, sc in zip(states[:3], scans):
+        wd = sc.world_directions()
+        slot_r, acc_r = oracle.lidar_policy(wd, sc.ranges, sc.valid, st.velocity, LIDAR, 0.3)
+        pol = P.lidar_policy(st.velocity, sc, lp)
+        assert rel_err(pol.metric.ravel(), slot_r[:9]) <= SUM_TOL
+        assert rel_err(pol.accel, acc_r) <= ACC_TOL
+        # raw points: p = dir * range (f32), invalid beams -> zero points
+        pts = np.where(sc.valid[:, None], sc.directions * sc.ranges[:, None], 0.0)
+        pts32 = pts.astype(np.float32)
+        pol2 = P.lidar_policy_points(st.velocity, pts32, lp)
+        p64 = pts32.astype(np.float64)
+        r = np.sqrt((p64 * p64).sum(1))
+        with np.errstate(invalid="ignore", divide="ignore"):
+            dd = p64 / r[:, None]
+        ok = r > 0
+        slot_p, acc_p = oracle.lidar_policy(np.where(ok[:, None], dd, 0.0), r, ok, st.velocity,
+                                            LIDAR, 0.3)
+        assert rel_err(pol2.metric.ravel(), slot_p[:9]) <= 1e-7
+        assert rel_err(pol2.accel, acc_p) <= 1e-5
+    acc_b, met_b, nh_b = P.lidar_policy_batch([s.velocity for s in states[:3]], scans, lp)
+    for k, (st, sc) in enumerate(zip(states[:3], scans)):
+        slot_r, acc_r = oracle.lidar_policy(sc.world_directions(), sc.ranges, sc.valid,
+                                            st.velocity, LIDAR, 0.3)
+        assert nh_b[k] == int(slot_r[12])
+        assert rel_err(met_b[k].ravel(), slot_r[:9]) <= SUM_TOL
+        assert rel_err(acc_b[k], acc_r) <= ACC_TOL
+
+
+def test_ray_split_partials_fold(be, c1):
+    """Config C5 mechanics: ray ranges of one pose -> per-range slots ->
+    fixed-order fold + pinv on device == the whole-pose evaluation."""
+    import torch
+
+    from paper_2301_08068_b200.device import RayPolicyEngine
+
+    scene, grid, states, dirs = c1
+    st = states[0]
+    eng = RayPolicyEngine(grid, dirs, STATIC_MAP, 10.0, device=0)
+    x = torch.tensor(st.position, dtype=torch.float64, device="cuda")
+    v = torch.tensor(st.velocity, dtype=torch.float64, device="cuda")
+    whole_s, whole_a = eng.evaluate(x.view(1, 3), v.view(1, 3))
+    n = eng.n_rays
+    edges = [0, n // 8, n // 3, n // 2, n]
+    parts = torch.stack([eng.partial(x, v, a, b) for a, b in zip(edges[:-1], edges[1:])])
+    s, a = eng.resolve(parts)
+    torch.cuda.synchronize()
+    check_policy(s.cpu().numpy(), a.cpu().numpy(), whole_s[0].cpu().numpy(),
+                 whole_a[0].cpu().numpy())
+
+
+def test_device_halton_close_to_reference(be, oracle):
+    import paper_2301_08068_b200 as P
+
+    n = 65536
+    d = P.sample_directions(n).directions
+    r = oracle.sample_directions(n)
+    assert d.shape == r.shape
+    assert np.abs(d - r).max() <= 4e-16
+    assert np.allclose(np.linalg.norm(d, axis=1), 1.0, atol=1e-12)
