@@ -29,6 +29,7 @@ using namespace rmpb;
 static thread_local std::string g_err;
 static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int64_t> g_opt_seg_rays{0};
+static std::atomic<int64_t> g_opt_kernel{2};  // 1: one ray per thread per pass; 2: lane refill
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -170,6 +171,8 @@ struct rmpb_bundle {
   double* d_dy = nullptr;
   double* d_dz = nullptr;
   int* d_perm = nullptr;   // stored -> original (null when identity)
+  double* d_rcp = nullptr; // [6][n] double-double reciprocals of dx, dy, dz
+  int64_t rs = 0;          // row stride of d_rcp (full size; differs for range views)
   double* d_aos = nullptr; // original order AoS (for LiDAR use / download)
 };
 
@@ -234,7 +237,7 @@ static int check_params(const double* p) {
 static void choose_segments(int64_t P, int64_t n, int* segs, int* seg_rays) {
   int64_t sr = g_opt_seg_rays.load();
   if (sr <= 0) {
-    const int64_t target_units = 148LL * 8 * 2;
+    const int64_t target_units = 148LL * 4 * 8;
     sr = kBlock;
     while (sr < n && P * ((n + sr * 2 - 1) / (sr * 2)) >= target_units) sr *= 2;
   }
@@ -263,6 +266,11 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
   if (!name) return fail(RMPB_ERR_INVALID, "name is NULL");
   if (!strcmp(name, "seg_rays")) {
     g_opt_seg_rays.store(value);
+    return RMPB_OK;
+  }
+  if (!strcmp(name, "kernel")) {
+    if (value != 1 && value != 2) return fail(RMPB_ERR_INVALID, "kernel must be 1 or 2");
+    g_opt_kernel.store(value);
     return RMPB_OK;
   }
   return fail(RMPB_ERR_INVALID, "unknown option '%s'", name);
@@ -521,6 +529,8 @@ static int bundle_finish(rmpb_bundle* b, cudaStream_t st) {
   CK(cudaMalloc((void**)&b->d_dx, n * sizeof(double)));
   CK(cudaMalloc((void**)&b->d_dy, n * sizeof(double)));
   CK(cudaMalloc((void**)&b->d_dz, n * sizeof(double)));
+  CK(cudaMalloc((void**)&b->d_rcp, 6 * (size_t)n * sizeof(double)));
+  b->rs = n;
   if (b->order == RMPB_ORDER_MORTON) {
     unsigned *k_in, *k_out;
     int* i_in;
@@ -539,7 +549,8 @@ static int bundle_finish(rmpb_bundle* b, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
     cudaFree(tmp); cudaFree(k_in); cudaFree(k_out); cudaFree(i_in);
   }
-  k_gather_dirs<<<grid_blocks(n), 256, 0, st>>>(n, b->d_aos, b->d_perm, b->d_dx, b->d_dy, b->d_dz);
+  k_gather_dirs<<<grid_blocks(n), 256, 0, st>>>(n, b->d_aos, b->d_perm, b->d_dx, b->d_dy, b->d_dz,
+                                                b->d_rcp);
   CKL();
   CK(cudaStreamSynchronize(st));
   return RMPB_OK;
@@ -587,7 +598,7 @@ static int bundle_new(const double* dirs, int64_t n, int order, int device, bool
   cudaStreamDestroy(st);
   if (rc != RMPB_OK) {
     rmpb_bundle* p = b.release();
-    cudaFree(p->d_aos); cudaFree(p->d_dx); cudaFree(p->d_dy); cudaFree(p->d_dz); cudaFree(p->d_perm);
+    cudaFree(p->d_aos); cudaFree(p->d_dx); cudaFree(p->d_dy); cudaFree(p->d_dz); cudaFree(p->d_perm); cudaFree(p->d_rcp);
     delete p;
     return rc;
   }
@@ -617,6 +628,7 @@ extern "C" int rmpb_bundle_destroy(rmpb_bundle* b) {
   if (!b) return RMPB_OK;
   DeviceGuard dg(b->device);
   cudaFree(b->d_aos); cudaFree(b->d_dx); cudaFree(b->d_dy); cudaFree(b->d_dz);
+  cudaFree(b->d_rcp);
   if (b->d_perm) cudaFree(b->d_perm);
   delete b;
   return RMPB_OK;
@@ -625,6 +637,7 @@ extern "C" int rmpb_bundle_destroy(rmpb_bundle* b) {
 static Bundle bundle_view(const rmpb_bundle* b) {
   Bundle v;
   v.dx = b->d_dx; v.dy = b->d_dy; v.dz = b->d_dz; v.perm = b->d_perm; v.n = (int)b->n;
+  v.rcp = b->d_rcp; v.rs = (int)b->rs;
   return v;
 }
 
@@ -638,9 +651,20 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
   Bundle bv = bundle_view(b);
   const long long units = (long long)P * segs;
   if (units >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many CTA units");
+  const bool v2 = g_opt_kernel.load() == 2;
   return with_grid(g, [&](auto acc) -> int {
-    k_ray_policy<<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
-                                                     step_scale, segs, seg_rays, ro);
+    using G = decltype(acc);
+    if (!v2)
+      k_ray_policy<<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
+                                                       step_scale, segs, seg_rays, ro);
+    else if (ro.t)
+      k_ray_policy2<G, true><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
+                                                                 max_range, eps, step_scale, segs,
+                                                                 seg_rays, ro);
+    else
+      k_ray_policy2<G, false><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
+                                                                  max_range, eps, step_scale, segs,
+                                                                  seg_rays, ro);
     CKL();
     return RMPB_OK;
   });
@@ -789,6 +813,7 @@ extern "C" int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bundl
   sub.d_dx = b->d_dx + ray_begin;
   sub.d_dy = b->d_dy + ray_begin;
   sub.d_dz = b->d_dz + ray_begin;
+  sub.d_rcp = b->d_rcp + ray_begin;  // row stride stays b->rs
   sub.d_perm = nullptr;
   sub.n = ray_end - ray_begin;
   if (sub.n == 0) {

@@ -40,7 +40,32 @@ struct GridGeom {
   double ox, oy, oz, res;
   double mx, my, mz;     // n - 1.0 (the clamp bounds)
   double hx, hy, hz;     // origin + (n-1)*res (the slab bounds)
+  double rhi, rlo;       // double-double 1/res for the exact division (exdiv)
+  double dx2, dy2, dz2;  // (double)(n - 2): the clamped cell's base
 };
+
+// Exact a / b for a divisor with precomputed yhi = RN(1/b),
+// ylo = RN(fma(-b, yhi, 1) * yhi): q0 = RN(a (yhi + ylo)) is within half an
+// ulp (+2^-105 rel) of a/b, hence faithful, and Markstein's correction
+// q = RN(q0 + (a - b q0) yhi) is the correctly rounded quotient -- bit-identical
+// to IEEE a / b (no exact rounding ties exist for a non-power-of-two divisor;
+// for a power of two every step is exact).  4 fp64 ops, no MUFU, no branch.
+// Validated: oracle/check_exact_div.c, tests/test_exact_division.py.
+__device__ __forceinline__ double exdiv(double a, double b, double yhi, double ylo) {
+  double q0 = __fma_rn(a, yhi, __dmul_rn(a, ylo));
+  double r = __fma_rn(-q0, b, a);
+  return __fma_rn(r, yhi, q0);
+}
+
+__host__ __device__ inline void recip_dd(double b, double& hi, double& lo) {
+  hi = 1.0 / b;
+#ifdef __CUDA_ARCH__
+  double e = __fma_rn(-b, hi, 1.0);
+#else
+  double e = __builtin_fma(-b, hi, 1.0);
+#endif
+  lo = e * hi;
+}
 
 __host__ inline GridGeom make_geom(int64_t nx, int64_t ny, int64_t nz, double ox, double oy,
                                    double oz, double res) {
@@ -52,6 +77,8 @@ __host__ inline GridGeom make_geom(int64_t nx, int64_t ny, int64_t nz, double ox
   g.hx = ox + (double)(nx - 1) * res;
   g.hy = oy + (double)(ny - 1) * res;
   g.hz = oz + (double)(nz - 1) * res;
+  recip_dd(res, g.rhi, g.rlo);
+  g.dx2 = (double)(nx - 2); g.dy2 = (double)(ny - 2); g.dz2 = (double)(nz - 2);
   return g;
 }
 
@@ -63,7 +90,7 @@ struct LinearGrid {
   const T* __restrict__ v;
   int sy, sx;  // strides: nz, ny*nz (node counts < 2^31 checked at create)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    const T* b = v + ((int64_t)ix * sx + (int64_t)iy * sy + iz);
+    const T* b = v + (ix * sx + iy * sy + iz);  // < 2^31 nodes (checked at create)
     Corners c;
     c.v000 = (double)__ldg(b);           c.v001 = (double)__ldg(b + 1);
     c.v010 = (double)__ldg(b + sy);      c.v011 = (double)__ldg(b + sy + 1);
@@ -77,7 +104,7 @@ struct QuadGridF32 {
   const float4* __restrict__ q;
   int qy, qx;  // strides in quads: (nz-1), (ny-1)*(nz-1)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    const float4* b = q + ((int64_t)ix * qx + (int64_t)iy * qy + iz);
+    const float4* b = q + (ix * qx + iy * qy + iz);
     float4 a = __ldg(b), c = __ldg(b + qx);
     Corners k;
     k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
@@ -90,7 +117,7 @@ struct QuadGridF64 {
   const double2* __restrict__ q;  // 2 double2 per quad
   int qy, qx;
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    const double2* b = q + 2 * ((int64_t)ix * qx + (int64_t)iy * qy + iz);
+    const double2* b = q + 2 * (int64_t)(ix * qx + iy * qy + iz);
     const double2* c = b + 2 * (int64_t)qx;
     double2 a0 = __ldg(b), a1 = __ldg(b + 1), c0 = __ldg(c), c1 = __ldg(c + 1);
     Corners k;
@@ -149,6 +176,78 @@ __device__ __forceinline__ double interp(const G& grid, const GridGeom& g, doubl
   double c0 = c00 + fy * (c01 - c00);
   double c1 = c10 + fy * (c11 - c10);
   return c0 + fx * (c1 - c0);
+}
+
+// Cell coordinate of one axis, identical to the reference's
+//   u = clamp(u, 0, n-1); i = min((int64)floor(u), n-2); f = u - (double)i
+// without the XU pipe: u + 2^52 rounds u (< 2^52) to the nearest integer in
+// the low mantissa bits, a compare fixes round-up to floor.  A NaN u (not
+// reachable from finite inputs) yields an in-range index via the int clamp.
+__device__ __forceinline__ void cell_coord(double u, double m, int nm2, double dnm2, int& i,
+                                           double& f) {
+  u = u < 0.0 ? 0.0 : u;  // the reference's compares (not fmin/fmax: no NaN fixups)
+  u = u > m ? m : u;
+  const double big = u + 4503599627370496.0;  // 2^52
+  double r = big - 4503599627370496.0;
+  int ri = __double2loint(big);
+  if (r > u) { r = r - 1.0; ri -= 1; }
+  if (ri > nm2) { ri = nm2; r = dnm2; }
+  i = ri < 0 ? 0 : ri;
+  f = u - r;
+}
+
+// interp with exdiv + cell_coord: bit-identical to interp() above.
+template <class G>
+__device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, double px,
+                                              double py, double pz, int& ix, int& iy, int& iz) {
+  double fx, fy, fz;
+  cell_coord(exdiv(px - g.ox, g.res, g.rhi, g.rlo), g.mx, g.nx - 2, g.dx2, ix, fx);
+  cell_coord(exdiv(py - g.oy, g.res, g.rhi, g.rlo), g.my, g.ny - 2, g.dy2, iy, fy);
+  cell_coord(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), g.mz, g.nz - 2, g.dz2, iz, fz);
+  Corners c = grid.load(ix, iy, iz);
+  double c00 = c.v000 + fz * (c.v001 - c.v000);
+  double c01 = c.v010 + fz * (c.v011 - c.v010);
+  double c10 = c.v100 + fz * (c.v101 - c.v100);
+  double c11 = c.v110 + fz * (c.v111 - c.v110);
+  double c0 = c00 + fy * (c01 - c00);
+  double c1 = c10 + fy * (c11 - c10);
+  return c0 + fx * (c1 - c0);
+}
+
+// Per-ray reciprocal of a direction component (0 -> unused).
+struct RecipDir { double hx, lx, hy, ly, hz, lz; };
+
+// box_span with exdiv by the per-ray reciprocals: bit-identical to box_span.
+__device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, double sy, double sz,
+                                              double dx, double dy, double dz, const RecipDir& q,
+                                              double& t0, double& t1) {
+  double tlo = -CUDART_INF, thi = CUDART_INF, ta, tb, tmp;
+  if (dx != 0.0) {
+    ta = exdiv(g.ox - sx, dx, q.hx, q.lx); tb = exdiv(g.hx - sx, dx, q.hx, q.lx);
+    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
+    if (ta > tlo) tlo = ta;
+    if (tb < thi) thi = tb;
+  } else if (sx < g.ox || sx > g.hx) {
+    return false;
+  }
+  if (dy != 0.0) {
+    ta = exdiv(g.oy - sy, dy, q.hy, q.ly); tb = exdiv(g.hy - sy, dy, q.hy, q.ly);
+    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
+    if (ta > tlo) tlo = ta;
+    if (tb < thi) thi = tb;
+  } else if (sy < g.oy || sy > g.hy) {
+    return false;
+  }
+  if (dz != 0.0) {
+    ta = exdiv(g.oz - sz, dz, q.hz, q.lz); tb = exdiv(g.hz - sz, dz, q.hz, q.lz);
+    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
+    if (ta > tlo) tlo = ta;
+    if (tb < thi) thi = tb;
+  } else if (sz < g.oz || sz > g.hz) {
+    return false;
+  }
+  t0 = tlo; t1 = thi;
+  return true;
 }
 
 // Slab interval against the node domain (rmpnav/_kernels/_ckern.pyx:171-212).

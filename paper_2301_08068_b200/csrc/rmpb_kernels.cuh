@@ -41,8 +41,16 @@ struct Bundle {
   const double* __restrict__ dx;
   const double* __restrict__ dy;
   const double* __restrict__ dz;
-  const int* __restrict__ perm;  // stored index -> original index (null = identity)
+  const double* __restrict__ rcp;  // [6][n]: hi/lo reciprocal of dx, dy, dz (exdiv)
+  const int* __restrict__ perm;    // stored index -> original index (null = identity)
   int n;
+  int rs;                          // row stride of rcp (the full bundle size)
+  __device__ __forceinline__ RecipDir recip(int i) const {
+    RecipDir q;
+    q.hx = rcp[i]; q.lx = rcp[rs + i]; q.hy = rcp[2 * rs + i];
+    q.ly = rcp[3 * rs + i]; q.hz = rcp[4 * rs + i]; q.lz = rcp[5 * rs + i];
+    return q;
+  }
 };
 
 __device__ __forceinline__ void acc_to_arr(const Acc& a, double* o) {
@@ -127,6 +135,210 @@ k_ray_policy(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max
     int s = warp_sum_i(my_steps);
     if ((threadIdx.x & 31) == 0) atomicAdd(ro.step_total, (unsigned long long)s);
   }
+  finish_unit(acc, io, pose, seg, segs);
+}
+
+// K1/K3 v2: the production trace kernel.
+//
+// * exact arithmetic via interp_fast / box_span_fast (no MUFU, no F2I/I2F);
+// * work split: a unit's rays are cut into 32-ray chunks (consecutive in the
+//   Morton-ordered bundle) dealt round-robin to the CTA's warps, which keeps
+//   the warps' total march lengths balanced;
+// * ray preparation (direction, slab interval, start / end t) is done for a
+//   whole chunk at once by all 32 lanes (converged) into a per-warp shared
+//   buffer; rays that miss the map domain are retired right there;
+// * lane refill: a lane whose ray finishes pops the next prepared ray
+//   (ballot + prefix popc), so lanes never idle behind the warp's longest
+//   ray.  The ray -> lane schedule depends only on the data: deterministic;
+// * deferred policy: hits inside the activation radius are queued per warp
+//   and evaluated 32 at a time by the whole warp (no divergent
+//   transcendentals inside the march); each batch is reduced with a fixed
+//   butterfly and added to the warp's accumulator in batch order, then the
+//   CTA reduces warps in warp order: bitwise reproducible.
+constexpr int kQueue = 64;
+constexpr int kPrep = 32;
+
+struct K2Smem {
+  double acc[kWarps][9];
+  double qt[kWarps][kQueue];
+  int qr[kWarps][kQueue];
+  double pt[kWarps][kPrep], pe[kWarps][kPrep];
+  double px[kWarps][kPrep], py[kWarps][kPrep], pz[kWarps][kPrep];
+  int pr[kWarps][kPrep];
+};
+
+// Evaluates queue entry `lane` (when `valid`) and adds the warp's batch sum
+// to the warp accumulator (lane 0).
+__device__ __forceinline__ void policy_flush(K2Smem& sm, int warp, int lane, bool valid,
+                                             const Bundle& b, int ray, double d, double vx,
+                                             double vy, double vz, const PolicyParams& p) {
+  Acc a;
+  a.zero();
+  if (valid) policy_accumulate(a, b.dx[ray], b.dy[ray], b.dz[ray], d, vx, vy, vz, p);
+  const bool nz = a.a00 != 0.0 || a.a11 != 0.0 || a.a22 != 0.0 || a.b0 != 0.0 || a.b1 != 0.0 ||
+                  a.b2 != 0.0 || a.a01 != 0.0 || a.a02 != 0.0 || a.a12 != 0.0;
+  if (!__any_sync(0xffffffffu, nz)) return;
+  double v[9] = {a.a00, a.a01, a.a02, a.a11, a.a12, a.a22, a.b0, a.b1, a.b2};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sm.acc[warp][k] += v[k];
+  }
+}
+
+#ifndef RMPB_MINB
+#define RMPB_MINB 4
+#endif
+template <class G, bool RAYOUT>
+__global__ void __launch_bounds__(kBlock, RMPB_MINB)
+k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
+              double eps, double step_scale, int segs, int seg_rays, RayOut ro) {
+  __shared__ K2Smem sm;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned FULL = 0xffffffffu;
+  const unsigned lt = (1u << lane) - 1u;
+  const int unit = blockIdx.x;
+  const int pose = unit / segs, seg = unit - pose * segs;
+  double sx, sy, sz;
+  io.pose(pose, sx, sy, sz);
+  if (lane < 9) sm.acc[warp][lane] = 0.0;
+  const int begin = seg * seg_rays;
+  const int end = min(begin + seg_rays, b.n);
+  const int nchunks = (end - begin + 31) >> 5;
+  double* qt = sm.qt[warp];
+  int* qr = sm.qr[warp];
+
+  int chunk = warp, pcount = 0, phead = 0, qn = 0, cnt = 0, my_steps = 0;
+  int ray = 0, steps = 0;
+  bool alive = false;
+  double dx = 0, dy = 0, dz = 0, t = 0, tend = 0;
+  __syncwarp();
+  while (true) {
+    // ---- refill from the prepared-ray buffer (prepare a chunk when empty)
+    unsigned need = __ballot_sync(FULL, !alive);
+    while (need != 0u && (pcount > 0 || chunk < nchunks)) {
+      if (pcount == 0) {
+        const int r = begin + (chunk << 5) + lane;
+        chunk += kWarps;
+        bool ok = r < end;
+        double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
+        if (ok) {
+          ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
+          ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, b.recip(r), t0, t1);
+          if (ok) {
+            t0 = t0 > 0.0 ? t0 : 0.0;
+            t1 = t1 < max_range ? t1 : max_range;
+            ok = !(t0 > t1);
+          }
+          if (RAYOUT && !ok) {
+            const int o = b.perm ? b.perm[r] : r;
+            ro.t[o] = CUDART_INF;
+            if (ro.cell) { ro.cell[3 * o] = -1; ro.cell[3 * o + 1] = -1; ro.cell[3 * o + 2] = -1; }
+            if (ro.steps) ro.steps[o] = 0;
+          }
+        }
+        const unsigned m = __ballot_sync(FULL, ok);
+        if (ok) {
+          const int pos = __popc(m & lt);
+          sm.pt[warp][pos] = t0; sm.pe[warp][pos] = t1;
+          sm.px[warp][pos] = ex; sm.py[warp][pos] = ey; sm.pz[warp][pos] = ez;
+          sm.pr[warp][pos] = r;
+        }
+        pcount = __popc(m);
+        phead = 0;
+        __syncwarp();
+        continue;
+      }
+      const int rank = __popc(need & lt);
+      if (!alive && rank < pcount) {
+        const int e = phead + rank;
+        t = sm.pt[warp][e]; tend = sm.pe[warp][e];
+        dx = sm.px[warp][e]; dy = sm.py[warp][e]; dz = sm.pz[warp][e];
+        ray = sm.pr[warp][e];
+        alive = true;
+        steps = 0;
+      }
+      const int take = min(pcount, __popc(need));
+      phead += take;
+      pcount -= take;
+      need = __ballot_sync(FULL, !alive);
+    }
+    if (__ballot_sync(FULL, alive) == 0u) break;
+    // ---- one sphere-trace step per live lane
+    bool enq = false;
+    if (alive) {
+      int ix, iy, iz;
+      const double d = interp_fast(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
+      ++steps;
+      bool fin, hit = false;
+      if (d < eps) {
+        hit = true;
+        fin = true;
+      } else {
+        t += step_scale * d;
+        fin = t > tend;
+      }
+      if (fin) {
+        alive = false;
+        my_steps += steps;
+        if (hit) {
+          cnt += 1;  // min_range = 0 for map policies: every hit counts
+          enq = t < p.radius;
+        }
+        if (RAYOUT) {
+          const int o = b.perm ? b.perm[ray] : ray;
+          ro.t[o] = hit ? t : CUDART_INF;
+          if (ro.cell) {
+            ro.cell[3 * o] = hit ? ix : -1; ro.cell[3 * o + 1] = hit ? iy : -1;
+            ro.cell[3 * o + 2] = hit ? iz : -1;
+          }
+          if (ro.steps) ro.steps[o] = steps;
+        }
+      }
+    }
+    // ---- queue policy work; evaluate in full-warp batches of 32
+    const unsigned em = __ballot_sync(FULL, enq);
+    if (em) {
+      if (enq) {
+        const int pos = qn + __popc(em & lt);
+        qt[pos] = t;
+        qr[pos] = ray;
+      }
+      qn += __popc(em);
+      if (qn >= 32) {
+        __syncwarp();
+        double vx, vy, vz;
+        io.vel(pose, vx, vy, vz);
+        policy_flush(sm, warp, lane, true, b, qr[lane], qt[lane], vx, vy, vz, p);
+        __syncwarp();
+        if (lane < qn - 32) { qt[lane] = qt[lane + 32]; qr[lane] = qr[lane + 32]; }
+        qn -= 32;
+        __syncwarp();
+      }
+    }
+  }
+  __syncwarp();
+  if (qn > 0) {
+    double vx, vy, vz;
+    io.vel(pose, vx, vy, vz);
+    const bool valid = lane < qn;
+    policy_flush(sm, warp, lane, valid, b, valid ? qr[lane] : 0, valid ? qt[lane] : 0.0, vx, vy,
+                 vz, p);
+  }
+  if (ro.step_total) {
+    int s = warp_sum_i(my_steps);
+    if (lane == 0) atomicAdd(ro.step_total, (unsigned long long)s);
+  }
+  __syncwarp();
+  Acc acc;
+  acc.zero();
+  if (lane == 0) {
+    acc.a00 = sm.acc[warp][0]; acc.a01 = sm.acc[warp][1]; acc.a02 = sm.acc[warp][2];
+    acc.a11 = sm.acc[warp][3]; acc.a12 = sm.acc[warp][4]; acc.a22 = sm.acc[warp][5];
+    acc.b0 = sm.acc[warp][6]; acc.b1 = sm.acc[warp][7]; acc.b2 = sm.acc[warp][8];
+  }
+  acc.cnt = cnt;
   finish_unit(acc, io, pose, seg, segs);
 }
 
