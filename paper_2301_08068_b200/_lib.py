@@ -19,7 +19,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.environ.get("RMPB_LIBRARY", os.path.join(HERE, "librmpb.so"))
+LIB_PATH = os.environ.get("RMPB_LIBRARY") or os.path.join(HERE, "librmpb.so")
 
 RMPB_OK = 0
 RMPB_ERR_INVALID = -1

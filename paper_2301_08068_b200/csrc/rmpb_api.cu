@@ -657,7 +657,7 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
     if (!v2)
       k_ray_policy<<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
                                                        step_scale, segs, seg_rays, ro);
-    else if (ro.t)
+    else if (ro.t || ro.step_total)
       k_ray_policy2<G, true><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
                                                                  max_range, eps, step_scale, segs,
                                                                  seg_rays, ro);

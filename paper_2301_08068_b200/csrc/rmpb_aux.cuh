@@ -206,7 +206,7 @@ __global__ void k_scene_trace(ScenePack s, double tm, double sx, double sy, doub
     double d = scene_sd(s, tm, sx + t * dx, sy + t * dy, sz + t * dz);
     if (d < eps) { r = t; break; }
     t += step_scale * d;
-    if (t > max_range) break;
+    if (!(t <= max_range)) break;  // NaN-safe form of (t > max_range)
   }
   out[i] = r;
 }

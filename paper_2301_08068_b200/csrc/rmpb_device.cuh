@@ -90,7 +90,7 @@ struct LinearGrid {
   const T* __restrict__ v;
   int sy, sx;  // strides: nz, ny*nz (node counts < 2^31 checked at create)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    const T* b = v + (ix * sx + iy * sy + iz);  // < 2^31 nodes (checked at create)
+    const T* b = v + (unsigned)(ix * sx + iy * sy + iz);  // < 2^31 nodes (checked at create)
     Corners c;
     c.v000 = (double)__ldg(b);           c.v001 = (double)__ldg(b + 1);
     c.v010 = (double)__ldg(b + sy);      c.v011 = (double)__ldg(b + sy + 1);
@@ -104,8 +104,8 @@ struct QuadGridF32 {
   const float4* __restrict__ q;
   int qy, qx;  // strides in quads: (nz-1), (ny-1)*(nz-1)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    const float4* b = q + (ix * qx + iy * qy + iz);
-    float4 a = __ldg(b), c = __ldg(b + qx);
+    const float4* b = q + (unsigned)(ix * qx + iy * qy + iz);
+    float4 a = __ldg(b), c = __ldg(b + (unsigned)qx);
     Corners k;
     k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
     k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;
@@ -180,20 +180,25 @@ __device__ __forceinline__ double interp(const G& grid, const GridGeom& g, doubl
 
 // Cell coordinate of one axis, identical to the reference's
 //   u = clamp(u, 0, n-1); i = min((int64)floor(u), n-2); f = u - (double)i
-// without the XU pipe: u + 2^52 rounds u (< 2^52) to the nearest integer in
-// the low mantissa bits, a compare fixes round-up to floor.  A NaN u (not
-// reachable from finite inputs) yields an in-range index via the int clamp.
-__device__ __forceinline__ void cell_coord(double u, double m, int nm2, double dnm2, int& i,
-                                           double& f) {
-  u = u < 0.0 ? 0.0 : u;  // the reference's compares (not fmin/fmax: no NaN fixups)
-  u = u > m ? m : u;
-  const double big = u + 4503599627370496.0;  // 2^52
-  double r = big - 4503599627370496.0;
+// without the XU pipe and without double selects on the common path:
+// u + 1.5*2^52 rounds u (|u| < 2^31) to the nearest integer, which sits in
+// the low 32 mantissa bits (two's complement); a compare turns round into
+// floor.  i in [0, n-2] then needs no clamp and f = u - floor(u) is exactly
+// the reference's f.  Otherwise u was clamped by the reference: u < 0 gives
+// (i, f) = (0, 0) and u >= n-1 gives (n-2, (n-1)-(n-2) = 1) -- a rarely
+// taken branch (only at the map boundary).  The points traced always lie in
+// the slab interval, so |u| is far below 2^31; NaN is handled by the caller.
+__device__ __forceinline__ void cell_coord(double u, int nm2, int& i, double& f) {
+  const double M = 6755399441055744.0;  // 1.5 * 2^52
+  const double big = u + M;
+  double r = big - M;
   int ri = __double2loint(big);
   if (r > u) { r = r - 1.0; ri -= 1; }
-  if (ri > nm2) { ri = nm2; r = dnm2; }
-  i = ri < 0 ? 0 : ri;
   f = u - r;
+  if ((unsigned)ri > (unsigned)nm2) {
+    if (ri < 0) { ri = 0; f = 0.0; } else { ri = nm2; f = 1.0; }
+  }
+  i = ri;
 }
 
 // interp with exdiv + cell_coord: bit-identical to interp() above.
@@ -201,9 +206,9 @@ template <class G>
 __device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, double px,
                                               double py, double pz, int& ix, int& iy, int& iz) {
   double fx, fy, fz;
-  cell_coord(exdiv(px - g.ox, g.res, g.rhi, g.rlo), g.mx, g.nx - 2, g.dx2, ix, fx);
-  cell_coord(exdiv(py - g.oy, g.res, g.rhi, g.rlo), g.my, g.ny - 2, g.dy2, iy, fy);
-  cell_coord(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), g.mz, g.nz - 2, g.dz2, iz, fz);
+  cell_coord(exdiv(px - g.ox, g.res, g.rhi, g.rlo), g.nx - 2, ix, fx);
+  cell_coord(exdiv(py - g.oy, g.res, g.rhi, g.rlo), g.ny - 2, iy, fy);
+  cell_coord(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), g.nz - 2, iz, fz);
   Corners c = grid.load(ix, iy, iz);
   double c00 = c.v000 + fz * (c.v001 - c.v000);
   double c01 = c.v010 + fz * (c.v011 - c.v010);
@@ -307,7 +312,7 @@ __device__ __forceinline__ TraceResult trace_ray(const G& grid, const GridGeom& 
     ++r.steps;
     if (d < eps) { r.t = t; r.cx = ix; r.cy = iy; r.cz = iz; break; }
     t += step_scale * d;
-    if (t > t_end) break;
+    if (!(t <= t_end)) break;  // NaN-safe form of (t > t_end)
   }
   return r;
 }

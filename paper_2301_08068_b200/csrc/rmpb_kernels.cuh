@@ -190,6 +190,10 @@ __device__ __forceinline__ void policy_flush(K2Smem& sm, int warp, int lane, boo
 #ifndef RMPB_MINB
 #define RMPB_MINB 4
 #endif
+#ifndef RMPB_REFILL
+#define RMPB_REFILL 8  // refill when at least this many lanes are idle (or none alive)
+#endif
+// RAYOUT: per-ray parity outputs (t, cell, steps) and the step counter.
 template <class G, bool RAYOUT>
 __global__ void __launch_bounds__(kBlock, RMPB_MINB)
 k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
@@ -215,8 +219,10 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   double dx = 0, dy = 0, dz = 0, t = 0, tend = 0;
   __syncwarp();
   while (true) {
-    // ---- refill from the prepared-ray buffer (prepare a chunk when empty)
+    // ---- refill from the prepared-ray buffer (prepare a chunk when empty);
+    // only once enough lanes idle, so the refill cost is amortised
     unsigned need = __ballot_sync(FULL, !alive);
+    if (__popc(need) < RMPB_REFILL && need != FULL) need = 0u;
     while (need != 0u && (pcount > 0 || chunk < nchunks)) {
       if (pcount == 0) {
         const int r = begin + (chunk << 5) + lane;
@@ -231,7 +237,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
             t1 = t1 < max_range ? t1 : max_range;
             ok = !(t0 > t1);
           }
-          if (RAYOUT && !ok) {
+          if (RAYOUT && !ok && ro.t) {
             const int o = b.perm ? b.perm[r] : r;
             ro.t[o] = CUDART_INF;
             if (ro.cell) { ro.cell[3 * o] = -1; ro.cell[3 * o + 1] = -1; ro.cell[3 * o + 2] = -1; }
@@ -257,7 +263,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
         dx = sm.px[warp][e]; dy = sm.py[warp][e]; dz = sm.pz[warp][e];
         ray = sm.pr[warp][e];
         alive = true;
-        steps = 0;
+        if (RAYOUT) steps = 0;
       }
       const int take = min(pcount, __popc(need));
       phead += take;
@@ -270,23 +276,23 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     if (alive) {
       int ix, iy, iz;
       const double d = interp_fast(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
-      ++steps;
+      if (RAYOUT) ++steps;
       bool fin, hit = false;
       if (d < eps) {
         hit = true;
         fin = true;
       } else {
         t += step_scale * d;
-        fin = t > tend;
+        fin = !(t <= tend);  // == (t > tend) for numbers; a NaN t ends the ray
       }
       if (fin) {
         alive = false;
-        my_steps += steps;
+        if (RAYOUT) my_steps += steps;
         if (hit) {
           cnt += 1;  // min_range = 0 for map policies: every hit counts
           enq = t < p.radius;
         }
-        if (RAYOUT) {
+        if (RAYOUT && ro.t) {
           const int o = b.perm ? b.perm[ray] : ray;
           ro.t[o] = hit ? t : CUDART_INF;
           if (ro.cell) {
@@ -326,7 +332,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     policy_flush(sm, warp, lane, valid, b, valid ? qr[lane] : 0, valid ? qt[lane] : 0.0, vx, vy,
                  vz, p);
   }
-  if (ro.step_total) {
+  if (RAYOUT && ro.step_total) {
     int s = warp_sum_i(my_steps);
     if (lane == 0) atomicAdd(ro.step_total, (unsigned long long)s);
   }

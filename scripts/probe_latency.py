@@ -24,6 +24,17 @@ for P_ in (1, 2, 8, 64):
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
         e0.record(); eng.evaluate(x, v); e1.record(); e1.synchronize(); ts.append(e0.elapsed_time(e1) * 1e3)
     res[f"kernel_us_P{P_}"] = statistics.median(ts)
+# single-pose kernel time vs max range (fixed overhead vs march)
+for mr in (1e-6, 0.5, 2.0, 5.0, 10.0):
+    e2 = RayPolicyEngine(eng.grid, eng.bundle, params.as_tuple(), mr)
+    x1 = torch.tensor(states[0].position, dtype=torch.float64, device="cuda").view(1, 3)
+    v1 = torch.tensor(states[0].velocity, dtype=torch.float64, device="cuda").view(1, 3)
+    for _ in range(5): e2.evaluate(x1, v1)
+    ts = []
+    for i in range(30):
+        a = torch.cuda.Event(enable_timing=True); b_ = torch.cuda.Event(enable_timing=True)
+        a.record(); e2.evaluate(x1, v1); b_.record(); b_.synchronize(); ts.append(a.elapsed_time(b_) * 1e3)
+    res[f"p1_us_range_{mr}"] = statistics.median(ts)
 # C-ABI host call
 def med(fn, n=200):
     for _ in range(10): fn(0)
