@@ -68,7 +68,7 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "100"],
+                 "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
@@ -113,8 +113,26 @@ def build_world(backend_bake=None, distance=None, total_poses=4096):
 
     scene = synth.c1_scene()
     grid = synth.c1_grid(scene, bake=backend_bake)
+    if distance is None:
+        distance = synth.host_box_distance(scene)  # input synthesis only
     states = synth.bench_states(scene, count=total_poses, seed=123, distance=distance)
     return scene, grid, states
+
+
+def ncu_summary():
+    """Latest committed ncu --set full summary of the hot kernel (profiles/)."""
+    import glob
+
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_ncu_summary.json")))
+    if not files:
+        return None
+    try:
+        with open(files[-1]) as fh:
+            d = json.load(fh)
+        d["file"] = os.path.relpath(files[-1], ROOT)
+        return d
+    except Exception:
+        return None
 
 
 def measured_peaks():
@@ -236,10 +254,16 @@ def run_b200(args):
     peaks, peak_src = measured_peaks()
     algo_bytes = vox_steps * BYTES_PER_STEP
     achieved = algo_bytes / (kern_ms * 1e-3) / 1e9
+    ncu = ncu_summary()
+    traffic = args.ncu_traffic
+    if traffic is None and ncu is not None:
+        traffic = ncu.get("dram_bytes_per_launch")
     roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
-            "traffic": args.ncu_traffic, "peak_source": peak_src,
-            "kernel": "k_ray_policy<QuadGridF32>",
+            "traffic": traffic, "peak_source": peak_src,
+            "traffic_source": (ncu or {}).get("file"),
+            "l2_read_GBps_ncu": (ncu or {}).get("l2_read_GBps"),
+            "kernel": "k_ray_policy2<QuadGridF32>",
             "algorithmic_bytes_per_launch": algo_bytes,
             "voxel_steps_per_launch": vox_steps,
             "note": "bytes = voxel-steps x 8 corners x 4 B (f32 map); map is L2-resident"}

@@ -126,7 +126,8 @@ struct Workspace {
   DevBuf in, in2, in3, out, out2, out3, partials;
   DevBuf tickets;  // zeroed on growth
   size_t tickets_n = 0;
-  HostBuf hres;    // mapped small results (slots / accels)
+  HostBuf hres;    // pinned + mapped results (slots / accels)
+  HostBuf hin;     // pinned staging of host inputs
   int ensure_tickets(size_t n) {
     if (n <= tickets_n) return RMPB_OK;
     TRY(tickets.ensure(n * sizeof(unsigned)));
@@ -777,19 +778,28 @@ extern "C" int rmpb_ray_policy_batch(const rmpb_grid* g, const rmpb_bundle* b, c
   Workspace* ws = workspace(g->device, stream);
   std::lock_guard<std::mutex> lk(ws->mu);
   cudaStream_t st = S(stream);
-  TRY(ws->in.ensure(P * 6 * sizeof(double)));
-  TRY(ws->out.ensure(P * 16 * sizeof(double)));
+  // host buffers -> pinned staging -> one H2D; results D2H into pinned.
+  const size_t in_b = (size_t)P * 6 * sizeof(double), out_b = (size_t)P * 16 * sizeof(double);
+  TRY(ws->hin.ensure(in_b));
+  TRY(ws->hres.ensure(out_b));
+  TRY(ws->in.ensure(in_b));
+  TRY(ws->out.ensure(out_b));
+  double* hx = (double*)ws->hin.p;
+  memcpy(hx, x, (size_t)P * 3 * sizeof(double));
+  memcpy(hx + 3 * P, v, (size_t)P * 3 * sizeof(double));
   double* dx = (double*)ws->in.p;
   double* dv = dx + 3 * P;
   double* ds = (double*)ws->out.p;
   double* da = ds + 13 * P;
-  CK(cudaMemcpyAsync(dx, x, P * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
-  CK(cudaMemcpyAsync(dv, v, P * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(dx, hx, in_b, cudaMemcpyHostToDevice, st));
   TRY(ray_policy_batch_impl(g, b, dx, dv, P, params, max_range, eps, step_scale, ds,
                             out_accel ? da : nullptr, nullptr, ws, st));
-  CK(cudaMemcpyAsync(out_slot, ds, P * 13 * sizeof(double), cudaMemcpyDeviceToHost, st));
-  if (out_accel) CK(cudaMemcpyAsync(out_accel, da, P * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(ws->hres.p, ds, out_accel ? out_b : (size_t)P * 13 * sizeof(double),
+                     cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  const double* ho = (const double*)ws->hres.p;
+  memcpy(out_slot, ho, (size_t)P * 13 * sizeof(double));
+  if (out_accel) memcpy(out_accel, ho + 13 * P, (size_t)P * 3 * sizeof(double));
   return RMPB_OK;
 }
 

@@ -222,7 +222,9 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     // ---- refill from the prepared-ray buffer (prepare a chunk when empty);
     // only once enough lanes idle, so the refill cost is amortised
     unsigned need = __ballot_sync(FULL, !alive);
-    if (__popc(need) < RMPB_REFILL && need != FULL) need = 0u;
+    const bool drained = pcount == 0 && chunk >= nchunks;
+    if (need == FULL && drained) break;
+    if ((__popc(need) < RMPB_REFILL && need != FULL) || drained) need = 0u;
     while (need != 0u && (pcount > 0 || chunk < nchunks)) {
       if (pcount == 0) {
         const int r = begin + (chunk << 5) + lane;
@@ -269,10 +271,11 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
       phead += take;
       pcount -= take;
       need = __ballot_sync(FULL, !alive);
+      if (need == FULL && pcount == 0 && chunk >= nchunks) break;
     }
-    if (__ballot_sync(FULL, alive) == 0u) break;
+    if (need == FULL) break;  // (only reachable once every ray is done)
     // ---- one sphere-trace step per live lane
-    bool enq = false;
+    bool enq = false, hit_now = false;
     if (alive) {
       int ix, iy, iz;
       const double d = interp_fast(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
@@ -287,11 +290,9 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
       }
       if (fin) {
         alive = false;
+        hit_now = hit;
         if (RAYOUT) my_steps += steps;
-        if (hit) {
-          cnt += 1;  // min_range = 0 for map policies: every hit counts
-          enq = t < p.radius;
-        }
+        if (hit) enq = t < p.radius;
         if (RAYOUT && ro.t) {
           const int o = b.perm ? b.perm[ray] : ray;
           ro.t[o] = hit ? t : CUDART_INF;
@@ -304,6 +305,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
       }
     }
     // ---- queue policy work; evaluate in full-warp batches of 32
+    cnt += __popc(__ballot_sync(FULL, hit_now));  // warp-uniform; min_range = 0: every hit counts
     const unsigned em = __ballot_sync(FULL, enq);
     if (em) {
       if (enq) {
@@ -343,8 +345,8 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     acc.a00 = sm.acc[warp][0]; acc.a01 = sm.acc[warp][1]; acc.a02 = sm.acc[warp][2];
     acc.a11 = sm.acc[warp][3]; acc.a12 = sm.acc[warp][4]; acc.a22 = sm.acc[warp][5];
     acc.b0 = sm.acc[warp][6]; acc.b1 = sm.acc[warp][7]; acc.b2 = sm.acc[warp][8];
+    acc.cnt = cnt;  // warp-uniform count: contributed once per warp
   }
-  acc.cnt = cnt;
   finish_unit(acc, io, pose, seg, segs);
 }
 

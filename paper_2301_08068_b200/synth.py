@@ -79,6 +79,28 @@ def bench_states(scene: Scene, count: int = 10, seed: int = 123, clearance: floa
     return out
 
 
+def host_box_distance(scene: Scene):
+    """Scene distance for BENCH INPUT GENERATION ONLY (rejection sampling of
+    start states, never on the evaluated path): a NumPy restatement of the
+    union-of-boxes case of _ckern.pyx:21-56 with the same operation order,
+    so the accept / reject decisions equal the reference's.  Avoids one GPU
+    launch per candidate while synthesising thousands of poses."""
+    pk = scene.packed()
+    if (pk["kinds"] != 1).any() or (pk["ops"] != 0).any() or (pk["velocities"] != 0).any():
+        raise ValueError("host_box_distance handles static union-of-boxes scenes only")
+    c, h, empty = pk["centers"], pk["sizes"], float(pk["empty_dist"])
+
+    def distance(x):
+        x = np.asarray(x, dtype=np.float64).reshape(3)
+        q = np.abs(x - c) - h
+        e = np.maximum(q, 0.0)
+        mx = np.maximum(np.maximum(q[:, 0], q[:, 1]), q[:, 2])
+        dp = np.sqrt(e[:, 0] * e[:, 0] + e[:, 1] * e[:, 1] + e[:, 2] * e[:, 2]) + np.minimum(mx, 0.0)
+        return float(min(empty, dp.min())) if dp.size else empty
+
+    return distance
+
+
 def states_arrays(states) -> tuple[np.ndarray, np.ndarray]:
     x = np.ascontiguousarray([s.position for s in states], dtype=np.float64).reshape(-1, 3)
     v = np.ascontiguousarray([s.velocity for s in states], dtype=np.float64).reshape(-1, 3)
