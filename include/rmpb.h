@@ -206,6 +206,14 @@ RMPB_EXPORT int rmpb_bake(const rmpb_scene* s, double ox, double oy, double oz, 
 /* Bake straight into a device grid; storage RMPB_STORE_F32 ROUNDS to f32. */
 RMPB_EXPORT int rmpb_bake_grid(const rmpb_scene* s, double ox, double oy, double oz, double res, int64_t nx,
                    int64_t ny, int64_t nz, int storage, int layout, int device, rmpb_grid** out);
+/* Truncated bake for TSDF maps (config C5): values clamp(sd, -tau, tau),
+ * brick-culled (exact w.r.t. the unculled bake + clamp); storage F32 rounds
+ * once to f32; layout BRICK (default) stores only bricks != +tau. */
+RMPB_EXPORT int rmpb_bake_grid_tsdf(const rmpb_scene* s, double ox, double oy, double oz, double res,
+                        int64_t nx, int64_t ny, int64_t nz, double tau, int storage, int layout,
+                        int device, rmpb_grid** out);
+/* Node values of any grid back to the host as f64, C-order (nx*ny*nz). */
+RMPB_EXPORT int rmpb_grid_values(const rmpb_grid* g, double* out);
 RMPB_EXPORT int rmpb_esdf_sample(const rmpb_grid* g, const double* pts, int64_t n, double* out_d,
                      double* out_g, uint8_t* out_flag, void* stream);
 

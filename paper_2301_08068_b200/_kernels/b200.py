@@ -149,6 +149,23 @@ class DeviceGrid:
                *[int(d) for d in dims], int(storage), int(layout), scene.device, ctypes.byref(h))
         return cls(tuple(int(d) for d in dims), o, res, device=scene.device, _handle=h)
 
+    @classmethod
+    def bake_tsdf(cls, scene: "DeviceScene", origin, res, dims, tau, storage=L.STORE_F32,
+                  layout=L.LAYOUT_BRICK):
+        """Truncated GPU bake (clamp(sd, -tau, tau)) into a device grid."""
+        h = ctypes.c_void_p()
+        o = np.asarray(origin, dtype=np.float64).reshape(3)
+        L.call("rmpb_bake_grid_tsdf", scene.handle, o[0], o[1], o[2], float(res),
+               *[int(d) for d in dims], float(tau), int(storage), int(layout), scene.device,
+               ctypes.byref(h))
+        return cls(tuple(int(d) for d in dims), o, res, device=scene.device, _handle=h)
+
+    def values(self) -> np.ndarray:
+        """Node values back on the host (f64, C-order), from any layout."""
+        out = np.empty(self.dims, dtype=np.float64)
+        L.call("rmpb_grid_values", self.handle, out.ctypes.data)
+        return out
+
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:

@@ -77,6 +77,8 @@ _SIGS = {
     "rmpb_scene_trace": (_i, [_vp, _vp, _vp, _i64, _d, _d, _d, _d, _vp, _vp]),
     "rmpb_bake": (_i, [_vp, _d, _d, _d, _d, _i64, _i64, _i64, _vp, _vp]),
     "rmpb_bake_grid": (_i, [_vp, _d, _d, _d, _d, _i64, _i64, _i64, _i, _i, _i, _vp]),
+    "rmpb_bake_grid_tsdf": (_i, [_vp, _d, _d, _d, _d, _i64, _i64, _i64, _d, _i, _i, _i, _vp]),
+    "rmpb_grid_values": (_i, [_vp, _vp]),
     "rmpb_esdf_sample": (_i, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
 }
 

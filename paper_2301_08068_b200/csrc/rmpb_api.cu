@@ -5,6 +5,7 @@
 // allocation on the hot path.  Compiled with -fmad=false (see Makefile).
 #include <cuda_runtime.h>
 #include <cub/device/device_radix_sort.cuh>
+#include <cub/device/device_scan.cuh>
 
 #include <atomic>
 #include <cstdarg>
@@ -352,6 +353,81 @@ static int grid_build(rmpb_grid* g, const void* d_src, int dtype, int storage, i
   return RMPB_OK;
 }
 
+// BRICK layout from a device linear array (f32 or f64, C-order).
+template <typename T>
+static int brick_build_t(rmpb_grid* g, const T* d_lin, T fill, cudaStream_t st) {
+  const int nx = (int)g->nx, ny = (int)g->ny, nz = (int)g->nz;
+  const int bnx = (nx + 7) / 8, bny = (ny + 7) / 8, bnz = (nz + 7) / 8;
+  const int nb = bnx * bny * bnz;
+  int *flag = nullptr, *slot = nullptr;
+  CK(cudaMalloc((void**)&flag, (size_t)(nb + 1) * sizeof(int)));
+  CK(cudaMalloc((void**)&slot, (size_t)(nb + 1) * sizeof(int)));
+  k_brick_flags<T><<<nb, 512, 0, st>>>(d_lin, nx, ny, nz, fill, flag);
+  CKL();
+  CK(cudaMemsetAsync(flag + nb, 0, sizeof(int), st));
+  size_t tmpb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmpb, flag, slot, nb + 1, st));
+  void* tmp = nullptr;
+  CK(cudaMalloc(&tmp, tmpb));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmpb, flag, slot, nb + 1, st));
+  g_launches.fetch_add(1);
+  int count = 0;
+  CK(cudaMemcpyAsync(&count, slot + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  cudaFree(tmp);
+  const size_t pool_b = (size_t)(count > 0 ? count : 1) * 512 * sizeof(T);
+  CK(cudaMalloc(&g->d_values, pool_b));
+  CK(cudaMalloc((void**)&g->d_table, (size_t)nb * sizeof(int32_t)));
+  k_brick_fill<T><<<nb, 512, 0, st>>>(d_lin, nx, ny, nz, fill, flag, slot, g->d_table, (T*)g->d_values);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+  cudaFree(flag);
+  cudaFree(slot);
+  g->layout = LAYOUT_BRICK;
+  g->bnx = bnx; g->bny = bny; g->bnz = bnz;
+  g->bricks = count;
+  g->bytes = (int64_t)(pool_b + (size_t)nb * sizeof(int32_t));
+  return RMPB_OK;
+}
+
+// d_src: device linear values (dtype); resolves storage like grid_build.
+static int brick_build(rmpb_grid* g, const void* d_src, int dtype, double fill, int storage,
+                       cudaStream_t st) {
+  const long long n = g->nx * g->ny * g->nz;
+  int store = storage;
+  if (dtype == RMPB_F32) {
+    if (storage == RMPB_STORE_F64) return fail(RMPB_ERR_UNSUPPORTED, "f32 input with f64 storage");
+    store = RMPB_STORE_F32;
+    if ((double)(float)fill != fill)
+      return fail(RMPB_ERR_INVALID, "fill %.17g is not representable in the f32 map", fill);
+  } else if (storage != RMPB_STORE_F64) {
+    int* d_bad;
+    int bad = 0;
+    CK(cudaMallocAsync((void**)&d_bad, sizeof(int), st));
+    CK(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+    k_check_f32<<<grid_blocks(n), 256, 0, st>>>(n, (const double*)d_src, d_bad);
+    CKL();
+    CK(cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CK(cudaFreeAsync(d_bad, st));
+    CK(cudaStreamSynchronize(st));
+    if ((double)(float)fill != fill) bad = 1;
+    if (bad && storage == RMPB_STORE_F32)
+      return fail(RMPB_ERR_INVALID, "STORE_F32 requested but values / fill are not f32-exact");
+    store = bad ? RMPB_STORE_F64 : RMPB_STORE_F32;
+  }
+  g->storage = store;
+  g->fill = fill;
+  if (store == RMPB_STORE_F64) return brick_build_t<double>(g, (const double*)d_src, fill, st);
+  if (dtype == RMPB_F32) return brick_build_t<float>(g, (const float*)d_src, (float)fill, st);
+  float* lin = nullptr;
+  CK(cudaMalloc((void**)&lin, n * sizeof(float)));
+  k_to_f32<<<grid_blocks(n), 256, 0, st>>>(n, (const double*)d_src, lin);
+  CKL();
+  int rc = brick_build_t<float>(g, lin, (float)fill, st);
+  cudaFree(lin);
+  return rc;
+}
+
 static int grid_new(const void* values, bool on_device, int dtype, int64_t nx, int64_t ny,
                     int64_t nz, double ox, double oy, double oz, double res, int storage,
                     int layout, int device, rmpb_grid** out) {
@@ -412,77 +488,96 @@ extern "C" int rmpb_grid_create_brick(const void* values, int dtype, int64_t nx,
   if (!values) return fail(RMPB_ERR_INVALID, "values is NULL");
   if (dtype != RMPB_F32 && dtype != RMPB_F64) return fail(RMPB_ERR_INVALID, "bad dtype %d", dtype);
   TRY(grid_check_dims(nx, ny, nz, res));
-  // Brick construction happens on the host side of the API (a one-off map
-  // ingestion step, like the reference's ESDF load, geometry.py:472-488):
-  // scan bricks, allocate the non-uniform ones, upload pool + table.
-  const int B = 8;
-  const int bnx = (int)((nx + B - 1) / B), bny = (int)((ny + B - 1) / B), bnz = (int)((nz + B - 1) / B);
-  const bool f32in = dtype == RMPB_F32;
-  auto val = [&](int64_t i, int64_t j, int64_t k) -> double {
-    int64_t idx = (i * ny + j) * nz + k;
-    return f32in ? (double)((const float*)values)[idx] : ((const double*)values)[idx];
-  };
-  // storage resolution
-  int store = storage;
-  if (f32in) store = RMPB_STORE_F32;
-  else if (storage != RMPB_STORE_F64) {
-    bool exact = (double)(float)fill == fill;
-    const double* v = (const double*)values;
-    for (int64_t i = 0; exact && i < nx * ny * nz; ++i) exact = ((double)(float)v[i] == v[i]) || v[i] != v[i];
-    if (!exact && storage == RMPB_STORE_F32)
-      return fail(RMPB_ERR_INVALID, "STORE_F32 requested but values are not f32-exact");
-    store = exact ? RMPB_STORE_F32 : RMPB_STORE_F64;
-  }
-  std::vector<int32_t> table((size_t)bnx * bny * bnz, -1);
-  int64_t nb = 0;
-  for (int bi = 0; bi < bnx; ++bi)
-    for (int bj = 0; bj < bny; ++bj)
-      for (int bk = 0; bk < bnz; ++bk) {
-        bool uniform = true;
-        for (int li = 0; li < B && uniform; ++li)
-          for (int lj = 0; lj < B && uniform; ++lj)
-            for (int lk = 0; lk < B && uniform; ++lk) {
-              int64_t i = bi * B + li, j = bj * B + lj, k = bk * B + lk;
-              if (i >= nx || j >= ny || k >= nz) continue;
-              if (!(val(i, j, k) == fill)) uniform = false;
-            }
-        if (!uniform) table[((size_t)bi * bny + bj) * bnz + bk] = (int32_t)nb++;
-      }
-  const size_t esz = store == RMPB_STORE_F32 ? 4 : 8;
-  std::vector<unsigned char> pool((size_t)(nb > 0 ? nb : 1) * 512 * esz);
-  for (int bi = 0; bi < bnx; ++bi)
-    for (int bj = 0; bj < bny; ++bj)
-      for (int bk = 0; bk < bnz; ++bk) {
-        int32_t s = table[((size_t)bi * bny + bj) * bnz + bk];
-        if (s < 0) continue;
-        for (int li = 0; li < B; ++li)
-          for (int lj = 0; lj < B; ++lj)
-            for (int lk = 0; lk < B; ++lk) {
-              int64_t i = bi * B + li, j = bj * B + lj, k = bk * B + lk;
-              double x = (i < nx && j < ny && k < nz) ? val(i, j, k) : fill;
-              size_t o = (size_t)s * 512 + (li << 6 | lj << 3 | lk);
-              if (store == RMPB_STORE_F32) ((float*)pool.data())[o] = (float)x;
-              else ((double*)pool.data())[o] = x;
-            }
-      }
   DeviceGuard dg(device);
   if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
   std::unique_ptr<rmpb_grid> g(new rmpb_grid());
   g->device = device;
   g->nx = nx; g->ny = ny; g->nz = nz;
   g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
-  g->storage = store;
-  g->layout = LAYOUT_BRICK;
-  g->bnx = bnx; g->bny = bny; g->bnz = bnz;
-  g->fill = fill;
-  g->bricks = nb;
-  CK(cudaMalloc(&g->d_values, pool.size()));
-  CK(cudaMemcpy(g->d_values, pool.data(), pool.size(), cudaMemcpyHostToDevice));
-  CK(cudaMalloc((void**)&g->d_table, table.size() * sizeof(int32_t)));
-  CK(cudaMemcpy(g->d_table, table.data(), table.size() * sizeof(int32_t), cudaMemcpyHostToDevice));
-  g->bytes = (int64_t)(pool.size() + table.size() * sizeof(int32_t));
+  const size_t bytes = (size_t)(nx * ny * nz) * (dtype == RMPB_F32 ? 4 : 8);
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  void* tmp = nullptr;
+  int rc = RMPB_OK;
+  if (cudaMalloc(&tmp, bytes) != cudaSuccess) rc = fail(RMPB_ERR_NOMEM, "brick upload alloc");
+  if (rc == RMPB_OK) {
+    cudaMemcpyAsync(tmp, values, bytes, cudaMemcpyHostToDevice, st);
+    rc = brick_build(g.get(), tmp, dtype, fill, storage, st);
+  }
+  cudaStreamSynchronize(st);
+  if (tmp) cudaFree(tmp);
+  cudaStreamDestroy(st);
+  if (rc != RMPB_OK) return rc;
   *out = g.release();
   return RMPB_OK;
+}
+
+extern "C" int rmpb_bake_grid_tsdf(const rmpb_scene* s, double ox, double oy, double oz,
+                                   double res, int64_t nx, int64_t ny, int64_t nz, double tau,
+                                   int storage, int layout, int device, rmpb_grid** out) {
+  if (!s || !out) return fail(RMPB_ERR_INVALID, "NULL scene / out");
+  *out = nullptr;
+  TRY(grid_check_dims(nx, ny, nz, res));
+  if (!(tau > 0.0)) return fail(RMPB_ERR_INVALID, "truncation must be positive");
+  if (layout == RMPB_LAYOUT_AUTO) layout = LAYOUT_BRICK;
+  if (device != s->device) return fail(RMPB_ERR_INVALID, "scene lives on device %d", s->device);
+  const long long n = nx * ny * nz;
+  DeviceGuard dg(device);
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  std::unique_ptr<rmpb_grid> g(new rmpb_grid());
+  g->device = device;
+  g->nx = nx; g->ny = ny; g->nz = nz;
+  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  const bool f32 = storage == RMPB_STORE_F32;
+  void* tmp = nullptr;
+  int rc = RMPB_OK;
+  if (cudaMalloc(&tmp, n * (f32 ? 4 : 8)) != cudaSuccess) rc = fail(RMPB_ERR_NOMEM, "bake alloc");
+  if (rc == RMPB_OK) {
+    const int nb = (int)(((nx + 7) / 8) * ((ny + 7) / 8) * ((nz + 7) / 8));
+    if (f32)
+      k_bake_tsdf<float><<<nb, 512, 0, st>>>(s->pack, ox, oy, oz, res, (int)nx, (int)ny, (int)nz,
+                                             tau, (float*)tmp);
+    else
+      k_bake_tsdf<double><<<nb, 512, 0, st>>>(s->pack, ox, oy, oz, res, (int)nx, (int)ny, (int)nz,
+                                              tau, (double*)tmp);
+    g_launches.fetch_add(1);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = fail(RMPB_ERR_CUDA, "k_bake_tsdf: %s", cudaGetErrorString(e));
+  }
+  if (rc == RMPB_OK) {
+    const double fill = f32 ? (double)(float)tau : tau;
+    if (layout == LAYOUT_BRICK)
+      rc = brick_build(g.get(), tmp, f32 ? RMPB_F32 : RMPB_F64, fill, storage, st);
+    else
+      rc = grid_build(g.get(), tmp, f32 ? RMPB_F32 : RMPB_F64, storage, layout, st);
+  }
+  cudaStreamSynchronize(st);
+  if (tmp) cudaFree(tmp);
+  cudaStreamDestroy(st);
+  if (rc != RMPB_OK) return rc;
+  *out = g.release();
+  return RMPB_OK;
+}
+
+/* Copy a grid's node values back to the host as f64 C-order (any layout). */
+extern "C" int rmpb_grid_values(const rmpb_grid* g, double* out) {
+  if (!g || !out) return fail(RMPB_ERR_INVALID, "NULL grid / out");
+  DeviceGuard dg(g->device);
+  const long long n = g->nx * g->ny * g->nz;
+  double* d = nullptr;
+  CK(cudaMalloc((void**)&d, n * sizeof(double)));
+  int rc = with_grid(g, [&](auto acc) -> int {
+    k_grid_values<<<grid_blocks(n), 256>>>(acc, (int)g->nx, (int)g->ny, (int)g->nz, d);
+    CKL();
+    return RMPB_OK;
+  });
+  if (rc == RMPB_OK) {
+    cudaError_t e = cudaMemcpy(out, d, n * sizeof(double), cudaMemcpyDeviceToHost);
+    if (e != cudaSuccess) rc = fail(RMPB_ERR_CUDA, "grid values copy: %s", cudaGetErrorString(e));
+  }
+  cudaFree(d);
+  return rc;
 }
 
 extern "C" int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype) {

@@ -194,6 +194,154 @@ __global__ void k_bake(ScenePack s, double ox, double oy, double oz, double res,
   }
 }
 
+// Truncated bake for TSDF maps (config C5): value = clamp(sd, -tau, tau),
+// one CTA per 8^3 brick.  The CTA first collects the primitives whose
+// bounding box lies within tau (+ margin) of the brick, then every node
+// evaluates only those, in scene order.  Exact w.r.t. the unculled bake
+// followed by the clamp: a culled primitive has |dp| > tau at every node of
+// the brick, so it can only move values that the clamp saturates anyway.
+template <typename T>
+__global__ void __launch_bounds__(512)
+k_bake_tsdf(ScenePack s, double ox, double oy, double oz, double res, int nx, int ny, int nz,
+            double tau, T* __restrict__ out) {
+  __shared__ int cand[2048];
+  __shared__ int ncand;
+  const int bnz = (nz + 7) >> 3, bny = (ny + 7) >> 3;
+  const int bid = blockIdx.x;
+  const int bk = bid % bnz, bj = (bid / bnz) % bny, bi = bid / (bnz * bny);
+  const int li = threadIdx.x >> 6, lj = (threadIdx.x >> 3) & 7, lk = threadIdx.x & 7;
+  const int i = bi * 8 + li, j = bj * 8 + lj, k = bk * 8 + lk;
+  // brick AABB in world coordinates (nodes bi*8 .. bi*8+7)
+  const double lo[3] = {ox + res * (double)(bi * 8), oy + res * (double)(bj * 8),
+                        oz + res * (double)(bk * 8)};
+  const double hi[3] = {ox + res * (double)(bi * 8 + 7), oy + res * (double)(bj * 8 + 7),
+                        oz + res * (double)(bk * 8 + 7)};
+  const double margin = tau + 1e-6 + 1e-9 * fabs(res);
+  if (threadIdx.x == 0) ncand = 0;
+  __syncthreads();
+  bool overflow = false;
+  for (int base = 0; base < s.n; base += blockDim.x) {
+    const int p = base + threadIdx.x;
+    bool near = false;
+    if (p < s.n) {
+      double d2 = 0.0;
+      for (int a = 0; a < 3; ++a) {
+        double c = s.centers[3 * p + a];
+        double h = s.kinds[p] == 0 ? s.sizes[3 * p] : s.sizes[3 * p + a];
+        double plo = c - h, phi = c + h;
+        double gap = fmax(fmax(plo - hi[a], lo[a] - phi), 0.0);
+        d2 += gap * gap;
+      }
+      near = d2 <= margin * margin;
+    }
+    // ordered compaction (warp ballots in warp order keeps scene order)
+    const unsigned m = __ballot_sync(0xffffffffu, near);
+    __shared__ int wcount[16];
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    if (lane == 0) wcount[w] = __popc(m);
+    __syncthreads();
+    int off = 0;
+    for (int q = 0; q < w; ++q) off += wcount[q];
+    int total = 0;
+    for (int q = 0; q < (int)(blockDim.x >> 5); ++q) total += wcount[q];
+    if (near) {
+      int pos = ncand + off + __popc(m & ((1u << lane) - 1u));
+      if (pos < 2048) cand[pos] = p;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) ncand += total;
+    __syncthreads();
+  }
+  overflow = ncand > 2048;
+  if (i >= nx || j >= ny || k >= nz) return;
+  const double px = ox + res * (double)i, py = oy + res * (double)j, pz = oz + res * (double)k;
+  double d;
+  if (overflow) {
+    d = scene_sd(s, 0.0, px, py, pz);
+  } else {
+    d = s.empty;
+    for (int c = 0; c < ncand; ++c) {
+      const int q = cand[c];
+      double dx = px - (s.centers[3 * q] + s.vels[3 * q] * 0.0);
+      double dy = py - (s.centers[3 * q + 1] + s.vels[3 * q + 1] * 0.0);
+      double dz = pz - (s.centers[3 * q + 2] + s.vels[3 * q + 2] * 0.0);
+      double dp;
+      if (s.kinds[q] == 0) {
+        dp = sqrt(dx * dx + dy * dy + dz * dz) - s.sizes[3 * q];
+      } else {
+        double qx = fabs(dx) - s.sizes[3 * q];
+        double qy = fabs(dy) - s.sizes[3 * q + 1];
+        double qz = fabs(dz) - s.sizes[3 * q + 2];
+        double ex = qx > 0.0 ? qx : 0.0, ey = qy > 0.0 ? qy : 0.0, ez = qz > 0.0 ? qz : 0.0;
+        double mx = qx;
+        if (qy > mx) mx = qy;
+        if (qz > mx) mx = qz;
+        dp = sqrt(ex * ex + ey * ey + ez * ez) + (mx < 0.0 ? mx : 0.0);
+      }
+      if (s.ops[q] == 0) { if (dp < d) d = dp; }
+      else { if (-dp > d) d = -dp; }
+    }
+  }
+  d = d < -tau ? -tau : (d > tau ? tau : d);
+  out[((long long)i * ny + j) * nz + k] = (T)d;
+}
+
+// ---------------------------------------------------------------------------
+// BRICK layout builder on device (block-hashed TSDF): flag bricks holding any
+// value != fill, exclusive-scan the flags into slots, scatter the bricks.
+template <typename T>
+__global__ void __launch_bounds__(512)
+k_brick_flags(const T* __restrict__ v, int nx, int ny, int nz, T fill, int* __restrict__ flag) {
+  const int bnz = (nz + 7) >> 3, bny = (ny + 7) >> 3;
+  const int bid = blockIdx.x;
+  const int bk = bid % bnz, bj = (bid / bnz) % bny, bi = bid / (bnz * bny);
+  const int i = bi * 8 + (threadIdx.x >> 6), j = bj * 8 + ((threadIdx.x >> 3) & 7),
+            k = bk * 8 + (threadIdx.x & 7);
+  bool diff = false;
+  if (i < nx && j < ny && k < nz) {
+    T x = v[((long long)i * ny + j) * nz + k];
+    diff = !(x == fill);
+  }
+  int any = __syncthreads_or(diff);
+  if (threadIdx.x == 0) flag[bid] = any ? 1 : 0;
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512)
+k_brick_fill(const T* __restrict__ v, int nx, int ny, int nz, T fill, const int* __restrict__ flag,
+             const int* __restrict__ slot, int* __restrict__ table, T* __restrict__ pool) {
+  const int bnz = (nz + 7) >> 3, bny = (ny + 7) >> 3;
+  const int bid = blockIdx.x;
+  const int bk = bid % bnz, bj = (bid / bnz) % bny, bi = bid / (bnz * bny);
+  if (threadIdx.x == 0) table[bid] = flag[bid] ? slot[bid] : -1;
+  if (!flag[bid]) return;
+  const int li = threadIdx.x >> 6, lj = (threadIdx.x >> 3) & 7, lk = threadIdx.x & 7;
+  const int i = bi * 8 + li, j = bj * 8 + lj, k = bk * 8 + lk;
+  T x = (i < nx && j < ny && k < nz) ? v[((long long)i * ny + j) * nz + k] : fill;
+  pool[(long long)slot[bid] * 512 + ((li << 6) | (lj << 3) | lk)] = x;
+}
+
+// Node values back out of any layout (test / export path): node (i,j,k) is
+// corner v000 of cell (i,j,k), or a v1xx / vx1x / vxx1 corner at the far faces.
+template <class G>
+__global__ void k_grid_values(G grid, int nx, int ny, int nz, double* __restrict__ out) {
+  long long n = (long long)nx * ny * nz;
+  long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; idx < n; idx += stride) {
+    int k = (int)(idx % nz);
+    long long r = idx / nz;
+    int j = (int)(r % ny);
+    int i = (int)(r / ny);
+    int ci = min(i, nx - 2), cj = min(j, ny - 2), ck = min(k, nz - 2);
+    Corners c = grid.load(ci, cj, ck);
+    int a = i - ci, b = j - cj, d = k - ck;
+    double v = a ? (b ? (d ? c.v111 : c.v110) : (d ? c.v101 : c.v100))
+                 : (b ? (d ? c.v011 : c.v010) : (d ? c.v001 : c.v000));
+    out[idx] = v;
+  }
+}
+
 // scene_trace (_ckern.pyx:251-273): from t = 0, no box clip.
 __global__ void k_scene_trace(ScenePack s, double tm, double sx, double sy, double sz,
                               const double* __restrict__ dirs, int n, double max_range, double eps,

@@ -52,6 +52,44 @@ def c1_grid(scene: Scene | None = None, bake=None) -> EsdfGrid:
     return EsdfGrid(np.zeros(3), C1_RES, C1_DIMS, vals)
 
 
+# C5: 50 x 50 x 10 m @ 0.05 m (1000 x 1000 x 200 nodes), random boxes at the
+# C1 density (200 boxes per 19.9 x 19.9 x 9.9 m), TSDF truncation 4 voxels.
+C5_RES = 0.05
+C5_DIMS = (1000, 1000, 200)
+C5_ORIGIN = np.zeros(3)
+C5_HI = np.array([49.95, 49.95, 9.95])
+C5_TAU = 0.2
+
+
+def c5_scene(seed: int = 1) -> Scene:
+    ratio = float(np.prod(C5_HI) / np.prod(C1_HI))
+    return c1_scene(n_boxes=int(round(200 * ratio)), seed=seed, lo=C5_ORIGIN, hi=C5_HI)
+
+
+def c5_grids(scene: Scene):
+    """(dense QUAD grid, block-hashed BRICK grid, info) of the f32 TSDF,
+    baked on the device (clamp(sd, -tau, tau), rounded once to f32)."""
+    from . import _lib as L
+    from ._kernels import b200
+
+    ds = b200.device_scene(scene.packed())
+    brick = b200.DeviceGrid.bake_tsdf(ds, C5_ORIGIN, C5_RES, C5_DIMS, C5_TAU,
+                                      storage=L.STORE_F32, layout=L.LAYOUT_BRICK)
+    dense = b200.DeviceGrid.bake_tsdf(ds, C5_ORIGIN, C5_RES, C5_DIMS, C5_TAU,
+                                      storage=L.STORE_F32, layout=L.LAYOUT_QUAD)
+    nb = int(np.prod([(d + 7) // 8 for d in C5_DIMS]))
+    info = {"bricks_allocated": brick.bricks, "bricks_total": nb,
+            "brick_bytes": brick.device_bytes, "dense_quad_bytes": dense.device_bytes}
+    return dense, brick, info
+
+
+def c5_values_host(scene: Scene, grid=None) -> np.ndarray:
+    """The exact C5 node values (f64, f32-exact) for the CPU oracle."""
+    if grid is None:
+        grid = c5_grids(scene)[1]
+    return grid.values()
+
+
 def grid_sha_prefix(grid: EsdfGrid) -> str:
     return hashlib.sha256(grid.values.astype(np.float32).tobytes()).hexdigest()[:16]
 

@@ -1,0 +1,287 @@
+#!/usr/bin/env python3
+"""Secondary measurements for BASELINE.json configs C2 (ray-count x range
+sweep), C3 (LiDAR-direct 128x1024 scans) and C5 (1000x1000x200 block-hashed
+TSDF, 1 M rays per pose, ray split) on ONE B200, each beside the reference's
+CPU path timed on the box's host cores (bounded samples).  One JSON object
+per line on stdout.  bench.py stays the driver contract; this script is the
+evidence for the other rows of SURVEY.md §8.
+
+usage: python scripts/bench_configs.py [--only c2,c3,c5] [--quick]
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.join(ROOT, "oracle"))
+
+STATIC = (88.0, 1.4, 140.0, 1.2, 1e-6, 2.4, 0.2)
+LIDAR = (1.2, 1.5, 3.0, 1.0, 1e-6, 1.3, 1.0)
+
+
+def ev_time(fn, reps=3, flush=None):
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        if flush is not None:
+            flush.zero_()
+        a = torch.cuda.Event(enable_timing=True)
+        b = torch.cuda.Event(enable_timing=True)
+        a.record()
+        fn()
+        b.record()
+        b.synchronize()
+        ts.append(a.elapsed_time(b))
+    return min(ts), statistics.median(ts)
+
+
+def wall_med(fn, n=50):
+    for _ in range(5):
+        fn(0)
+    ts = []
+    for i in range(n):
+        t0 = time.perf_counter()
+        fn(i)
+        ts.append(time.perf_counter() - t0)
+    return statistics.median(ts)
+
+
+def cpu_threads():
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+def c2(args, out):
+    import torch
+
+    import oracle as O
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200._kernels import b200
+    from paper_2301_08068_b200.device import RayPolicyEngine
+
+    scene = synth.c1_scene()
+    grid = synth.c1_grid(scene)
+    dist = synth.host_box_distance(scene)
+    ns = [4096, 16384, 65536, 262144, 1048576]
+    ranges = [2.0, 5.0, 10.0, 20.0]
+    if args.quick:
+        ns, ranges = [4096, 65536, 1048576], [2.0, 10.0]
+    states = synth.bench_states(scene, count=8192, seed=123, distance=dist)
+    xa, va = synth.states_arrays(states)
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    threads = cpu_threads()
+    pool = O.RefPool(threads) if O.ref_available() else None
+    dg = b200.DeviceGrid(grid.values, grid.origin, grid.resolution)
+    for n in ns:
+        bundle = b200.DeviceBundle(halton_n=n)
+        dirs_ref = O.sample_directions(n)
+        P = max(1, min(8192, (1 << 28) // n))
+        x = torch.from_numpy(xa[:P].copy()).cuda()
+        v = torch.from_numpy(va[:P].copy()).cuda()
+        for mr in ranges:
+            eng = RayPolicyEngine(dg, bundle, STATIC, mr)
+            ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+            eng.evaluate(x, v, step_counter=ctr)
+            torch.cuda.synchronize()
+            steps = int(ctr.item())
+            best, med = ev_time(lambda: eng.evaluate(x, v), reps=3, flush=flush)
+            x1, v1 = x[:1].contiguous(), v[:1].contiguous()
+            lat_best, lat_med = ev_time(lambda: eng.evaluate(x1, v1), reps=20)
+            rec = {"config": "C2", "rays": n, "max_range_m": mr, "poses_per_launch": P,
+                   "ms_per_launch": round(med, 4), "rays_per_s": round(P * n / (med * 1e-3), 1),
+                   "hz_throughput": round(P / (med * 1e-3), 1),
+                   "voxel_steps_per_s": round(steps / (med * 1e-3), 1),
+                   "steps_per_ray": round(steps / (P * n), 3),
+                   "single_pose_kernel_us_events": round(lat_med * 1e3, 1)}
+            if pool is not None:
+                k = 0
+                t0 = time.perf_counter()
+                while True:
+                    st = states[k % len(states)]
+                    O.ref_ray_policy(grid.values, grid.origin, grid.resolution, st.position,
+                                     st.velocity, dirs_ref, STATIC, mr, pool)
+                    k += 1
+                    el = time.perf_counter() - t0
+                    if el > (1.0 if args.quick else 3.0) or k >= 200:
+                        break
+                rec["cpu_reference"] = {"rays_per_s": round(k * n / el, 1),
+                                        "hz": round(k / el, 2), "threads": threads,
+                                        "sample": f"{k} poses"}
+            print(json.dumps(rec), flush=True)
+            out.append(rec)
+    if pool is not None:
+        pool.close()
+
+
+def c3(args, out):
+    import torch
+
+    import oracle as O
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200.device import lidar_policy_batch_device
+    from paper_2301_08068_b200.policies import lidar_policy, preset
+    from paper_2301_08068_b200.rays import scan_pattern
+
+    scene = synth.c1_scene()
+    states = synth.bench_states(scene, count=10, seed=123,
+                                distance=synth.host_box_distance(scene))
+    scans = synth.lidar_scans(scene, states, 128, 1024, 20.0)
+    lp = preset("lidar").obstacle
+    n = 128 * 1024
+    # single scan through the public API (host buffers, lattice cached on device)
+    lat = wall_med(lambda i: lidar_policy(states[i % 10].velocity, scans[i % 10], lp), n=100)
+    # throughput: S scans per launch, device resident
+    S = 1024
+    dirs = torch.from_numpy(np.ascontiguousarray(scan_pattern(128, 1024))).cuda()
+    rg = torch.from_numpy(np.stack([scans[i % 10].ranges for i in range(S)])).cuda()
+    vl = torch.from_numpy(np.stack([scans[i % 10].valid for i in range(S)]).astype(np.uint8)).cuda()
+    R = torch.eye(3, dtype=torch.float64, device="cuda").reshape(1, 9).repeat(S, 1).contiguous()
+    v = torch.from_numpy(np.stack([states[i % 10].velocity for i in range(S)])).cuda()
+    flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+    best, med = ev_time(lambda: lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3),
+                        reps=5, flush=flush)
+    beam_bytes = 8 + 1  # range f64 + valid u8 per beam (lattice L2-resident)
+    gbs = S * n * beam_bytes / (med * 1e-3) / 1e9
+    rec = {"config": "C3", "beams_per_scan": n, "scans_per_launch": S,
+           "ms_per_launch": round(med, 4), "scans_per_s": round(S / (med * 1e-3), 1),
+           "beams_per_s": round(S * n / (med * 1e-3), 1),
+           "stream_GBps": round(gbs, 1), "hbm_frac": round(gbs / 6541.8, 3),
+           "single_scan_api_us_median": round(lat * 1e6, 1),
+           "single_scan_hz": round(1.0 / lat, 1)}
+    if O.ref_available():
+        pool = O.RefPool(cpu_threads())
+        wd = [np.ascontiguousarray(s.world_directions()) for s in scans]
+
+        def ref_one(i):
+            s = scans[i % 10]
+            O.ref_lidar_policy(wd[i % 10], s.ranges, s.valid, states[i % 10].velocity, LIDAR, 0.3,
+                               pool)
+        lat_ref = wall_med(ref_one, n=30)
+        pool.close()
+        pool1 = O.RefPool(1)
+
+        def ref_one1(i):
+            s = scans[i % 10]
+            O.ref_lidar_policy(wd[i % 10], s.ranges, s.valid, states[i % 10].velocity, LIDAR, 0.3,
+                               pool1)
+        lat_ref1 = wall_med(ref_one1, n=30)
+        rec["cpu_reference"] = {"single_scan_ms_median_all_threads": round(lat_ref * 1e3, 3),
+                                "single_scan_ms_median_1_thread": round(lat_ref1 * 1e3, 3),
+                                "threads": cpu_threads(),
+                                "note": "rmpnav lidar_policy reduce with world dirs precomputed"}
+    print(json.dumps(rec), flush=True)
+    out.append(rec)
+
+
+def c5(args, out):
+    import torch
+
+    import oracle as O
+    from paper_2301_08068_b200 import _lib as L, synth
+    from paper_2301_08068_b200._kernels import b200
+    from paper_2301_08068_b200.device import RayPolicyEngine
+    from paper_2301_08068_b200.parallel import balanced_range
+
+    t0 = time.perf_counter()
+    scene = synth.c5_scene()
+    dg_dense, dg_brick, info = synth.c5_grids(scene)
+    bake_s = time.perf_counter() - t0
+    states = synth.bench_states(scene, count=8, seed=123,
+                                distance=synth.host_box_distance(scene))
+    n = 1 << 20
+    bundle = b200.DeviceBundle(halton_n=n)
+    rec = {"config": "C5", "dims": list(synth.C5_DIMS), "res_m": synth.C5_RES,
+           "boxes": len(scene.primitives), "tau_m": synth.C5_TAU, "rays": n,
+           "bake_and_build_s": round(bake_s, 2), **info}
+    res = {}
+    for name, dg in (("dense_quad", dg_dense), ("brick", dg_brick)):
+        eng = RayPolicyEngine(dg, bundle, STATIC, 10.0)
+        x = torch.from_numpy(np.stack([s.position for s in states])).cuda()
+        v = torch.from_numpy(np.stack([s.velocity for s in states])).cuda()
+        ctr = torch.zeros(1, dtype=torch.int64, device="cuda")
+        eng.evaluate(x, v, step_counter=ctr)
+        torch.cuda.synchronize()
+        best, med = ev_time(lambda: eng.evaluate(x, v), reps=3)
+        x1, v1 = x[0].contiguous(), v[0].contiguous()
+        one_best, one_med = ev_time(lambda: eng.evaluate(x1.view(1, 3), v1.view(1, 3)), reps=10)
+        # 8-way ray split of one pose: per-GPU share and the fixed-order fold
+        shares = []
+        parts = []
+        for r in range(8):
+            b_, e_ = balanced_range(n, 8, r)
+            sb, sm = ev_time(lambda: eng.partial(x1, v1, b_, e_), reps=5)
+            shares.append(sm)
+            parts.append(eng.partial(x1, v1, b_, e_))
+        slot_split, acc_split = eng.resolve(torch.stack(parts))
+        slot_whole, acc_whole = eng.evaluate(x1.view(1, 3), v1.view(1, 3))
+        torch.cuda.synchronize()
+        sw, aw = slot_whole[0].cpu().numpy(), acc_whole[0].cpu().numpy()
+        ss, as_ = slot_split.cpu().numpy(), acc_split.cpu().numpy()
+        res[name] = {"ms_per_launch_8_poses": round(med, 3),
+                     "rays_per_s": round(8 * n / (med * 1e-3), 1),
+                     "voxel_steps_per_s": round(int(ctr.item()) / (med * 1e-3), 1),
+                     "steps_per_ray": round(int(ctr.item()) / (8 * n), 3),
+                     "single_pose_ms": round(one_med, 3),
+                     "ray_split_8_share_ms_max": round(max(shares), 3),
+                     "split_vs_whole_rel": float(np.abs(ss[:12] - sw[:12]).max() /
+                                                 max(1e-300, np.abs(sw[:12]).max())),
+                     "split_n_hits_equal": bool(ss[12] == sw[12])}
+    rec["gpu"] = res
+    # parity of the block-hashed map vs the dense map and the CPU oracle on a
+    # sample of the pose's rays
+    x0 = states[0].position
+    samp = np.ascontiguousarray(O.sample_directions(4096))
+    tb, cb, _ = b200.grid_trace_ex(dg_brick, synth.C5_ORIGIN, synth.C5_RES, x0, samp, 10.0,
+                                   0.5 * synth.C5_RES, 0.9, with_cells=True)
+    td, cd, _ = b200.grid_trace_ex(dg_dense, synth.C5_ORIGIN, synth.C5_RES, x0, samp, 10.0,
+                                   0.5 * synth.C5_RES, 0.9, with_cells=True)
+    rec["brick_vs_dense_bit_exact"] = bool(np.array_equal(tb, td) and np.array_equal(cb, cd))
+    if args.oracle_c5:
+        vals = synth.c5_values_host(scene)
+        tr, cr = O.grid_trace(vals, synth.C5_ORIGIN, synth.C5_RES, x0, samp, 10.0,
+                              0.5 * synth.C5_RES, 0.9, with_cells=True, workers=cpu_threads())
+        rec["brick_vs_oracle_bit_exact"] = bool(np.array_equal(tb, tr) and np.array_equal(cb, cr))
+        if O.ref_available():
+            pool = O.RefPool(cpu_threads())
+            st = states[0]
+            k = 0
+            t1 = time.perf_counter()
+            dirs_ref = O.sample_directions(n)
+            O.ref_ray_policy(vals, synth.C5_ORIGIN, synth.C5_RES, st.position, st.velocity,
+                             dirs_ref, STATIC, 10.0, pool)
+            el = time.perf_counter() - t1
+            pool.close()
+            rec["cpu_reference_1pose_s"] = round(el, 3)
+            rec["cpu_reference_threads"] = cpu_threads()
+    print(json.dumps(rec), flush=True)
+    out.append(rec)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--only", default="c2,c3,c5")
+    ap.add_argument("--quick", action="store_true")
+    ap.add_argument("--oracle-c5", action="store_true",
+                    help="also check C5 against the dense CPU oracle (needs ~1 GB host RAM)")
+    args = ap.parse_args()
+    out = []
+    for name in args.only.split(","):
+        {"c2": c2, "c3": c3, "c5": c5}[name.strip()](args, out)
+
+
+if __name__ == "__main__":
+    main()

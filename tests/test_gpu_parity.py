@@ -389,3 +389,41 @@ def test_device_halton_close_to_reference(be, oracle):
     assert d.shape == r.shape
     assert np.abs(d - r).max() <= 1e-15  # libdevice vs NumPy SIMD trig: a few ulp
     assert np.allclose(np.linalg.norm(d, axis=1), 1.0, atol=1e-12)
+
+
+def test_tsdf_bake_bricks_and_readback(be, oracle):
+    """Truncated (TSDF) GPU bake: brick-culled bake == clamp of the full
+    oracle bake; BRICK / QUAD / LINEAR layouts read back the same nodes and
+    trace bit-identically to the oracle on the dense values."""
+    from paper_2301_08068_b200 import _lib as L, synth
+
+    scene = synth.c1_scene(n_boxes=60, seed=4, hi=np.array([6.35, 4.75, 3.15]))
+    dims, res, tau = (128, 96, 64), 0.05, 0.2
+    ds = be.device_scene(scene.packed())
+    brick = be.DeviceGrid.bake_tsdf(ds, np.zeros(3), res, dims, tau, storage=L.STORE_F32,
+                                    layout=L.LAYOUT_BRICK)
+    quad = be.DeviceGrid.bake_tsdf(ds, np.zeros(3), res, dims, tau, storage=L.STORE_F32,
+                                   layout=L.LAYOUT_QUAD)
+    full = oracle.bake_values(scene.packed(), np.zeros(3), res, dims, workers=8)
+    want = np.clip(full, -tau, tau).astype(np.float32).astype(np.float64)
+    vb, vq = brick.values(), quad.values()
+    assert np.array_equal(vb, want) and np.array_equal(vq, want)
+    assert 0 < brick.bricks < np.prod([(d + 7) // 8 for d in dims])
+    lin = be.DeviceGrid(want, np.zeros(3), res, layout=L.LAYOUT_LINEAR)
+    assert np.array_equal(lin.values(), want)
+    rng = np.random.default_rng(9)
+    dirs = rng.normal(size=(8192, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    start = np.array([3.1, 2.2, 1.5])
+    t_r, c_r = oracle.grid_trace(want, np.zeros(3), res, start, dirs, 6.0, 0.5 * res, 0.9,
+                                 with_cells=True)
+    for g in (brick, quad, lin):
+        t, c, _ = be.grid_trace_ex(g, np.zeros(3), res, start, dirs, 6.0, 0.5 * res, 0.9,
+                                   with_cells=True)
+        assert np.array_equal(t, t_r) and np.array_equal(c, c_r)
+    # fused policy on the brick map == oracle
+    v = np.array([0.5, -0.4, 0.2])
+    slot, acc = be.ray_policy_fused(brick, np.zeros(3), res, start, v, dirs, STATIC_MAP, 6.0,
+                                    0.5 * res, 0.9)
+    slot_r = oracle.policy_slot(dirs, t_r, v, STATIC_MAP)
+    check_policy(slot, acc, slot_r, oracle.accel_from_slot(slot_r))
