@@ -217,6 +217,28 @@ RMPB_EXPORT int rmpb_grid_values(const rmpb_grid* g, double* out);
 RMPB_EXPORT int rmpb_esdf_sample(const rmpb_grid* g, const double* pts, int64_t n, double* out_d,
                      double* out_g, uint8_t* out_flag, void* stream);
 
+/* ---- batched closed-loop rollouts on device (row f1; sim.py:155-306) ----- */
+/* P robots from start[P*3] toward goal[P*3] on one map / bundle / scene:
+ * per tick the collision / goal / time-out / stuck checks, the fused ray
+ * policy, combine with the goal attractor {alpha, beta, c}, the |a| clamp
+ * and the semi-implicit Euler step run on the GPU with no host round trip.
+ * cfg = {dt, max_time, robot_radius, goal_tolerance, max_accel,
+ * stuck_window, stuck_speed, max_range, hold_mode} (RolloutConfig,
+ * sim.py:102-134).  record_ticks > 0 keeps (x, v, accel) of the first ticks. */
+typedef struct rmpb_rollout rmpb_rollout;
+RMPB_EXPORT int rmpb_rollout_create(const rmpb_grid* g, const rmpb_bundle* b, const rmpb_scene* scene,
+                        int64_t P, const double* start, const double* goal,
+                        const double attractor[3], const double params[7], const double cfg[9],
+                        int64_t record_ticks, rmpb_rollout** out);
+/* Advance up to max_ticks control ticks (stops early once every robot is done). */
+RMPB_EXPORT int rmpb_rollout_run(rmpb_rollout* r, int64_t max_ticks, int64_t* active_left, void* stream);
+/* outcome: 0 running, 1 SUCCESS, 2 COLLISION, 3 TIMEOUT, 4 STUCK (sim.py:51-55). */
+RMPB_EXPORT int rmpb_rollout_result(const rmpb_rollout* r, int32_t* outcome, int64_t* steps,
+                        int64_t* n_clamped, double* x, double* v);
+/* rec: P x (record_ticks + 1) x 9 doubles (x, v, accel per tick). */
+RMPB_EXPORT int rmpb_rollout_trajectory(const rmpb_rollout* r, double* rec);
+RMPB_EXPORT int rmpb_rollout_destroy(rmpb_rollout* r);
+
 #ifdef __cplusplus
 }
 #endif

@@ -21,6 +21,7 @@
 #include "../../include/rmpb.h"
 #include "rmpb_aux.cuh"
 #include "rmpb_kernels.cuh"
+#include "rmpb_rollout.cuh"
 
 using namespace rmpb;
 
@@ -828,7 +829,7 @@ static int ray_policy_batch_impl(const rmpb_grid* g, const rmpb_bundle* b, const
                                  const double* d_v, int64_t P, const double params[7],
                                  double max_range, double eps, double step_scale, double* d_slot,
                                  double* d_accel, uint64_t* step_total, Workspace* ws,
-                                 cudaStream_t st) {
+                                 cudaStream_t st, const int* d_active = nullptr) {
   int segs, seg_rays;
   choose_segments(P, b->n, &segs, &seg_rays);
   if (segs > 1) {
@@ -839,6 +840,7 @@ static int ray_policy_batch_impl(const rmpb_grid* g, const rmpb_bundle* b, const
   io.x = d_x; io.v = d_v; io.slot = d_slot; io.accel = d_accel;
   io.partials = (double*)ws->partials.p;
   io.tickets = (unsigned*)ws->tickets.p;
+  io.active = d_active;
   RayOut ro{};
   ro.step_total = (unsigned long long*)step_total;
   return launch_ray_policy(g, b, io, P, make_params(params, 0.0), max_range, eps, step_scale, segs,
@@ -1393,5 +1395,162 @@ extern "C" int rmpb_esdf_sample(const rmpb_grid* g, const double* pts, int64_t n
   CK(cudaMemcpyAsync(out_g, og, n * 3 * sizeof(double), cudaMemcpyDeviceToHost, st));
   CK(cudaMemcpyAsync(out_flag, of, n, cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// batched closed-loop rollouts (row f1)
+
+struct rmpb_rollout {
+  const rmpb_grid* g;
+  const rmpb_bundle* b;
+  const rmpb_scene* scene;
+  int64_t P;
+  double params[7];
+  double max_range;
+  RolloutCfg cfg;
+  RolloutState s;
+  void* mem = nullptr;  // one allocation for all per-robot state
+  double* slots = nullptr;
+  double* accels = nullptr;
+  unsigned* h_active = nullptr;  // pinned mirror of the running count
+  cudaStream_t st = nullptr;
+};
+
+extern "C" int rmpb_rollout_create(const rmpb_grid* g, const rmpb_bundle* b, const rmpb_scene* sc,
+                                   int64_t P, const double* start, const double* goal,
+                                   const double attractor[3], const double params[7],
+                                   const double cfg[9], int64_t record_ticks,
+                                   rmpb_rollout** out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (!sc || !start || !goal || !attractor || !cfg) return fail(RMPB_ERR_INVALID, "NULL argument");
+  if (sc->device != g->device) return fail(RMPB_ERR_INVALID, "scene and grid on different devices");
+  if (P < 1 || P > (1 << 24)) return fail(RMPB_ERR_INVALID, "bad robot count");
+  const double dt = cfg[0];
+  if (!(dt > 0.0)) return fail(RMPB_ERR_INVALID, "dt must be positive");
+  if (cfg[2] < 0.0) return fail(RMPB_ERR_INVALID, "robot_radius must be >= 0");
+  if (!(attractor[0] > 0 && attractor[1] > 0 && attractor[2] > 0))
+    return fail(RMPB_ERR_INVALID, "attractor parameters must be positive");
+  DeviceGuard dg(g->device);
+  std::unique_ptr<rmpb_rollout> r(new rmpb_rollout());
+  r->g = g; r->b = b; r->scene = sc; r->P = P;
+  for (int i = 0; i < 7; ++i) r->params[i] = params[i];
+  r->max_range = cfg[7];
+  RolloutCfg& c = r->cfg;
+  c.dt = dt; c.max_time = cfg[1]; c.robot_radius = cfg[2]; c.goal_tol = cfg[3];
+  c.max_accel = cfg[4]; c.stuck_speed = cfg[6];
+  c.alpha = attractor[0]; c.beta = attractor[1]; c.c = attractor[2];
+  c.window = (int)llround(cfg[5] / dt); if (c.window < 1) c.window = 1;  // sim.py:221
+  c.max_steps = (int)llround(cfg[1] / dt);                                // sim.py:223
+  c.hold = cfg[8] != 0.0;
+  c.record = (int)(record_ticks < 0 ? 0 : record_ticks);
+  // layout of the single allocation
+  size_t off = 0;
+  auto take = [&](size_t bytes) { size_t o = off; off += (bytes + 255) / 256 * 256; return o; };
+  const size_t o_x = take(P * 3 * 8), o_v = take(P * 3 * 8), o_g = take(P * 3 * 8);
+  const size_t o_k = take(P * 4), o_a = take(P * 4), o_o = take(P * 4), o_c = take(P * 4);
+  const size_t o_sp = take((size_t)P * c.window * 8), o_sc = take(P * 4), o_sh = take(P * 4);
+  const size_t o_rec = c.record ? take((size_t)P * (c.record + 1) * 9 * 8) : 0;
+  const size_t o_slot = take(P * 13 * 8), o_acc = take(P * 3 * 8), o_na = take(16);
+  CK(cudaMalloc(&r->mem, off));
+  CK(cudaMemset(r->mem, 0, off));
+  char* m = (char*)r->mem;
+  RolloutState& s = r->s;
+  s.x = (double*)(m + o_x); s.v = (double*)(m + o_v); s.goal = (const double*)(m + o_g);
+  s.k = (int*)(m + o_k); s.active = (int*)(m + o_a); s.outcome = (int*)(m + o_o);
+  s.n_clamped = (int*)(m + o_c); s.speeds = (double*)(m + o_sp);
+  s.sp_count = (int*)(m + o_sc); s.sp_head = (int*)(m + o_sh);
+  s.rec = c.record ? (double*)(m + o_rec) : nullptr;
+  s.n_active = (unsigned*)(m + o_na);
+  r->slots = (double*)(m + o_slot);
+  r->accels = (double*)(m + o_acc);
+  CK(cudaMemcpy(s.x, start, P * 3 * 8, cudaMemcpyHostToDevice));
+  CK(cudaMemcpy((void*)s.goal, goal, P * 3 * 8, cudaMemcpyHostToDevice));
+  std::vector<int> ones((size_t)P, 1);
+  CK(cudaMemcpy(s.active, ones.data(), P * 4, cudaMemcpyHostToDevice));
+  CK(cudaHostAlloc((void**)&r->h_active, 64, cudaHostAllocDefault));
+  CK(cudaStreamCreateWithFlags(&r->st, cudaStreamNonBlocking));
+  *out = r.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_rollout_run(rmpb_rollout* r, int64_t max_ticks, int64_t* active_left,
+                                void* stream) {
+  if (!r) return fail(RMPB_ERR_INVALID, "rollout is NULL");
+  DeviceGuard dg(r->g->device);
+  cudaStream_t st = stream ? S(stream) : r->st;
+  Workspace* ws = workspace(r->g->device, stream ? stream : (void*)r->st);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  const int P = (int)r->P;
+  const int nb = (P + 127) / 128;
+  unsigned left = 1;
+  for (int64_t t = 0; t < max_ticks && left > 0; ++t) {
+    CK(cudaMemsetAsync(r->s.n_active, 0, sizeof(unsigned), st));
+    k_rollout_check<<<nb, 128, 0, st>>>(r->scene->pack, r->s, r->cfg, P);
+    CKL();
+    TRY(ray_policy_batch_impl(r->g, r->b, r->s.x, r->s.v, P, r->params, r->max_range,
+                              0.5 * r->g->geom.res, 0.9, r->slots, r->accels, nullptr, ws, st,
+                              r->s.active));
+    k_rollout_update<<<nb, 128, 0, st>>>(r->s, r->cfg, r->slots, r->accels, P);
+    CKL();
+    if ((t & 15) == 15 || t + 1 == max_ticks) {  // poll the running count now and then
+      CK(cudaMemcpyAsync(r->h_active, r->s.n_active, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      left = *r->h_active;
+    }
+  }
+  if (active_left) {
+    // exact count after the last tick: run the checks once more without side effects
+    CK(cudaStreamSynchronize(st));
+    std::vector<int> act((size_t)P);
+    CK(cudaMemcpy(act.data(), r->s.active, P * 4, cudaMemcpyDeviceToHost));
+    int64_t n = 0;
+    for (int v : act) n += v;
+    *active_left = n;
+  }
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_rollout_result(const rmpb_rollout* r, int32_t* outcome, int64_t* steps,
+                                   int64_t* n_clamped, double* x, double* v) {
+  if (!r) return fail(RMPB_ERR_INVALID, "rollout is NULL");
+  DeviceGuard dg(r->g->device);
+  CK(cudaStreamSynchronize(r->st));
+  const int64_t P = r->P;
+  std::vector<int> tmp((size_t)P);
+  if (outcome) CK(cudaMemcpy(outcome, r->s.outcome, P * 4, cudaMemcpyDeviceToHost));
+  if (steps) {
+    CK(cudaMemcpy(tmp.data(), r->s.k, P * 4, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < P; ++i) steps[i] = tmp[i];
+  }
+  if (n_clamped) {
+    CK(cudaMemcpy(tmp.data(), r->s.n_clamped, P * 4, cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < P; ++i) n_clamped[i] = tmp[i];
+  }
+  if (x) CK(cudaMemcpy(x, r->s.x, P * 24, cudaMemcpyDeviceToHost));
+  if (v) CK(cudaMemcpy(v, r->s.v, P * 24, cudaMemcpyDeviceToHost));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_rollout_trajectory(const rmpb_rollout* r, double* rec) {
+  if (!r || !rec) return fail(RMPB_ERR_INVALID, "NULL argument");
+  if (!r->s.rec) return fail(RMPB_ERR_UNSUPPORTED, "rollout was created without recording");
+  DeviceGuard dg(r->g->device);
+  CK(cudaStreamSynchronize(r->st));
+  CK(cudaMemcpy(rec, r->s.rec, (size_t)r->P * (r->cfg.record + 1) * 9 * 8, cudaMemcpyDeviceToHost));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_rollout_destroy(rmpb_rollout* r) {
+  if (!r) return RMPB_OK;
+  DeviceGuard dg(r->g->device);
+  if (r->st) cudaStreamSynchronize(r->st);
+  cudaFree(r->mem);
+  if (r->h_active) cudaFreeHost(r->h_active);
+  if (r->st) cudaStreamDestroy(r->st);
+  delete r;
   return RMPB_OK;
 }

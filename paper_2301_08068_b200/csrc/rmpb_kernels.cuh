@@ -22,6 +22,7 @@ struct PoseIO {
   unsigned* __restrict__ tickets; // [P] zero-initialised, self-resetting
   double* __restrict__ seg_out;   // [P*segs][10] raw segment partials (ray-split), or null
   double x0[3], v0[3];            // single pose by value when x / v are null
+  const int* __restrict__ active; // [P] skip poses whose flag is 0 (rollouts), or null
   __device__ __forceinline__ void pose(int p, double& a, double& b, double& c) const {
     if (x) { a = x[3 * p]; b = x[3 * p + 1]; c = x[3 * p + 2]; } else { a = x0[0]; b = x0[1]; c = x0[2]; }
   }
@@ -204,6 +205,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   const unsigned lt = (1u << lane) - 1u;
   const int unit = blockIdx.x;
   const int pose = unit / segs, seg = unit - pose * segs;
+  if (io.active && !io.active[pose]) return;  // whole CTA: finished rollout
   double sx, sy, sz;
   io.pose(pose, sx, sy, sz);
   if (lane < 9) sm.acc[warp][lane] = 0.0;

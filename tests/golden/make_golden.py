@@ -130,6 +130,20 @@ def main():
                          np.outer([1.0, 2.0, 2.0], [1.0, 2.0, 2.0]), MET[0]])
         g["pinv_in"] = mats
         g["pinv_out"] = np.array([R.core.pinv_psd(m) for m in mats])
+        # --- closed-loop rollouts (row f1): reference sim.rollout, ray planner ---
+        import rmpnav.sim as S
+        g["roll_start"], g["roll_goal"] = start, goal
+        RB = []
+        for k, (max_acc, n_rays) in enumerate(((40.0, 1024), (2.0, 512))):
+            rcfg = S.RolloutConfig(planner=S.PlannerSpec("ray", n_rays=n_rays),
+                                   params=R.preset("static_map"), dt=0.01, max_time=1.5,
+                                   max_accel=max_acc, max_range=10.0, backend=be)
+            tr = S.rollout(scene, start, goal, rcfg, grid=grid)
+            g[f"roll{k}_pos"], g[f"roll{k}_vel"], g[f"roll{k}_acc"] = tr.positions, tr.velocities, tr.accels
+            g[f"roll{k}_outcome"] = np.array(tr.outcome.value)
+            g[f"roll{k}_nclamped"] = np.array(tr.n_clamped)
+            g[f"roll{k}_dirs"] = R.sample_directions(n_rays).directions.copy()
+            g[f"roll{k}_maxacc"] = np.array(max_acc)
         out = os.path.join(HERE, "rmpnav_golden.npz")
         np.savez_compressed(out, **g)
         print(f"wrote {out} ({os.path.getsize(out)} bytes)")

@@ -427,3 +427,49 @@ def test_tsdf_bake_bricks_and_readback(be, oracle):
                                     0.5 * res, 0.9)
     slot_r = oracle.policy_slot(dirs, t_r, v, STATIC_MAP)
     check_policy(slot, acc, slot_r, oracle.accel_from_slot(slot_r))
+
+
+def _golden_scene(g):
+    import paper_2301_08068_b200 as P
+
+    prims = []
+    for k, o, c, s_, v in zip(g["scene_kinds"], g["scene_ops"], g["scene_centers"],
+                              g["scene_sizes"], g["scene_velocities"]):
+        kind = "sphere" if k == 0 else "box"
+        size = s_[0] if kind == "sphere" else s_
+        prims.append(P.Primitive(kind, c, size, "union" if o == 0 else "subtract", v))
+    lo, hi = g["scene_bounds"]
+    return P.Scene(P.Aabb(lo, hi), prims)
+
+
+def test_batched_rollout_vs_reference_golden(be, gworld, golden):
+    """Row f1: closed-loop rollouts on device reproduce the reference's
+    sim.rollout trajectories (ray planner): outcome, clamp count, every
+    (x, v, command) sample of the trajectory."""
+    import paper_2301_08068_b200 as P
+    from paper_2301_08068_b200.rollout import BatchRolloutConfig, RolloutBatch
+
+    g = golden
+    scene = _golden_scene(g)
+    pack, vals = gworld
+    grid = P.EsdfGrid(g["grid_origin"], float(g["grid_res"]), tuple(g["grid_dims"]), vals)
+    for k in (0, 1):
+        cfg = BatchRolloutConfig(params=P.preset("static_map"), dt=0.01, max_time=1.5,
+                                 max_accel=float(g[f"roll{k}_maxacc"]), max_range=10.0)
+        n_rec = g[f"roll{k}_pos"].shape[0] - 1
+        # 3 identical robots: lockstep batches must not interfere
+        starts = np.repeat(g["roll_start"][None], 3, axis=0)
+        goals = np.repeat(g["roll_goal"][None], 3, axis=0)
+        rb = RolloutBatch(scene, grid, P.RayBundle(g[f"roll{k}_dirs"]), starts, goals, cfg,
+                          record_ticks=n_rec)
+        rb.run()
+        res = rb.result()
+        for r in range(3):
+            assert res.outcome[r] == str(g[f"roll{k}_outcome"])
+            assert res.n_clamped[r] == int(g[f"roll{k}_nclamped"])
+            assert res.steps[r] == n_rec
+            tr = res.trajectory[r]
+            assert np.abs(tr[:, 0:3] - g[f"roll{k}_pos"]).max() < 1e-9
+            assert np.abs(tr[:, 3:6] - g[f"roll{k}_vel"]).max() < 1e-8
+            assert np.abs(tr[:, 6:9] - g[f"roll{k}_acc"]).max() < 1e-6 * max(
+                1.0, np.abs(g[f"roll{k}_acc"]).max())
