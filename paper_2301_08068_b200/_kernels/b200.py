@@ -250,14 +250,14 @@ _probe_idx: dict[int, np.ndarray] = {}
 
 
 def _fingerprint(a: np.ndarray) -> int:
-    """Cheap content check for cache hits: crc32 of 512 fixed pseudo-random
+    """Cheap content check for cache hits: crc32 of 256 fixed pseudo-random
     elements plus both ends.  An in-place edit that touches none of them is
     not seen -- call invalidate_caches() after mutating a cached array."""
     flat = a.reshape(-1)
     n = flat.shape[0]
     idx = _probe_idx.get(n)
     if idx is None:
-        idx = np.unique(np.random.default_rng(n).integers(0, n, size=512)) if n > 4096 \
+        idx = np.unique(np.random.default_rng(n).integers(0, n, size=256)) if n > 4096 \
             else np.arange(n)
         _probe_idx[n] = idx
     h = zlib.crc32(np.take(flat, idx).view(np.uint8))

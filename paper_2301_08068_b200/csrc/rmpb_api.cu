@@ -998,6 +998,8 @@ static int lidar_host(const double* d_dirs_or_null, const double* dirs, const do
   size_t total = off_v + (valid ? (size_t)n : 0);
   TRY(ws->in.ensure(total));
   char* d = (char*)ws->in.p;
+  // pageable host arrays go straight to the DMA engine: for MB-sized scans
+  // the driver's pipelined staging beats a host memcpy into pinned memory.
   if (!d_dirs_or_null) {
     if (!dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
     CK(cudaMemcpyAsync(d, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));

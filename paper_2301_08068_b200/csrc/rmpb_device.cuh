@@ -449,8 +449,38 @@ __device__ inline void jacobi3(double a[3][3], double V[3][3]) {
   }
 }
 
+// Fast path: when every Cholesky pivot of the (PSD) metric is >= 0.1 x its
+// trace, lambda_min >= 1e-3 lambda_max (the pivots bound det from below), so
+// pinv_psd's 1e-8 cutoff drops nothing and pinv(M) f = M^-1 f: a Cholesky
+// solve (~30 dependent fp64 ops instead of Jacobi sweeps).  Returns false when
+// the metric is not that well conditioned (rank-deficient ones included).
+__device__ inline bool chol_solve3(const double m[9], const double f[3], double out[3]) {
+  const double tr = m[0] + m[4] + m[8];
+  if (!(tr > 0.0)) return false;
+  const double tau = 0.1 * tr;
+  const double d0 = m[0];
+  if (!(d0 >= tau)) return false;
+  const double l00 = sqrt(d0);
+  const double l10 = m[3] / l00, l20 = m[6] / l00;
+  const double d1 = m[4] - l10 * l10;
+  if (!(d1 >= tau)) return false;
+  const double l11 = sqrt(d1);
+  const double l21 = (m[7] - l20 * l10) / l11;
+  const double d2 = m[8] - l20 * l20 - l21 * l21;
+  if (!(d2 >= tau)) return false;
+  const double l22 = sqrt(d2);
+  const double y0 = f[0] / l00;
+  const double y1 = (f[1] - l10 * y0) / l11;
+  const double y2 = (f[2] - l20 * y0 - l21 * y1) / l22;
+  out[2] = y2 / l22;
+  out[1] = (y1 - l21 * out[2]) / l11;
+  out[0] = (y0 - l10 * out[1] - l20 * out[2]) / l00;
+  return true;
+}
+
 // m: symmetric metric (row-major 9), f: weighted sum (3) -> accel (3).
 __device__ inline void pinv_apply(const double m[9], const double f[3], double out[3]) {
+  if (chol_solve3(m, f, out)) return;
   double a[3][3], V[3][3];
   for (int i = 0; i < 3; ++i)
     for (int j = 0; j < 3; ++j) a[i][j] = 0.5 * (m[3 * i + j] + m[3 * j + i]);

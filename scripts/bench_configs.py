@@ -271,16 +271,54 @@ def c5(args, out):
     out.append(rec)
 
 
+def c4loop(args, out):
+    """Row f1: closed-loop ticks for a batch of robots on the C1 map (every
+    tick = checks + fused 65536-ray policy + combine + clamp + Euler, on
+    device, no host round trip)."""
+    import torch
+
+    import paper_2301_08068_b200 as P
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200.rollout import BatchRolloutConfig, RolloutBatch
+
+    scene = synth.c1_scene()
+    grid = synth.c1_grid(scene)
+    dist = synth.host_box_distance(scene)
+    n_rob = 1024 if args.quick else 4096
+    starts = synth.states_arrays(synth.bench_states(scene, n_rob, seed=123, distance=dist))[0]
+    goals = synth.states_arrays(synth.bench_states(scene, n_rob, seed=321, distance=dist))[0]
+    bundle = P.sample_directions(65536)
+    cfg = BatchRolloutConfig(params=P.preset("static_map"), dt=0.01, max_time=60.0,
+                             max_range=10.0)
+    rb = RolloutBatch(scene, grid, bundle, starts, goals, cfg)
+    rb.run(2)
+    torch.cuda.synchronize()
+    ticks = 10 if args.quick else 30
+    t0 = time.perf_counter()
+    left = rb.run(ticks)
+    torch.cuda.synchronize()
+    el = time.perf_counter() - t0
+    res = rb.result()
+    rec = {"config": "C4-closed-loop", "robots": n_rob, "rays_per_robot": 65536,
+           "ticks": ticks, "s_per_tick": round(el / ticks, 5),
+           "robot_steps_per_s": round(n_rob * ticks / el, 1),
+           "still_running": left,
+           "outcomes": {k: res.outcome.count(k) for k in set(res.outcome)},
+           "note": "wall clock around rmpb_rollout_run (3 launches per tick, polled every 16)"}
+    print(json.dumps(rec), flush=True)
+    out.append(rec)
+
+
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--only", default="c2,c3,c5")
+    ap.add_argument("--only", default="c2,c3,c5,c4loop")
     ap.add_argument("--quick", action="store_true")
     ap.add_argument("--oracle-c5", action="store_true",
                     help="also check C5 against the dense CPU oracle (needs ~1 GB host RAM)")
     args = ap.parse_args()
     out = []
     for name in args.only.split(","):
-        {"c2": c2, "c3": c3, "c5": c5}[name.strip()](args, out)
+        {"c2": c2, "c3": c3, "c5": c5, "c4loop": c4loop}[name.strip()](args, out)
 
 
 if __name__ == "__main__":
