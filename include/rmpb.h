@@ -70,7 +70,7 @@ enum {
 enum { RMPB_F32 = 0, RMPB_F64 = 1 };                              /* value dtypes */
 enum { RMPB_STORE_AUTO = 0, RMPB_STORE_F32 = 1, RMPB_STORE_F64 = 2 }; /* grid storage */
 enum { RMPB_LAYOUT_LINEAR = 0, RMPB_LAYOUT_QUAD = 1, RMPB_LAYOUT_BRICK = 2,
-       RMPB_LAYOUT_AUTO = -1 };
+       RMPB_LAYOUT_QUADB = 3, RMPB_LAYOUT_AUTO = -1 };
 enum { RMPB_ORDER_IDENTITY = 0, RMPB_ORDER_MORTON = 1 };          /* bundle evaluation order */
 
 typedef struct rmpb_grid rmpb_grid;
@@ -238,6 +238,27 @@ RMPB_EXPORT int rmpb_rollout_result(const rmpb_rollout* r, int32_t* outcome, int
 /* rec: P x (record_ticks + 1) x 9 doubles (x, v, accel per tick). */
 RMPB_EXPORT int rmpb_rollout_trajectory(const rmpb_rollout* r, double* rec);
 RMPB_EXPORT int rmpb_rollout_destroy(rmpb_rollout* r);
+
+/* ---- K5: Amanatides-Woo DDA over bit-packed occupancy ------------------
+ * The traversal north_star names; NOT the reference's (sphere tracing,
+ * SPEC.md:228), so it is opt-in and reported separately.  Occupied = node
+ * value <= 0 (geometry.py:312-315), voxel of node (i,j,k) = res-cube centred
+ * on it.  float32 march, bit-exact against oracle/rmp_oracle.c
+ * orc_dda_trace: entry distance of the first occupied voxel (+inf = miss)
+ * and its index (-1 = miss). */
+typedef struct rmpb_occupancy rmpb_occupancy;
+RMPB_EXPORT int rmpb_occupancy_create(const rmpb_grid* g, rmpb_occupancy** out);
+RMPB_EXPORT int rmpb_occupancy_destroy(rmpb_occupancy* o);
+/* nx*ny*ceil(nz/32) words, bit k%32 of word (i*ny + j)*nzw + k/32. */
+RMPB_EXPORT int rmpb_occupancy_bits(const rmpb_occupancy* o, uint32_t* out);
+RMPB_EXPORT int rmpb_dda_trace(const rmpb_occupancy* o, const double* dirs, int64_t n, const double start[3],
+                   double max_range, float* out_t, int32_t* out_voxel, int32_t* out_steps,
+                   void* stream);
+/* Fused DDA + per-ray policy + reduction + pinv for P poses (device ptrs). */
+RMPB_EXPORT int rmpb_ray_policy_dda_batch_device(const rmpb_occupancy* o, const rmpb_bundle* b,
+                                     const double* d_x, const double* d_v, int64_t P,
+                                     const double params[7], double max_range, double* d_slot,
+                                     double* d_accel, void* stream);
 
 #ifdef __cplusplus
 }

@@ -310,3 +310,111 @@ void orc_esdf_sample(const double *values, int64_t nx, int64_t ny, int64_t nz,
         }
     }
 }
+
+/* ------------------------------------------------------------------------
+ * K5 (north_star "per-ray 3D DDA (Amanatides-Woo) through the occupancy
+ * grid"): NOT a reference function -- the reference sphere-traces
+ * (SPEC.md:228).  This is the CPU definition the CUDA DDA is checked
+ * against bit-for-bit; see DESIGN.md §K5.  Occupancy = node value <= 0
+ * (rmpnav/geometry.py:312-315); the voxel of node (i,j,k) is the res-cube
+ * centred on it.  All arithmetic is float32, no contraction, IEEE division,
+ * so CPU and GPU agree bitwise.  Outputs: entry distance t of the first
+ * occupied voxel (+inf = miss), its index, and the voxels visited.
+ */
+static int orc_occ(const uint32_t *bits, int64_t ny, int64_t nzw, int64_t i, int64_t j, int64_t k)
+{
+    return (bits[(i * ny + j) * nzw + (k >> 5)] >> (k & 31)) & 1u;
+}
+
+void orc_occupancy_bits(const double *values, int64_t nx, int64_t ny, int64_t nz, uint32_t *bits)
+{
+    int64_t nzw = (nz + 31) / 32;
+    memset(bits, 0, (size_t)(nx * ny * nzw) * sizeof(uint32_t));
+    for (int64_t i = 0; i < nx; ++i)
+        for (int64_t j = 0; j < ny; ++j)
+            for (int64_t k = 0; k < nz; ++k)
+                if (values[(i * ny + j) * nz + k] <= 0.0)
+                    bits[(i * ny + j) * nzw + (k >> 5)] |= 1u << (k & 31);
+}
+
+void orc_dda_trace(const uint32_t *bits, int64_t nx, int64_t ny, int64_t nz,
+                   double ox, double oy, double oz, double res,
+                   double sx, double sy, double sz, const double *dirs, int64_t s, int64_t e,
+                   double max_range, float *out_t, int32_t *out_vox, int32_t *out_steps)
+{
+    const int64_t nzw = (nz + 31) / 32;
+    const int n[3] = {(int)nx, (int)ny, (int)nz};
+    const float inv = 1.0f / (float)res;
+    const float o[3] = {(float)ox, (float)oy, (float)oz};
+    const float st[3] = {(float)sx, (float)sy, (float)sz};
+    const float tr = (float)max_range;
+    for (int64_t r = s; r < e; ++r) {
+        float u[3], dv[3];
+        for (int a = 0; a < 3; ++a) {
+            float p = st[a] - o[a];
+            p = p * inv;
+            u[a] = p + 0.5f;
+            float d = (float)dirs[3 * r + a];
+            dv[a] = d * inv;
+        }
+        float t0 = 0.0f, t1 = tr;
+        int ok = 1;
+        for (int a = 0; a < 3 && ok; ++a) {
+            if (dv[a] != 0.0f) {
+                float ta = (0.0f - u[a]) / dv[a];
+                float tb = ((float)n[a] - u[a]) / dv[a];
+                if (tb < ta) { float tmp = ta; ta = tb; tb = tmp; }
+                if (ta > t0) t0 = ta;
+                if (tb < t1) t1 = tb;
+            } else if (u[a] < 0.0f || u[a] >= (float)n[a]) {
+                ok = 0;
+            }
+        }
+        out_t[r] = INFINITY;
+        out_vox[3 * r] = out_vox[3 * r + 1] = out_vox[3 * r + 2] = -1;
+        int steps = 0;
+        if (ok && !(t0 > t1)) {
+            int vox[3], stp[3];
+            float tmax[3], tdel[3];
+            for (int a = 0; a < 3; ++a) {
+                float pa = dv[a] * t0;
+                pa = u[a] + pa;
+                int ia = (int)floorf(pa);
+                if (ia < 0) ia = 0;
+                if (ia > n[a] - 1) ia = n[a] - 1;
+                vox[a] = ia;
+                if (dv[a] > 0.0f) {
+                    stp[a] = 1;
+                    tmax[a] = ((float)(ia + 1) - u[a]) / dv[a];
+                    tdel[a] = 1.0f / dv[a];
+                } else if (dv[a] < 0.0f) {
+                    stp[a] = -1;
+                    tmax[a] = ((float)ia - u[a]) / dv[a];
+                    tdel[a] = -1.0f / dv[a];
+                } else {
+                    stp[a] = 0;
+                    tmax[a] = INFINITY;
+                    tdel[a] = INFINITY;
+                }
+            }
+            float t = t0;
+            for (;;) {
+                ++steps;
+                if (orc_occ(bits, ny, nzw, vox[0], vox[1], vox[2])) {
+                    out_t[r] = t;
+                    out_vox[3 * r] = vox[0]; out_vox[3 * r + 1] = vox[1]; out_vox[3 * r + 2] = vox[2];
+                    break;
+                }
+                int a = 0;
+                if (tmax[1] < tmax[a]) a = 1;
+                if (tmax[2] < tmax[a]) a = 2;
+                t = tmax[a];
+                if (!(t <= t1)) break;
+                vox[a] += stp[a];
+                if (vox[a] < 0 || vox[a] >= n[a]) break;
+                tmax[a] = tmax[a] + tdel[a];
+            }
+        }
+        if (out_steps) out_steps[r] = steps;
+    }
+}

@@ -123,7 +123,7 @@ class DeviceGrid:
                ctypes.byref(nb), ctypes.byref(nbr))
         self.storage = {L.STORE_F32: "f32", L.STORE_F64: "f64"}[st.value]
         self.layout = {L.LAYOUT_LINEAR: "linear", L.LAYOUT_QUAD: "quad",
-                       L.LAYOUT_BRICK: "brick"}[lay.value]
+                       L.LAYOUT_BRICK: "brick", L.LAYOUT_QUADB: "quadb"}[lay.value]
         self.device_bytes = int(nb.value)
         self.bricks = int(nbr.value)
 
@@ -203,6 +203,45 @@ class DeviceBundle:
         if h is not None and h.value:
             try:
                 L.load().rmpb_bundle_destroy(h)
+            except Exception:
+                pass
+            self.handle = None
+
+
+class DeviceOccupancy:
+    """K5: bit-packed occupancy (node value <= 0) of a device grid, for the
+    Amanatides-Woo DDA traversal (not the reference's sphere trace)."""
+
+    def __init__(self, grid: "DeviceGrid"):
+        self.grid = grid
+        self.device = grid.device
+        self.dims = grid.dims
+        h = ctypes.c_void_p()
+        L.call("rmpb_occupancy_create", grid.handle, ctypes.byref(h))
+        self.handle = h
+
+    def bits(self) -> np.ndarray:
+        nx, ny, nz = self.dims
+        out = np.empty(nx * ny * ((nz + 31) // 32), dtype=np.uint32)
+        L.call("rmpb_occupancy_bits", self.handle, out.ctypes.data)
+        return out
+
+    def trace(self, start, dirs, max_range):
+        """(t float32 (+inf = miss), voxel (N,3) int32 (-1 = miss), visited)."""
+        d = _f64(dirs, (-1, 3))
+        n = d.shape[0]
+        t = np.empty(n, np.float32)
+        vox = np.empty((n, 3), np.int32)
+        steps = np.empty(n, np.int32)
+        L.call("rmpb_dda_trace", self.handle, d.ctypes.data, n, _vec3(start).ctypes.data,
+               float(max_range), t.ctypes.data, vox.ctypes.data, steps.ctypes.data, None)
+        return t, vox, steps
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            try:
+                L.load().rmpb_occupancy_destroy(h)
             except Exception:
                 pass
             self.handle = None

@@ -29,7 +29,7 @@ RMPB_ERR_UNSUPPORTED = -4
 
 RMPB_F32, RMPB_F64 = 0, 1
 STORE_AUTO, STORE_F32, STORE_F64 = 0, 1, 2
-LAYOUT_LINEAR, LAYOUT_QUAD, LAYOUT_BRICK, LAYOUT_AUTO = 0, 1, 2, -1
+LAYOUT_LINEAR, LAYOUT_QUAD, LAYOUT_BRICK, LAYOUT_QUADB, LAYOUT_AUTO = 0, 1, 2, 3, -1
 ORDER_IDENTITY, ORDER_MORTON = 0, 1
 
 _vp = ctypes.c_void_p
@@ -85,6 +85,11 @@ _SIGS = {
     "rmpb_rollout_result": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),
     "rmpb_rollout_trajectory": (_i, [_vp, _vp]),
     "rmpb_rollout_destroy": (_i, [_vp]),
+    "rmpb_occupancy_create": (_i, [_vp, _vp]),
+    "rmpb_occupancy_destroy": (_i, [_vp]),
+    "rmpb_occupancy_bits": (_i, [_vp, _vp]),
+    "rmpb_dda_trace": (_i, [_vp, _vp, _i64, _vp, _d, _vp, _vp, _vp, _vp]),
+    "rmpb_ray_policy_dda_batch_device": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _d, _vp, _vp, _vp]),
 }
 
 EXPORTED = tuple(_SIGS)

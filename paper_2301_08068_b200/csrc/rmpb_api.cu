@@ -22,6 +22,7 @@
 #include "rmpb_aux.cuh"
 #include "rmpb_kernels.cuh"
 #include "rmpb_rollout.cuh"
+#include "rmpb_dda.cuh"
 
 using namespace rmpb;
 
@@ -198,6 +199,10 @@ static int with_grid(const rmpb_grid* g, F&& f) {
     LinearGrid<double> a{(const double*)g->d_values, G.nz, G.ny * G.nz};
     return f(a);
   }
+  if (g->layout == LAYOUT_QUADB) {
+    QuadGridF32B a{(const float4*)g->d_values, (G.ny - 1 + 1) / 2, (G.nz - 1 + 1) / 2};
+    return f(a);
+  }
   if (g->layout == LAYOUT_QUAD) {
     if (g->storage == RMPB_STORE_F32) {
       QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1)};
@@ -346,6 +351,23 @@ static int grid_build(rmpb_grid* g, const void* d_src, int dtype, int storage, i
     cudaFree(lin);
     g->d_values = q;
     g->bytes = nq * 4 * esz;
+  } else if (layout == LAYOUT_QUADB) {
+    if (store != RMPB_STORE_F32) {
+      cudaFree(lin);
+      return fail(RMPB_ERR_UNSUPPORTED, "QUADB layout needs f32-exact values");
+    }
+    const long long bnx = (g->nx + 1) / 2, bny = (g->ny - 1 + 1) / 2, bnz = (g->nz - 1 + 1) / 2;
+    const long long nq = bnx * bny * bnz * 8;
+    void* q = nullptr;
+    CK(cudaMalloc(&q, nq * 16));
+    CK(cudaMemsetAsync(q, 0, nq * 16, st));
+    k_build_quadb<<<grid_blocks(g->nx * (g->ny - 1) * (g->nz - 1)), 256, 0, st>>>(
+        (int)g->nx, (int)g->ny, (int)g->nz, (int)bny, (int)bnz, (const float*)lin, (float4*)q);
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    cudaFree(lin);
+    g->d_values = q;
+    g->bytes = nq * 16;
   } else {
     return fail(RMPB_ERR_INVALID, "unknown layout %d", layout);
   }
@@ -438,7 +460,7 @@ static int grid_new(const void* values, bool on_device, int dtype, int64_t nx, i
   if (dtype != RMPB_F32 && dtype != RMPB_F64) return fail(RMPB_ERR_INVALID, "bad dtype %d", dtype);
   TRY(grid_check_dims(nx, ny, nz, res));
   if (layout == RMPB_LAYOUT_AUTO) layout = LAYOUT_QUAD;
-  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD)
+  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD && layout != LAYOUT_QUADB)
     return fail(RMPB_ERR_INVALID, "layout %d not valid here (use rmpb_grid_create_brick)", layout);
   DeviceGuard dg(device);
   if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
@@ -1554,5 +1576,109 @@ extern "C" int rmpb_rollout_destroy(rmpb_rollout* r) {
   if (r->h_active) cudaFreeHost(r->h_active);
   if (r->st) cudaStreamDestroy(r->st);
   delete r;
+  return RMPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// K5: DDA over bit-packed occupancy (not reference parity; see rmpb_dda.cuh)
+
+struct rmpb_occupancy {
+  int device;
+  Occupancy o;
+  uint32_t* bits = nullptr;
+  int64_t bytes = 0;
+};
+
+extern "C" int rmpb_occupancy_create(const rmpb_grid* g, rmpb_occupancy** out) {
+  if (!g || !out) return fail(RMPB_ERR_INVALID, "NULL grid / out");
+  *out = nullptr;
+  DeviceGuard dg(g->device);
+  std::unique_ptr<rmpb_occupancy> oc(new rmpb_occupancy());
+  oc->device = g->device;
+  const int nx = (int)g->nx, ny = (int)g->ny, nz = (int)g->nz, nzw = (nz + 31) / 32;
+  const long long words = (long long)nx * ny * nzw;
+  CK(cudaMalloc((void**)&oc->bits, words * 4));
+  oc->bytes = words * 4;
+  TRY(with_grid(g, [&](auto acc) -> int {
+    k_occ_build<<<grid_blocks(words), 256>>>(acc, nx, ny, nz, nzw, oc->bits);
+    CKL();
+    return RMPB_OK;
+  }));
+  CK(cudaDeviceSynchronize());
+  Occupancy& o = oc->o;
+  o.bits = oc->bits; o.nx = nx; o.ny = ny; o.nz = nz; o.nzw = nzw;
+  o.ox = (float)g->geom.ox; o.oy = (float)g->geom.oy; o.oz = (float)g->geom.oz;
+  o.inv = 1.0f / (float)g->geom.res;
+  *out = oc.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_occupancy_destroy(rmpb_occupancy* oc) {
+  if (!oc) return RMPB_OK;
+  DeviceGuard dg(oc->device);
+  cudaFree(oc->bits);
+  delete oc;
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_occupancy_bits(const rmpb_occupancy* oc, uint32_t* out) {
+  if (!oc || !out) return fail(RMPB_ERR_INVALID, "NULL argument");
+  DeviceGuard dg(oc->device);
+  CK(cudaMemcpy(out, oc->bits, oc->bytes, cudaMemcpyDeviceToHost));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_dda_trace(const rmpb_occupancy* oc, const double* dirs, int64_t n,
+                              const double start[3], double max_range, float* out_t,
+                              int32_t* out_voxel, int32_t* out_steps, void* stream) {
+  if (!oc || !start || !out_t || !out_voxel) return fail(RMPB_ERR_INVALID, "NULL argument");
+  if (n < 0 || n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "bad ray count");
+  if (n == 0) return RMPB_OK;
+  if (!dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
+  DeviceGuard dg(oc->device);
+  Workspace* ws = workspace(oc->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  TRY(ws->in.ensure(n * 3 * sizeof(double)));
+  TRY(ws->out.ensure(n * sizeof(float)));
+  TRY(ws->out2.ensure(n * 3 * sizeof(int32_t)));
+  TRY(ws->out3.ensure(n * sizeof(int32_t)));
+  CK(cudaMemcpyAsync(ws->in.p, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+  k_dda_trace<<<(unsigned)((n + kBlock - 1) / kBlock), kBlock, 0, st>>>(
+      oc->o, (const double*)ws->in.p, (int)n, (float)start[0], (float)start[1], (float)start[2],
+      (float)max_range, (float*)ws->out.p, (int*)ws->out2.p, out_steps ? (int*)ws->out3.p : nullptr);
+  CKL();
+  CK(cudaMemcpyAsync(out_t, ws->out.p, n * sizeof(float), cudaMemcpyDeviceToHost, st));
+  CK(cudaMemcpyAsync(out_voxel, ws->out2.p, n * 3 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  if (out_steps)
+    CK(cudaMemcpyAsync(out_steps, ws->out3.p, n * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_ray_policy_dda_batch_device(const rmpb_occupancy* oc, const rmpb_bundle* b,
+                                                const double* d_x, const double* d_v, int64_t P,
+                                                const double params[7], double max_range,
+                                                double* d_slot, double* d_accel, void* stream) {
+  if (!oc || !b || !d_x || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL argument");
+  TRY(check_params(params));
+  if (P < 1) return fail(RMPB_ERR_INVALID, "P must be >= 1");
+  if (oc->device != b->device) return fail(RMPB_ERR_INVALID, "occupancy / bundle devices differ");
+  DeviceGuard dg(oc->device);
+  Workspace* ws = workspace(oc->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  int segs, seg_rays;
+  choose_segments(P, b->n, &segs, &seg_rays);
+  if (segs > 1) {
+    TRY(ws->partials.ensure((size_t)P * segs * kAcc * sizeof(double)));
+    TRY(ws->ensure_tickets((size_t)P));
+  }
+  PoseIO io{};
+  io.x = d_x; io.v = d_v; io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  k_ray_policy_dda<<<(unsigned)(P * segs), kBlock, 0, S(stream)>>>(
+      oc->o, bundle_view(b), io, make_params(params, 0.0), (float)max_range, segs, seg_rays);
+  CKL();
   return RMPB_OK;
 }

@@ -132,6 +132,25 @@ __global__ void k_build_quad(int nx, int ny, int nz, const T* __restrict__ v, Q*
   }
 }
 
+// QUADB builder: the QUAD record of cell (i,j,k) (i < nx, j < ny-1, k < nz-1)
+// at its 2x2x2-blocked index; padding records stay zero (never read).
+__global__ void k_build_quadb(int nx, int ny, int nz, int bny, int bnz, const float* __restrict__ v,
+                              float4* __restrict__ q) {
+  long long n = (long long)nx * (ny - 1) * (nz - 1);
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; t < n; t += stride) {
+    int k = (int)(t % (nz - 1));
+    long long r = t / (nz - 1);
+    int j = (int)(r % (ny - 1));
+    int i = (int)(r / (ny - 1));
+    const float* b = v + ((long long)i * ny + j) * nz + k;
+    unsigned idx = ((((unsigned)(i >> 1) * bny + (unsigned)(j >> 1)) * bnz + (unsigned)(k >> 1)) << 3) |
+                   ((i & 1) << 2) | ((j & 1) << 1) | (k & 1);
+    q[idx] = make_float4(b[0], b[1], b[nz], b[nz + 1]);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Analytic scene (geometry.py:177-197 pack; _ckern.pyx:21-56 distance).
 struct ScenePack {

@@ -1,0 +1,167 @@
+// rmpb_dda.cuh -- K5: per-ray 3D DDA (Amanatides-Woo) over a bit-packed
+// occupancy grid, the traversal north_star names.  NOT the reference's
+// algorithm (the reference sphere-traces the ESDF): it is a
+// separate, opt-in traversal, checked bit-for-bit against its own CPU
+// definition (oracle/rmp_oracle.c orc_dda_trace) and never mixed with the
+// reference-parity claims.
+//
+// Occupancy = node value <= 0 (rmpnav/geometry.py:312-315); the voxel of
+// node (i,j,k) is the res-cube centred on it.  One bit per voxel, 32 voxels
+// of a z-column per word: the C1 map is 500 KB -- L1/L2 resident.  The march
+// is float32 with no contraction and IEEE division (this file is compiled
+// with -fmad=false), so the CPU and GPU visit the same voxels and report the
+// same entry distance bit-for-bit.
+#pragma once
+#include "rmpb_kernels.cuh"
+
+namespace rmpb {
+
+struct Occupancy {
+  const uint32_t* __restrict__ bits;
+  int nx, ny, nz, nzw;   // nzw = ceil(nz / 32)
+  float ox, oy, oz, inv; // origin (f32) and 1/res (f32)
+  __device__ __forceinline__ bool occ(int i, int j, int k) const {
+    return (__ldg(bits + ((unsigned)(i * ny + j) * nzw + (k >> 5))) >> (k & 31)) & 1u;
+  }
+};
+
+// Node values -> occupancy bits, one 32-voxel word per thread.
+template <class G>
+__global__ void k_occ_build(G grid, int nx, int ny, int nz, int nzw, uint32_t* __restrict__ bits) {
+  long long n = (long long)nx * ny * nzw;
+  long long w = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; w < n; w += stride) {
+    const int kw = (int)(w % nzw);
+    const long long r = w / nzw;
+    const int j = (int)(r % ny), i = (int)(r / ny);
+    uint32_t word = 0;
+    for (int b = 0; b < 32; ++b) {
+      const int k = kw * 32 + b;
+      if (k >= nz) break;
+      const int ci = min(i, nx - 2), cj = min(j, ny - 2), ck = min(k, nz - 2);
+      Corners c = grid.load(ci, cj, ck);
+      const int a = i - ci, bb = j - cj, d = k - ck;
+      const double v = a ? (bb ? (d ? c.v111 : c.v110) : (d ? c.v101 : c.v100))
+                         : (bb ? (d ? c.v011 : c.v010) : (d ? c.v001 : c.v000));
+      if (v <= 0.0) word |= 1u << b;
+    }
+    bits[w] = word;
+  }
+}
+
+struct DdaResult {
+  float t;          // entry distance of the first occupied voxel, +inf on miss
+  int vx, vy, vz;   // its index (-1 on miss)
+  int steps;        // voxels visited
+};
+
+__device__ __forceinline__ DdaResult dda_ray(const Occupancy& o, float sx, float sy, float sz,
+                                             float dx, float dy, float dz, float max_range) {
+  DdaResult res;
+  res.t = CUDART_INF_F; res.vx = res.vy = res.vz = -1; res.steps = 0;
+  const int n[3] = {o.nx, o.ny, o.nz};
+  float u[3], dv[3];
+  {
+    const float st[3] = {sx, sy, sz}, org[3] = {o.ox, o.oy, o.oz}, d[3] = {dx, dy, dz};
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+      float p = st[a] - org[a];
+      p = p * o.inv;
+      u[a] = p + 0.5f;
+      dv[a] = d[a] * o.inv;
+    }
+  }
+  float t0 = 0.0f, t1 = max_range;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    if (dv[a] != 0.0f) {
+      float ta = (0.0f - u[a]) / dv[a];
+      float tb = ((float)n[a] - u[a]) / dv[a];
+      if (tb < ta) { float tmp = ta; ta = tb; tb = tmp; }
+      if (ta > t0) t0 = ta;
+      if (tb < t1) t1 = tb;
+    } else if (u[a] < 0.0f || u[a] >= (float)n[a]) {
+      return res;
+    }
+  }
+  if (t0 > t1) return res;
+  int vox[3], stp[3];
+  float tmax[3], tdel[3];
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    float pa = dv[a] * t0;
+    pa = u[a] + pa;
+    int ia = (int)floorf(pa);
+    ia = ia < 0 ? 0 : (ia > n[a] - 1 ? n[a] - 1 : ia);
+    vox[a] = ia;
+    if (dv[a] > 0.0f) {
+      stp[a] = 1;
+      tmax[a] = ((float)(ia + 1) - u[a]) / dv[a];
+      tdel[a] = 1.0f / dv[a];
+    } else if (dv[a] < 0.0f) {
+      stp[a] = -1;
+      tmax[a] = ((float)ia - u[a]) / dv[a];
+      tdel[a] = -1.0f / dv[a];
+    } else {
+      stp[a] = 0;
+      tmax[a] = CUDART_INF_F;
+      tdel[a] = CUDART_INF_F;
+    }
+  }
+  float t = t0;
+  while (true) {
+    ++res.steps;
+    if (o.occ(vox[0], vox[1], vox[2])) {
+      res.t = t; res.vx = vox[0]; res.vy = vox[1]; res.vz = vox[2];
+      break;
+    }
+    int a = 0;
+    if (tmax[1] < tmax[a]) a = 1;
+    if (tmax[2] < tmax[a]) a = 2;
+    t = tmax[a];
+    if (!(t <= t1)) break;
+    vox[a] += stp[a];
+    if (vox[a] < 0 || vox[a] >= n[a]) break;
+    tmax[a] = tmax[a] + tdel[a];
+  }
+  return res;
+}
+
+__global__ void __launch_bounds__(kBlock)
+k_dda_trace(Occupancy o, const double* __restrict__ dirs, int n, float sx, float sy, float sz,
+            float max_range, float* __restrict__ out_t, int* __restrict__ out_vox,
+            int* __restrict__ out_steps) {
+  const int i = blockIdx.x * kBlock + threadIdx.x;
+  if (i >= n) return;
+  DdaResult r = dda_ray(o, sx, sy, sz, (float)dirs[3 * i], (float)dirs[3 * i + 1],
+                        (float)dirs[3 * i + 2], max_range);
+  out_t[i] = r.t;
+  out_vox[3 * i] = r.vx; out_vox[3 * i + 1] = r.vy; out_vox[3 * i + 2] = r.vz;
+  if (out_steps) out_steps[i] = r.steps;
+}
+
+// Fused DDA + per-ray policy (distance = voxel entry distance) + reduction,
+// same unit / fold structure as the sphere-trace kernels.
+__global__ void __launch_bounds__(kBlock)
+k_ray_policy_dda(Occupancy o, Bundle b, PoseIO io, PolicyParams p, float max_range, int segs,
+                 int seg_rays) {
+  const int unit = blockIdx.x;
+  const int pose = unit / segs, seg = unit - pose * segs;
+  double sx, sy, sz, vx, vy, vz;
+  io.pose(pose, sx, sy, sz);
+  io.vel(pose, vx, vy, vz);
+  Acc acc;
+  acc.zero();
+  const int begin = seg * seg_rays;
+  const int end = min(begin + seg_rays, b.n);
+  for (int i = begin + threadIdx.x; i < end; i += kBlock) {
+    const double dx = b.dx[i], dy = b.dy[i], dz = b.dz[i];
+    DdaResult r = dda_ray(o, (float)sx, (float)sy, (float)sz, (float)dx, (float)dy, (float)dz,
+                          max_range);
+    policy_accumulate(acc, dx, dy, dz, (double)r.t, vx, vy, vz, p);
+  }
+  finish_unit(acc, io, pose, seg, segs);
+}
+
+}  // namespace rmpb

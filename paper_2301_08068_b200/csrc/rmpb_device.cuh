@@ -33,7 +33,10 @@ constexpr int kAcc = 10;          // a00 a01 a02 a11 a12 a22 b0 b1 b2 cnt
 //           unallocated bricks read as `fill`).
 // Values are copied verbatim (f32 storage only when every value is exactly
 // representable in f32), so all layouts interpolate bit-identically.
-enum Layout : int { LAYOUT_LINEAR = 0, LAYOUT_QUAD = 1, LAYOUT_BRICK = 2 };
+//   QUADB : QUAD records stored in 2x2x2 blocks of cells (128 B = one L1 line
+//           per block), so the two x-planes of a step and the next steps'
+//           cells share lines far more often than in the z-fastest order.
+enum Layout : int { LAYOUT_LINEAR = 0, LAYOUT_QUAD = 1, LAYOUT_BRICK = 2, LAYOUT_QUADB = 3 };
 
 struct GridGeom {
   int nx, ny, nz;
@@ -106,6 +109,24 @@ struct QuadGridF32 {
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
     const float4* b = q + (unsigned)(ix * qx + iy * qy + iz);
     float4 a = __ldg(b), c = __ldg(b + (unsigned)qx);
+    Corners k;
+    k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
+    k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;
+    return k;
+  }
+};
+
+struct QuadGridF32B {
+  const float4* __restrict__ q;
+  int bny, bnz;  // 2-cell blocks along y and z of the cell grid
+  __device__ __forceinline__ unsigned idx(int i, int j, int k) const {
+    return ((((unsigned)(i >> 1) * bny + (unsigned)(j >> 1)) * bnz + (unsigned)(k >> 1)) << 3) |
+           ((i & 1) << 2) | ((j & 1) << 1) | (k & 1);
+  }
+  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    const unsigned i0 = idx(ix, iy, iz);
+    const unsigned i1 = (ix & 1) ? idx(ix + 1, iy, iz) : i0 + 4u;
+    float4 a = __ldg(q + i0), c = __ldg(q + i1);
     Corners k;
     k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
     k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;

@@ -118,6 +118,32 @@ class RayPolicyEngine:
         return out_slot, out_accel
 
 
+class DdaPolicyEngine:
+    """K5: fused Amanatides-Woo DDA over occupancy + per-ray policy +
+    reduction for P poses (device tensors).  A different traversal from the
+    reference's sphere trace: its results are not reference-parity results."""
+
+    def __init__(self, grid, bundle, params, max_range: float = 20.0, device: int | None = None):
+        base = RayPolicyEngine(grid, bundle, params, max_range, device)
+        self.grid, self.bundle, self.params = base.grid, base.bundle, base.params
+        self.max_range = float(max_range)
+        self.occ = b200.DeviceOccupancy(self.grid)
+
+    def evaluate(self, x, v, out_slot=None, out_accel=None, stream=None):
+        torch = _torch()
+        _check_tensor(x, (3,), "float64", "x")
+        _check_tensor(v, (3,), "float64", "v")
+        P = x.shape[0]
+        if out_slot is None:
+            out_slot = torch.empty((P, 13), dtype=torch.float64, device=x.device)
+        if out_accel is None:
+            out_accel = torch.empty((P, 3), dtype=torch.float64, device=x.device)
+        L.call("rmpb_ray_policy_dda_batch_device", self.occ.handle, self.bundle.handle,
+               x.data_ptr(), v.data_ptr(), P, self.params.ctypes.data, self.max_range,
+               out_slot.data_ptr(), out_accel.data_ptr(), _stream_ptr(stream))
+        return out_slot, out_accel
+
+
 def lidar_policy_batch_device(dirs, R, ranges, valid, v, params, min_range=0.3, stream=None):
     """S scans sharing the lattice ``dirs`` (n x 3 f64, CUDA): R (S x 9 or
     None), ranges (S x n f64), valid (S x n uint8 / bool or None), v (S x 3).

@@ -221,6 +221,7 @@ def test_layouts_and_storage_identical(be, oracle, c1):
                               0.05, 0.9)
     variants = [dict(storage=L.STORE_F32, layout=L.LAYOUT_LINEAR),
                 dict(storage=L.STORE_F32, layout=L.LAYOUT_QUAD),
+                dict(storage=L.STORE_F32, layout=L.LAYOUT_QUADB),
                 dict(storage=L.STORE_F64, layout=L.LAYOUT_LINEAR),
                 dict(storage=L.STORE_F64, layout=L.LAYOUT_QUAD)]
     for kw in variants:
@@ -473,3 +474,53 @@ def test_batched_rollout_vs_reference_golden(be, gworld, golden):
             assert np.abs(tr[:, 3:6] - g[f"roll{k}_vel"]).max() < 1e-8
             assert np.abs(tr[:, 6:9] - g[f"roll{k}_acc"]).max() < 1e-6 * max(
                 1.0, np.abs(g[f"roll{k}_acc"]).max())
+
+
+def test_k5_dda_bit_exact_vs_cpu_definition(be, oracle, c1):
+    """K5 (north_star's DDA over occupancy; not reference parity): occupancy
+    bits, entry distances (float32 bits) and hit voxel indices equal the CPU
+    definition oracle/rmp_oracle.c orc_dda_trace, and every hit voxel is
+    occupied."""
+    import torch
+
+    from paper_2301_08068_b200.device import DdaPolicyEngine
+
+    scene, grid, states, dirs = c1
+    dg = be.DeviceGrid(grid.values, grid.origin, grid.resolution)
+    occ = be.DeviceOccupancy(dg)
+    bits_ref = oracle.occupancy_bits(grid.values)
+    assert np.array_equal(occ.bits(), bits_ref)
+    for st in states[:3]:
+        t, vox, steps = occ.trace(st.position, dirs, 10.0)
+        t_r, vox_r, steps_r = oracle.dda_trace(grid.values, grid.origin, grid.resolution,
+                                               st.position, dirs, 10.0, workers=8, bits=bits_ref)
+        assert np.array_equal(t.view(np.uint32), t_r.view(np.uint32))
+        assert np.array_equal(vox, vox_r) and np.array_equal(steps, steps_r)
+        h = np.isfinite(t)
+        assert (grid.values[vox[h, 0], vox[h, 1], vox[h, 2]] <= 0.0).all()
+    # edge directions / outside starts on a random grid
+    rng = np.random.default_rng(2)
+    vals = rng.normal(size=(37, 21, 70)) + 1.2
+    dirs2 = rng.normal(size=(3000, 3))
+    dirs2 /= np.linalg.norm(dirs2, axis=1, keepdims=True)
+    dirs2[:50, 0] = 0.0
+    dirs2[50:100, 1] = 0.0
+    dirs2[100:150, 2] = 0.0
+    g2 = be.DeviceGrid(vals, np.array([-0.3, 0.2, 0.1]), 0.07)
+    occ2 = be.DeviceOccupancy(g2)
+    for start in ([0.5, 0.8, 2.0], [-2.0, 0.9, 2.5], [1.0, 5.0, -1.0]):
+        t, vox, steps = occ2.trace(start, dirs2, 4.0)
+        t_r, vox_r, steps_r = oracle.dda_trace(vals, [-0.3, 0.2, 0.1], 0.07, start, dirs2, 4.0)
+        assert np.array_equal(t.view(np.uint32), t_r.view(np.uint32))
+        assert np.array_equal(vox, vox_r) and np.array_equal(steps, steps_r)
+    # fused DDA policy == oracle policy on the DDA distances
+    eng = DdaPolicyEngine(dg, dirs, STATIC_MAP, 10.0)
+    x = torch.tensor(np.stack([s.position for s in states[:4]]), dtype=torch.float64, device="cuda")
+    v = torch.tensor(np.stack([s.velocity for s in states[:4]]), dtype=torch.float64, device="cuda")
+    slots, accs = eng.evaluate(x, v)
+    slots, accs = slots.cpu().numpy(), accs.cpu().numpy()
+    for k, st in enumerate(states[:4]):
+        t_r, _, _ = oracle.dda_trace(grid.values, grid.origin, grid.resolution, st.position, dirs,
+                                     10.0, workers=8, bits=bits_ref)
+        slot_r = oracle.policy_slot(dirs, t_r.astype(np.float64), st.velocity, STATIC_MAP)
+        check_policy(slots[k], accs[k], slot_r, oracle.accel_from_slot(slot_r))
