@@ -70,7 +70,7 @@ enum {
 enum { RMPB_F32 = 0, RMPB_F64 = 1 };                              /* value dtypes */
 enum { RMPB_STORE_AUTO = 0, RMPB_STORE_F32 = 1, RMPB_STORE_F64 = 2 }; /* grid storage */
 enum { RMPB_LAYOUT_LINEAR = 0, RMPB_LAYOUT_QUAD = 1, RMPB_LAYOUT_BRICK = 2,
-       RMPB_LAYOUT_QUADB = 3, RMPB_LAYOUT_AUTO = -1 };
+       RMPB_LAYOUT_QUADB = 3, RMPB_LAYOUT_PAIR64 = 4, RMPB_LAYOUT_AUTO = -1 };
 enum { RMPB_ORDER_IDENTITY = 0, RMPB_ORDER_MORTON = 1 };          /* bundle evaluation order */
 
 typedef struct rmpb_grid rmpb_grid;

@@ -123,7 +123,8 @@ class DeviceGrid:
                ctypes.byref(nb), ctypes.byref(nbr))
         self.storage = {L.STORE_F32: "f32", L.STORE_F64: "f64"}[st.value]
         self.layout = {L.LAYOUT_LINEAR: "linear", L.LAYOUT_QUAD: "quad",
-                       L.LAYOUT_BRICK: "brick", L.LAYOUT_QUADB: "quadb"}[lay.value]
+                       L.LAYOUT_BRICK: "brick", L.LAYOUT_QUADB: "quadb",
+                       L.LAYOUT_PAIR64: "pair64"}[lay.value]
         self.device_bytes = int(nb.value)
         self.bricks = int(nbr.value)
 

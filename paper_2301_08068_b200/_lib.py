@@ -29,7 +29,8 @@ RMPB_ERR_UNSUPPORTED = -4
 
 RMPB_F32, RMPB_F64 = 0, 1
 STORE_AUTO, STORE_F32, STORE_F64 = 0, 1, 2
-LAYOUT_LINEAR, LAYOUT_QUAD, LAYOUT_BRICK, LAYOUT_QUADB, LAYOUT_AUTO = 0, 1, 2, 3, -1
+LAYOUT_LINEAR, LAYOUT_QUAD, LAYOUT_BRICK, LAYOUT_QUADB, LAYOUT_PAIR64, LAYOUT_AUTO = \
+    0, 1, 2, 3, 4, -1
 ORDER_IDENTITY, ORDER_MORTON = 0, 1
 
 _vp = ctypes.c_void_p

@@ -199,6 +199,10 @@ static int with_grid(const rmpb_grid* g, F&& f) {
     LinearGrid<double> a{(const double*)g->d_values, G.nz, G.ny * G.nz};
     return f(a);
   }
+  if (g->layout == LAYOUT_PAIR64) {
+    PairGridF64 a{(const double2*)g->d_values, G.nz - 1, G.ny * (G.nz - 1)};
+    return f(a);
+  }
   if (g->layout == LAYOUT_QUADB) {
     QuadGridF32B a{(const float4*)g->d_values, (G.ny - 1 + 1) / 2, (G.nz - 1 + 1) / 2};
     return f(a);
@@ -321,6 +325,8 @@ static int grid_build(rmpb_grid* g, const void* d_src, int dtype, int storage, i
     store = bad ? RMPB_STORE_F64 : RMPB_STORE_F32;
   }
   g->storage = store;
+  // AUTO: QUAD for f32 maps, PAIR64 for f64 maps (the fastest measured each)
+  if (layout == RMPB_LAYOUT_AUTO) layout = store == RMPB_STORE_F32 ? LAYOUT_QUAD : LAYOUT_PAIR64;
   const size_t esz = store == RMPB_STORE_F32 ? 4 : 8;
   // linear copy in the storage dtype
   void* lin = nullptr;
@@ -351,6 +357,21 @@ static int grid_build(rmpb_grid* g, const void* d_src, int dtype, int storage, i
     cudaFree(lin);
     g->d_values = q;
     g->bytes = nq * 4 * esz;
+  } else if (layout == LAYOUT_PAIR64) {
+    const long long np = g->nx * g->ny * (g->nz - 1);
+    void* q = nullptr;
+    CK(cudaMalloc(&q, np * 16));
+    if (store == RMPB_STORE_F32)
+      k_build_pair64<float><<<grid_blocks(np), 256, 0, st>>>((int)g->nx, (int)g->ny, (int)g->nz,
+                                                           (const float*)lin, (double2*)q);
+    else
+      k_build_pair64<double><<<grid_blocks(np), 256, 0, st>>>((int)g->nx, (int)g->ny, (int)g->nz,
+                                                            (const double*)lin, (double2*)q);
+    CKL();
+    CK(cudaStreamSynchronize(st));
+    cudaFree(lin);
+    g->d_values = q;
+    g->bytes = np * 16;
   } else if (layout == LAYOUT_QUADB) {
     if (store != RMPB_STORE_F32) {
       cudaFree(lin);
@@ -459,8 +480,8 @@ static int grid_new(const void* values, bool on_device, int dtype, int64_t nx, i
   if (!values) return fail(RMPB_ERR_INVALID, "values is NULL");
   if (dtype != RMPB_F32 && dtype != RMPB_F64) return fail(RMPB_ERR_INVALID, "bad dtype %d", dtype);
   TRY(grid_check_dims(nx, ny, nz, res));
-  if (layout == RMPB_LAYOUT_AUTO) layout = LAYOUT_QUAD;
-  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD && layout != LAYOUT_QUADB)
+  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD && layout != LAYOUT_QUADB &&
+      layout != LAYOUT_PAIR64 && layout != RMPB_LAYOUT_AUTO)
     return fail(RMPB_ERR_INVALID, "layout %d not valid here (use rmpb_grid_create_brick)", layout);
   DeviceGuard dg(device);
   if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
@@ -1352,9 +1373,9 @@ extern "C" int rmpb_bake_grid(const rmpb_scene* s, double ox, double oy, double 
   if (!s || !out) return fail(RMPB_ERR_INVALID, "NULL scene / out");
   *out = nullptr;
   TRY(grid_check_dims(nx, ny, nz, res));
-  if (layout == RMPB_LAYOUT_AUTO) layout = LAYOUT_QUAD;
-  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD)
-    return fail(RMPB_ERR_INVALID, "bake_grid supports LINEAR / QUAD layouts");
+  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD && layout != LAYOUT_PAIR64 &&
+      layout != RMPB_LAYOUT_AUTO)
+    return fail(RMPB_ERR_INVALID, "bake_grid supports LINEAR / QUAD / PAIR64 layouts");
   if (device != s->device) return fail(RMPB_ERR_INVALID, "scene lives on device %d", s->device);
   const long long n = nx * ny * nz;
   DeviceGuard dg(device);

@@ -132,6 +132,20 @@ __global__ void k_build_quad(int nx, int ny, int nz, const T* __restrict__ v, Q*
   }
 }
 
+// PAIR64 builder: pair[(i*ny + j)*(nz-1) + k] = {v[i,j,k], v[i,j,k+1]} in f64.
+template <typename T>
+__global__ void k_build_pair64(int nx, int ny, int nz, const T* __restrict__ v, double2* __restrict__ q) {
+  long long n = (long long)nx * ny * (nz - 1);
+  long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long stride = (long long)gridDim.x * blockDim.x;
+  for (; t < n; t += stride) {
+    int k = (int)(t % (nz - 1));
+    long long r = t / (nz - 1);
+    const T* b = v + r * nz + k;
+    q[t] = make_double2((double)b[0], (double)b[1]);
+  }
+}
+
 // QUADB builder: the QUAD record of cell (i,j,k) (i < nx, j < ny-1, k < nz-1)
 // at its 2x2x2-blocked index; padding records stay zero (never read).
 __global__ void k_build_quadb(int nx, int ny, int nz, int bny, int bnz, const float* __restrict__ v,

@@ -36,7 +36,10 @@ constexpr int kAcc = 10;          // a00 a01 a02 a11 a12 a22 b0 b1 b2 cnt
 //   QUADB : QUAD records stored in 2x2x2 blocks of cells (128 B = one L1 line
 //           per block), so the two x-planes of a step and the next steps'
 //           cells share lines far more often than in the z-fastest order.
-enum Layout : int { LAYOUT_LINEAR = 0, LAYOUT_QUAD = 1, LAYOUT_BRICK = 2, LAYOUT_QUADB = 3 };
+//   PAIR64: f64 z-pairs {v[i,j,k], v[i,j,k+1]} (double2): 4 aligned 16-B loads
+//           per step and no f32->f64 conversions.
+enum Layout : int { LAYOUT_LINEAR = 0, LAYOUT_QUAD = 1, LAYOUT_BRICK = 2, LAYOUT_QUADB = 3,
+                    LAYOUT_PAIR64 = 4 };
 
 struct GridGeom {
   int nx, ny, nz;
@@ -130,6 +133,20 @@ struct QuadGridF32B {
     Corners k;
     k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
     k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;
+    return k;
+  }
+};
+
+struct PairGridF64 {
+  const double2* __restrict__ q;
+  int py, px;  // strides in pairs: (nz-1), ny*(nz-1)
+  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    const double2* b = q + (unsigned)(ix * px + iy * py + iz);
+    double2 a0 = __ldg(b), a1 = __ldg(b + (unsigned)py);
+    double2 c0 = __ldg(b + (unsigned)px), c1 = __ldg(b + (unsigned)(px + py));
+    Corners k;
+    k.v000 = a0.x; k.v001 = a0.y; k.v010 = a1.x; k.v011 = a1.y;
+    k.v100 = c0.x; k.v101 = c0.y; k.v110 = c1.x; k.v111 = c1.y;
     return k;
   }
 };

@@ -27,7 +27,7 @@ def timed(eng, xx, vv, reps=3):
         e0.record(); eng.evaluate(xx, vv); e1.record(); e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     return min(ts)
-variants = [("f32", "quad"), ("f32", "quadb"), ("f32", "linear")]
+variants = [("f32", "quad"), ("f32", "pair64"), ("f64", "pair64")]
 for kern in (2,):
     L.set_option("kernel", kern)
     for st, lay in variants:
@@ -35,7 +35,7 @@ for kern in (2,):
             continue
         dg = b200.DeviceGrid(grid.values, grid.origin, grid.resolution,
                              storage={"f32": L.STORE_F32, "f64": L.STORE_F64}[st],
-                             layout={"quad": L.LAYOUT_QUAD, "linear": L.LAYOUT_LINEAR, "quadb": L.LAYOUT_QUADB}[lay])
+                             layout={"quad": L.LAYOUT_QUAD, "linear": L.LAYOUT_LINEAR, "quadb": L.LAYOUT_QUADB, "pair64": L.LAYOUT_PAIR64}[lay])
         eng = RayPolicyEngine(dg, bundle, params, 10.0)
         ms = timed(eng, x, v)
         lat = []

@@ -222,6 +222,7 @@ def test_layouts_and_storage_identical(be, oracle, c1):
     variants = [dict(storage=L.STORE_F32, layout=L.LAYOUT_LINEAR),
                 dict(storage=L.STORE_F32, layout=L.LAYOUT_QUAD),
                 dict(storage=L.STORE_F32, layout=L.LAYOUT_QUADB),
+                dict(storage=L.STORE_F32, layout=L.LAYOUT_PAIR64),
                 dict(storage=L.STORE_F64, layout=L.LAYOUT_LINEAR),
                 dict(storage=L.STORE_F64, layout=L.LAYOUT_QUAD)]
     for kw in variants:
