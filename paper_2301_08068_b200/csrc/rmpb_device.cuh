@@ -218,35 +218,41 @@ __device__ __forceinline__ double interp(const G& grid, const GridGeom& g, doubl
 
 // Cell coordinate of one axis, identical to the reference's
 //   u = clamp(u, 0, n-1); i = min((int64)floor(u), n-2); f = u - (double)i
-// without the XU pipe and without double selects on the common path:
-// u + 1.5*2^52 rounds u (|u| < 2^31) to the nearest integer, which sits in
-// the low 32 mantissa bits (two's complement); a compare turns round into
-// floor.  i in [0, n-2] then needs no clamp and f = u - floor(u) is exactly
-// the reference's f.  Otherwise u was clamped by the reference: u < 0 gives
-// (i, f) = (0, 0) and u >= n-1 gives (n-2, (n-1)-(n-2) = 1) -- a rarely
-// taken branch (only at the map boundary).  The points traced always lie in
-// the slab interval, so |u| is far below 2^31; NaN is handled by the caller.
-__device__ __forceinline__ void cell_coord(double u, int nm2, int& i, double& f) {
+// without the XU pipe and without selects on the common path: with
+// M = 1.5 * 2^52 (ulp 1 on [2^52, 2^53)) and |u| < 2^51, RZ(u + M) - M is
+// exactly floor(u) (the sum is positive, so round-toward-zero rounds down),
+// and the low mantissa word of RZ(u + M) is floor(u) as a two's-complement
+// int.  Then f = u - floor(u) is the reference's f whenever floor(u) lies in
+// [0, n-2]; otherwise the reference clamped u: see cell_fix (rare, only at
+// the map boundary).
+__device__ __forceinline__ void cell_floor(double u, int& i, double& f) {
   const double M = 6755399441055744.0;  // 1.5 * 2^52
-  const double big = u + M;
-  double r = big - M;
-  int ri = __double2loint(big);
-  if (r > u) { r = r - 1.0; ri -= 1; }
-  f = u - r;
-  if ((unsigned)ri > (unsigned)nm2) {
-    if (ri < 0) { ri = 0; f = 0.0; } else { ri = nm2; f = 1.0; }
+  const double big = __dadd_rz(u, M);
+  i = __double2loint(big);
+  f = u - (big - M);
+}
+// u < 0 -> (0, 0); u >= n-1 -> (n-2, (n-1) - (n-2) = 1).
+__device__ __forceinline__ void cell_fix(int nm2, int& i, double& f) {
+  if ((unsigned)i > (unsigned)nm2) {
+    if (i < 0) { i = 0; f = 0.0; } else { i = nm2; f = 1.0; }
   }
-  i = ri;
 }
 
-// interp with exdiv + cell_coord: bit-identical to interp() above.
+// interp with exdiv + cell_floor / cell_fix: bit-identical to interp() above.
 template <class G>
 __device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, double px,
                                               double py, double pz, int& ix, int& iy, int& iz) {
   double fx, fy, fz;
-  cell_coord(exdiv(px - g.ox, g.res, g.rhi, g.rlo), g.nx - 2, ix, fx);
-  cell_coord(exdiv(py - g.oy, g.res, g.rhi, g.rlo), g.ny - 2, iy, fy);
-  cell_coord(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), g.nz - 2, iz, fz);
+  cell_floor(exdiv(px - g.ox, g.res, g.rhi, g.rlo), ix, fx);
+  cell_floor(exdiv(py - g.oy, g.res, g.rhi, g.rlo), iy, fy);
+  cell_floor(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), iz, fz);
+  // one (rarely taken) branch for all three boundary clamps
+  if (((unsigned)ix > (unsigned)(g.nx - 2)) | ((unsigned)iy > (unsigned)(g.ny - 2)) |
+      ((unsigned)iz > (unsigned)(g.nz - 2))) {
+    cell_fix(g.nx - 2, ix, fx);
+    cell_fix(g.ny - 2, iy, fy);
+    cell_fix(g.nz - 2, iz, fz);
+  }
   Corners c = grid.load(ix, iy, iz);
   double c00 = c.v000 + fz * (c.v001 - c.v000);
   double c01 = c.v010 + fz * (c.v011 - c.v010);

@@ -160,6 +160,7 @@ constexpr int kQueue = 64;
 constexpr int kPrep = 32;
 
 struct K2Smem {
+  double pose[4];  // the unit's robot position (read per step: saves registers)
   double acc[kWarps][9];
   double qt[kWarps][kQueue];
   int qr[kWarps][kQueue];
@@ -208,7 +209,9 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   if (io.active && !io.active[pose]) return;  // whole CTA: finished rollout
   double sx, sy, sz;
   io.pose(pose, sx, sy, sz);
+  if (tid == 0) { sm.pose[0] = sx; sm.pose[1] = sy; sm.pose[2] = sz; }
   if (lane < 9) sm.acc[warp][lane] = 0.0;
+  __syncthreads();
   const int begin = seg * seg_rays;
   const int end = min(begin + seg_rays, b.n);
   const int nchunks = (end - begin + 31) >> 5;
@@ -235,7 +238,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
         double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
         if (ok) {
           ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
-          ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, b.recip(r), t0, t1);
+          ok = box_span_fast(g, sm.pose[0], sm.pose[1], sm.pose[2], ex, ey, ez, b.recip(r), t0, t1);
           if (ok) {
             t0 = t0 > 0.0 ? t0 : 0.0;
             t1 = t1 < max_range ? t1 : max_range;
@@ -280,7 +283,8 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     bool enq = false, hit_now = false;
     if (alive) {
       int ix, iy, iz;
-      const double d = interp_fast(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
+      const double px = sm.pose[0], py = sm.pose[1], pz = sm.pose[2];
+      const double d = interp_fast(grid, g, px + t * dx, py + t * dy, pz + t * dz, ix, iy, iz);
       if (RAYOUT) ++steps;
       bool fin, hit = false;
       if (d < eps) {

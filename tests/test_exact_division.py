@@ -1,5 +1,7 @@
-"""CPU: the FMA-based exact division the CUDA trace uses instead of IEEE
-`/` (rmpb_device.cuh ``exdiv``) reproduces a/b bit-for-bit."""
+"""CPU: the arithmetic substitutions of the CUDA trace reproduce the
+reference bit-for-bit: the FMA-based division (rmpb_device.cuh ``exdiv``)
+equals IEEE a/b, and the round-toward-zero floor + boundary fix-up
+(``cell_floor`` / ``cell_fix``) equals the reference clamp/floor/min."""
 
 import os
 import subprocess
@@ -14,3 +16,11 @@ def test_markstein_division_bit_exact(tmp_path):
                     "-lpthread"], check=True)
     out = subprocess.run([exe, "40000000"], capture_output=True, text=True, check=True).stdout
     assert "mismatches=0" in out, out
+
+
+def test_cell_floor_bit_exact(tmp_path):
+    src = os.path.join(ROOT, "oracle", "check_cell_floor.c")
+    exe = str(tmp_path / "check_cell_floor")
+    subprocess.run(["gcc", "-O1", "-frounding-math", "-o", exe, src, "-lm"], check=True)
+    out = subprocess.run([exe], capture_output=True, text=True, check=True).stdout
+    assert "bad=0" in out, out
