@@ -161,6 +161,8 @@ constexpr int kPrep = 32;
 
 struct K2Smem {
   double pose[4];  // the unit's robot position (read per step: saves registers)
+  double exit_lo[3], exit_hi[3];  // (lo - s), (hi - s) per axis, for inside poses
+  int inside;      // pose inside the node domain: slab entry is t = 0 exactly
   double acc[kWarps][9];
   double qt[kWarps][kQueue];
   int qr[kWarps][kQueue];
@@ -209,7 +211,15 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   if (io.active && !io.active[pose]) return;  // whole CTA: finished rollout
   double sx, sy, sz;
   io.pose(pose, sx, sy, sz);
-  if (tid == 0) { sm.pose[0] = sx; sm.pose[1] = sy; sm.pose[2] = sz; }
+  if (tid == 0) {
+    sm.pose[0] = sx; sm.pose[1] = sy; sm.pose[2] = sz;
+    // Inside the domain every axis' entry quotient is <= 0, so the reference's
+    // t = max(t0, 0) is exactly 0 and only the exit side is needed:
+    // (hi - s)/d for d > 0, (lo - s)/d for d < 0 (_ckern.pyx:171-212).
+    sm.inside = sx >= g.ox && sx <= g.hx && sy >= g.oy && sy <= g.hy && sz >= g.oz && sz <= g.hz;
+    sm.exit_lo[0] = g.ox - sx; sm.exit_lo[1] = g.oy - sy; sm.exit_lo[2] = g.oz - sz;
+    sm.exit_hi[0] = g.hx - sx; sm.exit_hi[1] = g.hy - sy; sm.exit_hi[2] = g.hz - sz;
+  }
   if (lane < 9) sm.acc[warp][lane] = 0.0;
   __syncthreads();
   const int begin = seg * seg_rays;
@@ -238,11 +248,32 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
         double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
         if (ok) {
           ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
-          ok = box_span_fast(g, sm.pose[0], sm.pose[1], sm.pose[2], ex, ey, ez, b.recip(r), t0, t1);
-          if (ok) {
-            t0 = t0 > 0.0 ? t0 : 0.0;
-            t1 = t1 < max_range ? t1 : max_range;
+          if (sm.inside) {
+            const RecipDir q = b.recip(r);
+            double thi = CUDART_INF;
+            if (ex != 0.0) {
+              const double tb = exdiv(ex > 0.0 ? sm.exit_hi[0] : sm.exit_lo[0], ex, q.hx, q.lx);
+              thi = tb < thi ? tb : thi;
+            }
+            if (ey != 0.0) {
+              const double tb = exdiv(ey > 0.0 ? sm.exit_hi[1] : sm.exit_lo[1], ey, q.hy, q.ly);
+              thi = tb < thi ? tb : thi;
+            }
+            if (ez != 0.0) {
+              const double tb = exdiv(ez > 0.0 ? sm.exit_hi[2] : sm.exit_lo[2], ez, q.hz, q.lz);
+              thi = tb < thi ? tb : thi;
+            }
+            t0 = 0.0;
+            t1 = thi < max_range ? thi : max_range;
             ok = !(t0 > t1);
+          } else {
+            ok = box_span_fast(g, sm.pose[0], sm.pose[1], sm.pose[2], ex, ey, ez, b.recip(r), t0,
+                               t1);
+            if (ok) {
+              t0 = t0 > 0.0 ? t0 : 0.0;
+              t1 = t1 < max_range ? t1 : max_range;
+              ok = !(t0 > t1);
+            }
           }
           if (RAYOUT && !ok && ro.t) {
             const int o = b.perm ? b.perm[r] : r;
