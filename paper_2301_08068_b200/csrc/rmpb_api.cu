@@ -32,7 +32,7 @@ using namespace rmpb;
 static thread_local std::string g_err;
 static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int64_t> g_opt_seg_rays{0};
-static std::atomic<int64_t> g_opt_kernel{2};  // 1: one ray per thread per pass; 2: lane refill
+static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread per pass, 2 lane refill
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -281,7 +281,7 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
     return RMPB_OK;
   }
   if (!strcmp(name, "kernel")) {
-    if (value != 1 && value != 2) return fail(RMPB_ERR_INVALID, "kernel must be 1 or 2");
+    if (value < 0 || value > 2) return fail(RMPB_ERR_INVALID, "kernel must be 0 (auto), 1 or 2");
     g_opt_kernel.store(value);
     return RMPB_OK;
   }
@@ -791,7 +791,9 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
   Bundle bv = bundle_view(b);
   const long long units = (long long)P * segs;
   if (units >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many CTA units");
-  const bool v2 = g_opt_kernel.load() == 2;
+  // one ray per thread -> the lean kernel (nothing to refill); else lane refill
+  const int64_t kopt = g_opt_kernel.load();
+  const bool v2 = kopt == 2 || (kopt == 0 && seg_rays > kBlock);
   return with_grid(g, [&](auto acc) -> int {
     using G = decltype(acc);
     if (!v2)

@@ -361,6 +361,32 @@ __device__ __forceinline__ TraceResult trace_ray(const G& grid, const GridGeom& 
   return r;
 }
 
+// Sphere trace with the exact fast arithmetic (exdiv slab interval with the
+// per-ray reciprocals, interp_fast): bit-identical to trace_ray.
+template <class G>
+__device__ __forceinline__ TraceResult trace_ray_fast(const G& grid, const GridGeom& g, double sx,
+                                                      double sy, double sz, double dx, double dy,
+                                                      double dz, const RecipDir& q,
+                                                      double max_range, double eps,
+                                                      double step_scale) {
+  TraceResult r;
+  r.t = CUDART_INF; r.cx = r.cy = r.cz = -1; r.steps = 0;
+  double t0, t1;
+  if (!box_span_fast(g, sx, sy, sz, dx, dy, dz, q, t0, t1)) return r;
+  double t = t0 > 0.0 ? t0 : 0.0;
+  const double t_end = t1 < max_range ? t1 : max_range;
+  if (t > t_end) return r;
+  int ix, iy, iz;
+  while (true) {
+    const double d = interp_fast(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
+    ++r.steps;
+    if (d < eps) { r.t = t; r.cx = ix; r.cy = iy; r.cz = iz; break; }
+    t += step_scale * d;
+    if (!(t <= t_end)) break;
+  }
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // Per-ray obstacle policy (rmpnav/_kernels/_ckern.pyx:290-316).  `dir` is the
 // cast direction; r = -dir points away from the obstacle (policies.py:550-552).

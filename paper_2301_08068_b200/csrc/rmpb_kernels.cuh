@@ -103,7 +103,9 @@ __device__ __forceinline__ void finish_unit(Acc& acc, const PoseIO& io, int pose
   }
 }
 
-// K1 / K3: fused sphere trace + per-ray policy + reduction (+ pinv).
+// K1 latency kernel: one ray per thread per pass, no refill bookkeeping --
+// used when every thread owns a single ray (small batches, e.g. one pose),
+// where the longest ray's dependent chain is the whole story.
 // grid: P * segs CTAs of kBlock threads; segment = seg_rays consecutive
 // stored rays of the bundle.
 template <class G>
@@ -120,9 +122,11 @@ k_ray_policy(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max
   const int begin = seg * seg_rays;
   const int end = min(begin + seg_rays, b.n);
   int my_steps = 0;
+  if (io.active && !io.active[pose]) return;
   for (int i = begin + threadIdx.x; i < end; i += kBlock) {
     const double dx = b.dx[i], dy = b.dy[i], dz = b.dz[i];
-    TraceResult r = trace_ray(grid, g, sx, sy, sz, dx, dy, dz, max_range, eps, step_scale);
+    TraceResult r = trace_ray_fast(grid, g, sx, sy, sz, dx, dy, dz, b.recip(i), max_range, eps,
+                                   step_scale);
     policy_accumulate(acc, dx, dy, dz, r.t, vx, vy, vz, p);
     my_steps += r.steps;
     if (ro.t) {

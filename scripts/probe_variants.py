@@ -28,7 +28,7 @@ def timed(eng, xx, vv, reps=3):
         ts.append(e0.elapsed_time(e1))
     return min(ts)
 variants = [("f32", "quad"), ("f32", "pair64"), ("f64", "pair64")]
-for kern in (2,):
+for kern in (0,):
     L.set_option("kernel", kern)
     for st, lay in variants:
         if kern == 1 and (st, lay) != ("f32", "quad"):
@@ -46,5 +46,5 @@ for kern in (2,):
         out[f"k{kern}_{st}_{lay}"] = {"batch_ms": round(ms, 3), "hz": round(P_BATCH / ms * 1e3, 1),
                                       "p1_us_med": round(statistics.median(lat), 1)}
         print(json.dumps({f"k{kern}_{st}_{lay}": out[f"k{kern}_{st}_{lay}"]}), flush=True)
-L.set_option("kernel", 2)
+L.set_option("kernel", 0)
 print(json.dumps(out))
