@@ -233,6 +233,11 @@ static PolicyParams make_params(const double p[7], double min_range) {
   PolicyParams q;
   q.eta_rep = p[0]; q.nu_rep = p[1]; q.eta_damp = p[2]; q.nu_damp = p[3];
   q.eps_p = p[4]; q.radius = p[5]; q.c = p[6]; q.min_range = min_range;
+  recip_dd(q.nu_rep, q.rnr_h, q.rnr_l);
+  recip_dd(q.nu_damp, q.rnd_h, q.rnd_l);
+  recip_dd(q.radius, q.rr_h, q.rr_l);
+  q.rr2 = q.radius * q.radius;  // the reference's RN(radius * radius) divisor
+  recip_dd(q.rr2, q.rr2_h, q.rr2_l);
   return q;
 }
 
@@ -1013,7 +1018,10 @@ static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
   io.partials = (double*)ws->partials.p;
   io.tickets = (unsigned*)ws->tickets.p;
   const long long units = (long long)S_ * segs;
-  k_lidar_policy<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
+  if (g_opt_kernel.load() == 1)
+    k_lidar_policy<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
+  else
+    k_lidar_policy2<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
   CKL();
   return RMPB_OK;
 }

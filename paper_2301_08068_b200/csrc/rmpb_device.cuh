@@ -393,6 +393,9 @@ __device__ __forceinline__ TraceResult trace_ray_fast(const G& grid, const GridG
 struct PolicyParams {
   double eta_rep, nu_rep, eta_damp, nu_damp, eps_p, radius, c;  // as_tuple order, policies.py:80-83
   double min_range;
+  // double-double reciprocals of the constant divisors (exdiv): nu_rep,
+  // nu_damp, radius and RN(radius * radius)
+  double rnr_h, rnr_l, rnd_h, rnd_l, rr_h, rr_l, rr2, rr2_h, rr2_l;
 };
 
 struct Acc {
@@ -416,10 +419,11 @@ __device__ __forceinline__ void policy_accumulate(Acc& acc, double dx, double dy
   double toward = dx * vx + dy * vy + dz * vz;
   if (!(d < p.radius) || !(toward > 0.0)) return;
   double rx = -dx, ry = -dy, rz = -dz;
-  double frep = p.eta_rep * exp(-d / p.nu_rep);
+  // divisions by the constant parameters use exdiv (bit-identical to `/`)
+  double frep = p.eta_rep * exp(exdiv(-d, p.nu_rep, p.rnr_h, p.rnr_l));
   double g = toward;
-  double fdamp = p.eta_damp / (d / p.nu_damp + p.eps_p) * g * g;
-  double w = d * d / (p.radius * p.radius) - 2.0 * d / p.radius + 1.0;
+  double fdamp = p.eta_damp / (exdiv(d, p.nu_damp, p.rnd_h, p.rnd_l) + p.eps_p) * g * g;
+  double w = exdiv(d * d, p.rr2, p.rr2_h, p.rr2_l) - exdiv(2.0 * d, p.radius, p.rr_h, p.rr_l) + 1.0;
   double smag = fdamp / (fdamp + p.c * log1p(exp(-2.0 * p.c * fdamp)));
   double a = w * smag * smag;
   if (a != 0.0) {

@@ -436,6 +436,126 @@ k_lidar_policy(ScanIO sc, PoseIO io, PolicyParams p, int segs, int seg_rays) {
   finish_unit(acc, io, scan, seg, segs);
 }
 
+// K2 v2: the same reduction, streaming-first.  Lanes stream 32 beams per
+// chunk (4 chunks' range / validity loads in flight), count the valid beams
+// with a ballot and queue (range, beam index) of the beams inside the
+// activation radius.  Each full batch of 32 queued beams is then evaluated
+// by the whole warp: one converged gather of the 32 lattice directions,
+// rotation, closing-velocity test and policy, butterfly-reduced.  Beam ->
+// warp assignment and queue order are data-determined: bitwise reproducible.
+struct LidarSmem {
+  double acc[kWarps][9];
+  double qd[kWarps][kQueue];
+  int qi[kWarps][kQueue];
+};
+
+__device__ __forceinline__ void lidar_flush(LidarSmem& sm, const ScanIO& sc, const double* R,
+                                            bool rot, int warp, int lane, bool valid, int i,
+                                            double d, double vx, double vy, double vz,
+                                            const PolicyParams& p) {
+  Acc a;
+  a.zero();
+  if (valid) {
+    const double ex = sc.dirs[3 * i], ey = sc.dirs[3 * i + 1], ez = sc.dirs[3 * i + 2];
+    double wx = ex, wy = ey, wz = ez;
+    if (rot) {  // directions @ orientation.T  (rays.py:172-173)
+      wx = ex * R[0] + ey * R[1] + ez * R[2];
+      wy = ex * R[3] + ey * R[4] + ez * R[5];
+      wz = ex * R[6] + ey * R[7] + ez * R[8];
+    }
+    policy_accumulate(a, wx, wy, wz, d, vx, vy, vz, p);
+  }
+  const bool nz = a.a00 != 0.0 || a.a11 != 0.0 || a.a22 != 0.0 || a.b0 != 0.0 || a.b1 != 0.0 ||
+                  a.b2 != 0.0 || a.a01 != 0.0 || a.a02 != 0.0 || a.a12 != 0.0;
+  if (!__any_sync(0xffffffffu, nz)) return;
+  double v[9] = {a.a00, a.a01, a.a02, a.a11, a.a12, a.a22, a.b0, a.b1, a.b2};
+#pragma unroll
+  for (int k = 0; k < 9; ++k) v[k] = warp_sum(v[k]);
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < 9; ++k) sm.acc[warp][k] += v[k];
+  }
+}
+
+__global__ void __launch_bounds__(kBlock, 4)
+k_lidar_policy2(ScanIO sc, PoseIO io, PolicyParams p, int segs, int seg_rays) {
+  __shared__ LidarSmem sm;
+  __shared__ double sR[9];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+  const int unit = blockIdx.x;
+  const int scan = unit / segs, seg = unit - scan * segs;
+  const bool rot = sc.R != nullptr;
+  if (rot && tid < 9) sR[tid] = sc.R[9 * scan + tid];
+  const double* rg = sc.ranges + (size_t)scan * sc.n;
+  const unsigned char* vl = sc.valid ? sc.valid + (size_t)scan * sc.n : nullptr;
+  if (lane < 9) sm.acc[warp][lane] = 0.0;
+  __syncthreads();
+  const int begin = seg * seg_rays;
+  const int end = min(begin + seg_rays, sc.n);
+  const int nchunks = (end - begin + 31) >> 5;
+  int qn = 0, cnt = 0;
+  constexpr int U = 4;
+  for (int c0 = warp; c0 < nchunks; c0 += U * kWarps) {
+    double dd[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = begin + ((c0 + u * kWarps) << 5) + lane;
+      const bool in = c0 + u * kWarps < nchunks && i < end;
+      dd[u] = in ? __ldcs(rg + i) : CUDART_INF;
+      if (in && vl && !__ldcs(vl + i)) dd[u] = CUDART_INF;
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const double d = dd[u];
+      const bool counted = !(d != d || d == CUDART_INF || d < p.min_range);
+      const bool enq = counted && d < p.radius;
+      cnt += __popc(__ballot_sync(FULL, counted));
+      const unsigned em = __ballot_sync(FULL, enq);
+      if (em) {
+        if (enq) {
+          const int pos = qn + __popc(em & lt);
+          sm.qd[warp][pos] = d;
+          sm.qi[warp][pos] = begin + ((c0 + u * kWarps) << 5) + lane;
+        }
+        qn += __popc(em);
+        if (qn >= 32) {
+          __syncwarp();
+          double vx, vy, vz;
+          io.vel(scan, vx, vy, vz);
+          lidar_flush(sm, sc, sR, rot, warp, lane, true, sm.qi[warp][lane], sm.qd[warp][lane], vx,
+                      vy, vz, p);
+          __syncwarp();
+          if (lane < qn - 32) {
+            sm.qd[warp][lane] = sm.qd[warp][lane + 32];
+            sm.qi[warp][lane] = sm.qi[warp][lane + 32];
+          }
+          qn -= 32;
+          __syncwarp();
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (qn > 0) {
+    double vx, vy, vz;
+    io.vel(scan, vx, vy, vz);
+    const bool valid = lane < qn;
+    lidar_flush(sm, sc, sR, rot, warp, lane, valid, valid ? sm.qi[warp][lane] : 0,
+                valid ? sm.qd[warp][lane] : 1.0, vx, vy, vz, p);
+  }
+  __syncwarp();
+  Acc acc;
+  acc.zero();
+  if (lane == 0) {
+    acc.a00 = sm.acc[warp][0]; acc.a01 = sm.acc[warp][1]; acc.a02 = sm.acc[warp][2];
+    acc.a11 = sm.acc[warp][3]; acc.a12 = sm.acc[warp][4]; acc.a22 = sm.acc[warp][5];
+    acc.b0 = sm.acc[warp][6]; acc.b1 = sm.acc[warp][7]; acc.b2 = sm.acc[warp][8];
+    acc.cnt = cnt;
+  }
+  finish_unit(acc, io, scan, seg, segs);
+}
+
 // K2b: LiDAR-direct from raw sensor-frame points (no map, no lattice): the
 // beam direction is p/|p| and its range |p|; zero / non-finite points are
 // invalid.  Float32 xyz as delivered by the sensor driver.
