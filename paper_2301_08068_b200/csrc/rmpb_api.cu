@@ -808,6 +808,7 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
       k_ray_policy2<G, true><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
                                                                  max_range, eps, step_scale, segs,
                                                                  seg_rays, ro);
+
     else
       k_ray_policy2<G, false><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
                                                                   max_range, eps, step_scale, segs,

@@ -27,7 +27,7 @@ def timed(eng, xx, vv, reps=3):
         e0.record(); eng.evaluate(xx, vv); e1.record(); e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     return min(ts)
-variants = [("f32", "quad"), ("f32", "pair64"), ("f64", "pair64")]
+variants = [("f32", "quad"), ("f64", "pair64")]
 for kern in (0,):
     L.set_option("kernel", kern)
     for st, lay in variants:
