@@ -286,25 +286,31 @@ _bundles: "OrderedDict[tuple, tuple]" = OrderedDict()
 _scenes: "OrderedDict[int, tuple]" = OrderedDict()
 
 
-_probe_idx: dict[int, np.ndarray] = {}
-
-
 def _fingerprint(a: np.ndarray) -> int:
-    """Cheap content check for cache hits: crc32 of 256 fixed pseudo-random
-    elements plus both ends.  An in-place edit that touches none of them is
-    not seen -- call invalidate_caches() after mutating a cached array."""
+    """Cheap content check for cache hits: crc32 of 8 cache lines spread over
+    the array plus both ends (a few cache misses, not a scan).  An in-place
+    edit that touches none of them is not seen -- call invalidate_caches()
+    after mutating a cached array."""
     flat = a.reshape(-1)
     n = flat.shape[0]
-    idx = _probe_idx.get(n)
-    if idx is None:
-        idx = np.unique(np.random.default_rng(n).integers(0, n, size=256)) if n > 4096 \
-            else np.arange(n)
-        _probe_idx[n] = idx
-    h = zlib.crc32(np.take(flat, idx).view(np.uint8))
-    if n > 4096:
-        h = zlib.crc32(flat[:64].view(np.uint8), h)
-        h = zlib.crc32(flat[-64:].view(np.uint8), h)
+    if n <= 512:
+        return zlib.crc32(flat)
+    step = n // 8
+    h = zlib.crc32(flat[-8:])
+    for k in range(8):
+        h = zlib.crc32(flat[k * step:k * step + 8], h)
     return h
+
+
+def _frozen(a: np.ndarray) -> bool:
+    """True when neither the array nor any base it views is writable (e.g.
+    RayBundle.directions from sample_directions): its content cannot change
+    through NumPy, so the cache needs no content check."""
+    while isinstance(a, np.ndarray):
+        if a.flags.writeable:
+            return False
+        a = a.base
+    return a is None or isinstance(a, (bytes,))
 
 
 def invalidate_caches() -> None:
@@ -342,7 +348,7 @@ def device_bundle(dirs) -> DeviceBundle:
     if isinstance(dirs, DeviceBundle):
         return dirs
     d = _f64(dirs, (-1, 3))
-    key = (d.ctypes.data, d.shape[0], _device, _fingerprint(d))
+    key = (d.ctypes.data, d.shape[0], _device, 0 if _frozen(d) else _fingerprint(d))
     with _lock:
         hit = _bundles.get(key)
         if hit is not None:
@@ -359,7 +365,7 @@ def register_bundle(dirs: np.ndarray, dev: DeviceBundle) -> None:
     """Associate a host direction array with an existing device bundle (e.g.
     one generated on device) so later calls do not re-upload it."""
     d = _f64(dirs, (-1, 3))
-    key = (d.ctypes.data, d.shape[0], dev.device, _fingerprint(d))
+    key = (d.ctypes.data, d.shape[0], dev.device, 0 if _frozen(d) else _fingerprint(d))
     with _lock:
         _bundles[key] = (dev, d)
         while len(_bundles) > _MAX_BUNDLES:
@@ -457,24 +463,42 @@ def policy_reduce(dirs: np.ndarray, dists: np.ndarray, v, params: tuple, min_ran
 # --------------------------------------------------------------------------
 # fused / batched entries (beyond the reference protocol)
 
+_param_cache: dict = {}
+
+
+def _params_cached(params):
+    key = tuple(params) if not isinstance(params, np.ndarray) else None
+    if key is not None:
+        hit = _param_cache.get(key)
+        if hit is None:
+            hit = _params(params)
+            if len(_param_cache) < 64:
+                _param_cache[key] = hit
+        return hit
+    return _params(params)
+
+
 def ray_policy_fused(values, origin, res, start, velocity, dirs, params, max_range, eps,
                      step_scale, with_rays=False):
     """Fused ray_policy (policies.py:182-192): returns (slot13, accel3) and,
     with ``with_rays``, per-ray (t, cells, steps) in original ray order."""
     g = device_grid(values, origin, res)
     b = device_bundle(dirs)
-    x = _vec3(start)
-    v = _vec3(velocity)
-    slot = np.empty(13)
-    acc = np.empty(3)
+    xv = np.empty(6)
+    xv[0:3] = start
+    xv[3:6] = velocity
+    out = np.empty(16)
     t = cells = steps = None
     if with_rays:
         t = np.empty(b.n)
         cells = np.empty((b.n, 3), np.int32)
         steps = np.empty(b.n, np.int32)
-    L.call("rmpb_ray_policy", g.handle, b.handle, x.ctypes.data, v.ctypes.data,
-           _params(params).ctypes.data, float(max_range), float(eps), float(step_scale),
-           slot.ctypes.data, acc.ctypes.data, _ptr(t), _ptr(cells), _ptr(steps), None)
+    base = xv.ctypes.data
+    L.check(L.load().rmpb_ray_policy(
+        g.handle, b.handle, base, base + 24, _params_cached(params).ctypes.data,
+        float(max_range), float(eps), float(step_scale), out.ctypes.data,
+        out.ctypes.data + 104, _ptr(t), _ptr(cells), _ptr(steps), None), "rmpb_ray_policy")
+    slot, acc = out[:13], out[13:]
     if with_rays:
         return slot, acc, t, cells, steps
     return slot, acc
