@@ -72,6 +72,10 @@ enum { RMPB_STORE_AUTO = 0, RMPB_STORE_F32 = 1, RMPB_STORE_F64 = 2 }; /* grid st
 enum { RMPB_LAYOUT_LINEAR = 0, RMPB_LAYOUT_QUAD = 1, RMPB_LAYOUT_BRICK = 2,
        RMPB_LAYOUT_QUADB = 3, RMPB_LAYOUT_PAIR64 = 4, RMPB_LAYOUT_AUTO = -1 };
 enum { RMPB_ORDER_IDENTITY = 0, RMPB_ORDER_MORTON = 1 };          /* bundle evaluation order */
+/* EXACT: bit-identical to the reference (fp64, its operation order).  FAST:
+ * fp32 march with FMA, opt-in, NOT reference-exact (grazing rays may differ;
+ * deviation measured in tests/test_gpu_parity.py). */
+enum { RMPB_MODE_EXACT = 0, RMPB_MODE_FAST = 1 };
 
 typedef struct rmpb_grid rmpb_grid;
 typedef struct rmpb_bundle rmpb_bundle;
@@ -140,6 +144,12 @@ RMPB_EXPORT int rmpb_ray_policy_batch_device(const rmpb_grid* g, const rmpb_bund
                                  const double* d_v, int64_t P, const double params[7],
                                  double max_range, double eps, double step_scale, double* d_slot,
                                  double* d_accel, uint64_t* opt_step_total, void* stream);
+/* Same with an explicit mode (RMPB_MODE_EXACT / RMPB_MODE_FAST). */
+RMPB_EXPORT int rmpb_ray_policy_batch_device_mode(const rmpb_grid* g, const rmpb_bundle* b,
+                                      const double* d_x, const double* d_v, int64_t P,
+                                      const double params[7], double max_range, double eps,
+                                      double step_scale, int mode, double* d_slot,
+                                      double* d_accel, uint64_t* opt_step_total, void* stream);
 /* Partial slot of stored rays [ray_begin, ray_end) of one pose (no pinv):
  * the per-GPU share of a ray-split pose (config C5).  Device pointers. */
 RMPB_EXPORT int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bundle* b, const double* d_x,

@@ -32,6 +32,7 @@ STORE_AUTO, STORE_F32, STORE_F64 = 0, 1, 2
 LAYOUT_LINEAR, LAYOUT_QUAD, LAYOUT_BRICK, LAYOUT_QUADB, LAYOUT_PAIR64, LAYOUT_AUTO = \
     0, 1, 2, 3, 4, -1
 ORDER_IDENTITY, ORDER_MORTON = 0, 1
+MODE_EXACT, MODE_FAST = 0, 1
 
 _vp = ctypes.c_void_p
 _i64 = ctypes.c_int64
@@ -60,6 +61,8 @@ _SIGS = {
     "rmpb_ray_policy_batch": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _d, _d, _d, _vp, _vp, _vp]),
     "rmpb_ray_policy_batch_device": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _d, _d, _d, _vp, _vp,
                                           _vp, _vp]),
+    "rmpb_ray_policy_batch_device_mode": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _d, _d, _d, _i,
+                                               _vp, _vp, _vp, _vp]),
     "rmpb_ray_policy_range_device": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _d, _d, _d, _vp,
                                           _vp]),
     "rmpb_fold_resolve_device": (_i, [_vp, _i64, _vp, _vp, _vp]),

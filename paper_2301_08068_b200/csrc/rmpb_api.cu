@@ -792,18 +792,24 @@ static Bundle bundle_view(const rmpb_bundle* b) {
 static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io, int64_t P,
                              const PolicyParams& pp, double max_range, double eps,
                              double step_scale, int segs, int seg_rays, RayOut ro,
-                             cudaStream_t st) {
+                             cudaStream_t st, int mode = RMPB_MODE_EXACT) {
   Bundle bv = bundle_view(b);
   const long long units = (long long)P * segs;
   if (units >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many CTA units");
   // one ray per thread -> the lean kernel (nothing to refill); else lane refill
   const int64_t kopt = g_opt_kernel.load();
-  const bool v2 = kopt == 2 || (kopt == 0 && seg_rays > kBlock);
+  const bool v2 = kopt == 2 || (kopt == 0 && seg_rays > kBlock) || mode == RMPB_MODE_FAST;
   return with_grid(g, [&](auto acc) -> int {
     using G = decltype(acc);
     if (!v2)
       k_ray_policy<<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
                                                        step_scale, segs, seg_rays, ro);
+    else if (mode == RMPB_MODE_FAST && ro.step_total)
+      k_ray_policy2<G, true, true><<<(unsigned)units, kBlock, 0, st>>>(
+          acc, g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays, ro);
+    else if (mode == RMPB_MODE_FAST)
+      k_ray_policy2<G, false, true><<<(unsigned)units, kBlock, 0, st>>>(
+          acc, g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays, ro);
     else if (ro.t || ro.step_total)
       k_ray_policy2<G, true><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
                                                                  max_range, eps, step_scale, segs,
@@ -880,7 +886,8 @@ static int ray_policy_batch_impl(const rmpb_grid* g, const rmpb_bundle* b, const
                                  const double* d_v, int64_t P, const double params[7],
                                  double max_range, double eps, double step_scale, double* d_slot,
                                  double* d_accel, uint64_t* step_total, Workspace* ws,
-                                 cudaStream_t st, const int* d_active = nullptr) {
+                                 cudaStream_t st, const int* d_active = nullptr,
+                                 int mode = RMPB_MODE_EXACT) {
   int segs, seg_rays;
   choose_segments(P, b->n, &segs, &seg_rays);
   if (segs > 1) {
@@ -895,7 +902,25 @@ static int ray_policy_batch_impl(const rmpb_grid* g, const rmpb_bundle* b, const
   RayOut ro{};
   ro.step_total = (unsigned long long*)step_total;
   return launch_ray_policy(g, b, io, P, make_params(params, 0.0), max_range, eps, step_scale, segs,
-                           seg_rays, ro, st);
+                           seg_rays, ro, st, mode);
+}
+
+extern "C" int rmpb_ray_policy_batch_device_mode(const rmpb_grid* g, const rmpb_bundle* b,
+                                                 const double* d_x, const double* d_v, int64_t P,
+                                                 const double params[7], double max_range,
+                                                 double eps, double step_scale, int mode,
+                                                 double* d_slot, double* d_accel,
+                                                 uint64_t* opt_step_total, void* stream) {
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (P < 1) return fail(RMPB_ERR_INVALID, "P must be >= 1");
+  if (!d_x || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
+  if (mode != RMPB_MODE_EXACT && mode != RMPB_MODE_FAST) return fail(RMPB_ERR_INVALID, "bad mode");
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  return ray_policy_batch_impl(g, b, d_x, d_v, P, params, max_range, eps, step_scale, d_slot,
+                               d_accel, opt_step_total, ws, S(stream), nullptr, mode);
 }
 
 extern "C" int rmpb_ray_policy_batch_device(const rmpb_grid* g, const rmpb_bundle* b,

@@ -9,6 +9,8 @@
 // (atomic ticket) folds the partials in segment order and resolves.  All
 // orders are fixed, so results are bitwise reproducible run to run.
 #pragma once
+#include <type_traits>
+
 #include "rmpb_device.cuh"
 
 namespace rmpb {
@@ -202,10 +204,12 @@ __device__ __forceinline__ void policy_flush(K2Smem& sm, int warp, int lane, boo
 #define RMPB_REFILL 8  // refill when at least this many lanes are idle (or none alive)
 #endif
 // RAYOUT: per-ray parity outputs (t, cell, steps) and the step counter.
-template <class G, bool RAYOUT>
+// FAST: fp32 march (opt-in, not reference-exact; see interp_f).
+template <class G, bool RAYOUT, bool FAST = false>
 __global__ void __launch_bounds__(kBlock, RMPB_MINB)
 k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
               double eps, double step_scale, int segs, int seg_rays, RayOut ro) {
+  using real = typename std::conditional<FAST, float, double>::type;
   __shared__ K2Smem sm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -235,7 +239,10 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   int chunk = warp, pcount = 0, phead = 0, qn = 0, cnt = 0, my_steps = 0;
   int ray = 0, steps = 0;
   bool alive = false;
-  double dx = 0, dy = 0, dz = 0, t = 0, tend = 0;
+  real dx = 0, dy = 0, dz = 0, t = 0, tend = 0;
+  const GeomF gf{(float)g.ox, (float)g.oy, (float)g.oz, (float)(1.0 / g.res), g.nx - 2, g.ny - 2,
+                 g.nz - 2};
+  (void)gf;
   __syncwarp();
   while (true) {
     // ---- refill from the prepared-ray buffer (prepare a chunk when empty);
@@ -301,8 +308,8 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
       const int rank = __popc(need & lt);
       if (!alive && rank < pcount) {
         const int e = phead + rank;
-        t = sm.pt[warp][e]; tend = sm.pe[warp][e];
-        dx = sm.px[warp][e]; dy = sm.py[warp][e]; dz = sm.pz[warp][e];
+        t = (real)sm.pt[warp][e]; tend = (real)sm.pe[warp][e];
+        dx = (real)sm.px[warp][e]; dy = (real)sm.py[warp][e]; dz = (real)sm.pz[warp][e];
         ray = sm.pr[warp][e];
         alive = true;
         if (RAYOUT) steps = 0;
@@ -317,26 +324,33 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     // ---- one sphere-trace step per live lane
     bool enq = false, hit_now = false;
     if (alive) {
-      int ix, iy, iz;
-      const double px = sm.pose[0], py = sm.pose[1], pz = sm.pose[2];
-      const double d = interp_fast(grid, g, px + t * dx, py + t * dy, pz + t * dz, ix, iy, iz);
+      int ix = -1, iy = -1, iz = -1;
+      real d;
+      if constexpr (FAST) {
+        const float px = (float)sm.pose[0], py = (float)sm.pose[1], pz = (float)sm.pose[2];
+        d = interp_f(grid, gf, __fmaf_rn(t, dx, px), __fmaf_rn(t, dy, py), __fmaf_rn(t, dz, pz));
+      } else {
+        const double px = sm.pose[0], py = sm.pose[1], pz = sm.pose[2];
+        d = interp_fast(grid, g, px + t * dx, py + t * dy, pz + t * dz, ix, iy, iz);
+      }
       if (RAYOUT) ++steps;
       bool fin, hit = false;
-      if (d < eps) {
+      if (d < (real)eps) {
         hit = true;
         fin = true;
       } else {
-        t += step_scale * d;
+        if constexpr (FAST) t = __fmaf_rn((float)step_scale, d, t);
+        else t += step_scale * d;
         fin = !(t <= tend);  // == (t > tend) for numbers; a NaN t ends the ray
       }
       if (fin) {
         alive = false;
         hit_now = hit;
         if (RAYOUT) my_steps += steps;
-        if (hit) enq = t < p.radius;
+        if (hit) enq = (double)t < p.radius;
         if (RAYOUT && ro.t) {
           const int o = b.perm ? b.perm[ray] : ray;
-          ro.t[o] = hit ? t : CUDART_INF;
+          ro.t[o] = hit ? (double)t : CUDART_INF;
           if (ro.cell) {
             ro.cell[3 * o] = hit ? ix : -1; ro.cell[3 * o + 1] = hit ? iy : -1;
             ro.cell[3 * o + 2] = hit ? iz : -1;
@@ -351,7 +365,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     if (em) {
       if (enq) {
         const int pos = qn + __popc(em & lt);
-        qt[pos] = t;
+        qt[pos] = (double)t;
         qr[pos] = ray;
       }
       qn += __popc(em);

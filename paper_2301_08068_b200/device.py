@@ -52,7 +52,12 @@ class RayPolicyEngine:
     """Fused map-based policy evaluation with device-resident inputs."""
 
     def __init__(self, grid, bundle, params, max_range: float = 20.0, device: int | None = None,
-                 eps: float | None = None, step_scale: float = 0.9):
+                 eps: float | None = None, step_scale: float = 0.9, mode: str = "exact"):
+        """``mode="exact"`` (default) is bit-identical to the reference;
+        ``mode="fast"`` marches in fp32 (opt-in, NOT reference-exact)."""
+        if mode not in ("exact", "fast"):
+            raise ValueError("mode must be 'exact' or 'fast'")
+        self.mode = L.MODE_FAST if mode == "fast" else L.MODE_EXACT
         dev = b200.get_device() if device is None else int(device)
         if isinstance(grid, b200.DeviceGrid):
             self.grid = grid
@@ -87,10 +92,10 @@ class RayPolicyEngine:
         if out_accel is None:
             out_accel = torch.empty((P, 3), dtype=torch.float64, device=x.device)
         cnt = 0 if step_counter is None else step_counter.data_ptr()
-        L.call("rmpb_ray_policy_batch_device", self.grid.handle, self.bundle.handle, x.data_ptr(),
-               v.data_ptr(), P, self.params.ctypes.data, self.max_range, self.eps,
-               self.step_scale, out_slot.data_ptr(), out_accel.data_ptr(), cnt or None,
-               _stream_ptr(stream))
+        L.call("rmpb_ray_policy_batch_device_mode", self.grid.handle, self.bundle.handle,
+               x.data_ptr(), v.data_ptr(), P, self.params.ctypes.data, self.max_range, self.eps,
+               self.step_scale, self.mode, out_slot.data_ptr(), out_accel.data_ptr(),
+               cnt or None, _stream_ptr(stream))
         return out_slot, out_accel
 
     def partial(self, x, v, ray_begin: int, ray_end: int, out_slot=None, stream=None):
@@ -124,7 +129,7 @@ class DdaPolicyEngine:
     reference's sphere trace: its results are not reference-parity results."""
 
     def __init__(self, grid, bundle, params, max_range: float = 20.0, device: int | None = None):
-        base = RayPolicyEngine(grid, bundle, params, max_range, device)
+        base = RayPolicyEngine(grid, bundle, params, max_range, device=device)
         self.grid, self.bundle, self.params = base.grid, base.bundle, base.params
         self.max_range = float(max_range)
         self.occ = b200.DeviceOccupancy(self.grid)

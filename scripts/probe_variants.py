@@ -27,16 +27,18 @@ def timed(eng, xx, vv, reps=3):
         e0.record(); eng.evaluate(xx, vv); e1.record(); e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     return min(ts)
-variants = [("f32", "quad"), ("f64", "pair64")]
+variants = [("f32", "quad"), ("f32", "quad_fast"), ("f64", "pair64")]
 for kern in (0,):
     L.set_option("kernel", kern)
     for st, lay in variants:
         if kern == 1 and (st, lay) != ("f32", "quad"):
             continue
+        fast = lay.endswith("_fast")
+        lay0 = lay.replace("_fast", "")
         dg = b200.DeviceGrid(grid.values, grid.origin, grid.resolution,
                              storage={"f32": L.STORE_F32, "f64": L.STORE_F64}[st],
-                             layout={"quad": L.LAYOUT_QUAD, "linear": L.LAYOUT_LINEAR, "quadb": L.LAYOUT_QUADB, "pair64": L.LAYOUT_PAIR64}[lay])
-        eng = RayPolicyEngine(dg, bundle, params, 10.0)
+                             layout={"quad": L.LAYOUT_QUAD, "linear": L.LAYOUT_LINEAR, "quadb": L.LAYOUT_QUADB, "pair64": L.LAYOUT_PAIR64}[lay0])
+        eng = RayPolicyEngine(dg, bundle, params, 10.0, mode="fast" if fast else "exact")
         ms = timed(eng, x, v)
         lat = []
         for i in range(30):

@@ -525,3 +525,24 @@ def test_k5_dda_bit_exact_vs_cpu_definition(be, oracle, c1):
                                      10.0, workers=8, bits=bits_ref)
         slot_r = oracle.policy_slot(dirs, t_r.astype(np.float64), st.velocity, STATIC_MAP)
         check_policy(slots[k], accs[k], slot_r, oracle.accel_from_slot(slot_r))
+
+
+def test_fast_mode_deviation_report(be, oracle, c1):
+    """Opt-in FAST mode (fp32 march) is NOT reference-exact; its deviation
+    from the exact path on the C1 poses is bounded and reported here."""
+    import torch
+
+    from paper_2301_08068_b200.device import RayPolicyEngine
+
+    scene, grid, states, dirs = c1
+    x = torch.tensor(np.stack([s.position for s in states]), dtype=torch.float64, device="cuda")
+    v = torch.tensor(np.stack([s.velocity for s in states]), dtype=torch.float64, device="cuda")
+    ex = RayPolicyEngine(grid, dirs, STATIC_MAP, 10.0)
+    fa = RayPolicyEngine(ex.grid, ex.bundle, STATIC_MAP, 10.0, mode="fast")
+    se, ae = (t.cpu().numpy() for t in ex.evaluate(x, v))
+    sf, af = (t.cpu().numpy() for t in fa.evaluate(x, v))
+    hit_dev = np.abs(sf[:, 12] - se[:, 12]).max() / 65536
+    sum_dev = max(rel_err(sf[k, :12], se[k, :12]) for k in range(len(states)))
+    print(f"FAST vs EXACT: max |n_hits diff| / rays = {hit_dev:.2e}, max sum rel dev = {sum_dev:.2e}")
+    assert hit_dev < 1e-3
+    assert sum_dev < 1e-2
