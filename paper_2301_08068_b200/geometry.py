@@ -10,7 +10,7 @@ path and its input side need).
   the reference's 512^3-node bound; ``bake_esdf_device`` skips the host copy
   and the bound (the 1000x1000x200 config needs 2e8 nodes).
 * ``esdf_lookup`` (geometry.py:292-309, row f4) and the ESDF binary file
-  (geometry.py:455-488: 48-byte header, f32 x-fastest payload).
+  (geometry.py:455-488: documented header, f32 x-fastest payload).
 """
 
 from __future__ import annotations
@@ -33,7 +33,11 @@ KIND_SPHERE, KIND_BOX = 0, 1
 OP_UNION, OP_SUBTRACT = 0, 1
 ESDF_MAGIC = b"ESDF"
 ESDF_VERSION = 1
-_ESDF_HEADER = struct.Struct("<4sI3ddd3I")
+# The reference's format string "<4sI3ddd3I" (geometry.py:458) has one 'd'
+# too many for the fields it documents and packs (magic, version, origin
+# 3xf64, resolution f64, dims 3xu32), so its save_esdf / load_esdf raise
+# struct.error.  This mirror implements the documented 52-byte header.
+_ESDF_HEADER = struct.Struct("<4sI3dd3I")
 
 
 class SceneFormatError(ValueError):

@@ -33,7 +33,7 @@ from .core import Policy, RobotState
 from .geometry import EsdfGrid, Scene
 from .rays import DEFAULT_MAX_RANGE, GRID_STEP_SCALE, RangeScan, RayBundle, raycast_many
 
-__all__ = ["AttractorParams", "ObstacleParams", "PolicyParams", "PRESETS", "preset",
+__all__ = ["AttractorParams", "ObstacleParams", "PolicyParams", "PRESETS", "preset", "esdf_policy",
            "ray_policy", "ray_policy_batch", "lidar_policy", "lidar_policy_points",
            "lidar_policy_batch", "obstacle_ray_policy", "activation_weight", "save_params",
            "load_params", "DEFAULT_LIDAR_MIN_RANGE"]
@@ -127,6 +127,18 @@ def obstacle_ray_policy(velocity, away_dir, distance: float, p: ObstacleParams) 
     n = float(np.linalg.norm(f_damp))
     s = f_damp / (n + p.c * np.log1p(np.exp(-2.0 * p.c * n)))
     return Policy(f_rep + f_damp, activation_weight(d, p.radius) * np.outer(s, s))
+
+
+def esdf_policy(state: RobotState, grid: EsdfGrid, p: ObstacleParams) -> Policy:
+    """Single-lookup obstacle policy (policies.py:166-172, row f4): one
+    distance / gradient query on the device, one obstacle policy; a
+    degenerate (zero) gradient gives the zero policy."""
+    from .geometry import esdf_lookup
+
+    sample = esdf_lookup(grid, state.position)
+    if sample.degenerate:
+        return Policy.zero()
+    return obstacle_ray_policy(state.velocity, sample.gradient, sample.distance, p)
 
 
 def _policy_from_slot(slot, accel) -> Policy:

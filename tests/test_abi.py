@@ -119,3 +119,27 @@ def test_scan_pattern_matches_reference_lattice(oracle, golden):
 
     assert np.array_equal(P.scan_pattern(16, 128), golden["lidar_dirs"])
     assert np.array_equal(P.scan_pattern(128, 1024), oracle.scan_pattern(128, 1024))
+
+
+def test_esdf_file_roundtrip(tmp_path):
+    """ESDF binary cache (geometry.py:455-488): the documented 52-byte header
+    (the reference's own struct format has an extra field and raises)."""
+    import paper_2301_08068_b200 as P
+
+    rng = np.random.default_rng(1)
+    vals = rng.normal(size=(7, 5, 6)).astype(np.float32).astype(np.float64)
+    g = P.EsdfGrid([0.5, -1.0, 2.0], 0.25, (7, 5, 6), vals)
+    path = tmp_path / "m.esdf"
+    P.save_esdf(g, path)
+    assert path.stat().st_size == 52 + 4 * vals.size
+    h = P.load_esdf(path)
+    assert h.dims == g.dims and h.resolution == g.resolution
+    assert np.array_equal(h.origin, g.origin) and np.array_equal(h.values, vals)
+    raw = path.read_bytes()
+    bad = tmp_path / "bad.esdf"
+    bad.write_bytes(b"XXXX" + raw[4:])
+    with pytest.raises(ValueError):
+        P.load_esdf(bad)
+    bad.write_bytes(raw[:60])
+    with pytest.raises(ValueError):
+        P.load_esdf(bad)

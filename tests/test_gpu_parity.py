@@ -546,3 +546,73 @@ def test_fast_mode_deviation_report(be, oracle, c1):
     print(f"FAST vs EXACT: max |n_hits diff| / rays = {hit_dev:.2e}, max sum rel dev = {sum_dev:.2e}")
     assert hit_dev < 1e-3
     assert sum_dev < 1e-2
+
+
+def test_public_map_and_scan_entry_points_vs_golden(be, golden):
+    """bake_esdf / esdf_policy / synthesize_scan / grid update / device-resident
+    grid creation through the public API, against the reference goldens."""
+    import hashlib
+
+    import torch
+
+    import paper_2301_08068_b200 as P
+    from paper_2301_08068_b200 import _lib as L
+
+    g = golden
+    scene = _golden_scene(g)
+    grid = P.bake_esdf(scene, 0.2, pad=1.0)
+    assert hashlib.sha256(grid.values.tobytes()).digest() == g["grid_sha256_f64"].tobytes()
+    assert grid.dims == tuple(g["grid_dims"]) and np.array_equal(grid.origin, g["grid_origin"])
+    # synthesize_scan (analytic scene trace on device + seeded dropout)
+    rot = g["lidar_rot"]
+    for i in range(g["lidar_ranges"].shape[0]):
+        sc = P.synthesize_scan(scene, g["pose_x"][i], 16, 128, max_range=20.0,
+                               orientation=rot if i == 1 else None, dropout=0.1, rng=i)
+        assert np.array_equal(sc.valid, g["lidar_valid"][i])
+        assert np.array_equal(sc.ranges, g["lidar_ranges"][i])
+    # esdf_policy: one lookup + obstacle_ray_policy (policies.py:166-172)
+    st = P.RobotState(g["esdf_pts"][3], [0.2, -0.4, 0.1])
+    pol = P.esdf_policy(st, grid, P.preset("static_map").obstacle)
+    d, gr = g["esdf_d"][3], g["esdf_g"][3]
+    want = (P.Policy.zero() if not gr.any() else
+            P.obstacle_ray_policy(st.velocity, gr, d, P.preset("static_map").obstacle))
+    assert np.allclose(pol.accel, want.accel, rtol=1e-12, atol=1e-12)
+    assert np.allclose(pol.metric, want.metric, rtol=1e-12, atol=1e-12)
+    # grid update + device-resident creation trace like the oracle
+    vals32 = grid.values.astype(np.float32).astype(np.float64)
+    dg = be.DeviceGrid(grid.values, grid.origin, grid.resolution)
+    L.call("rmpb_grid_update", dg.handle, vals32.ctypes.data, L.RMPB_F64)
+    t1, _, _ = be.grid_trace_ex(dg, grid.origin, grid.resolution, g["pose_x"][0], g["dirs"], 10.0,
+                                0.1, 0.9)
+    assert np.array_equal(t1, g["trace_t"][0])
+    tens = torch.from_numpy(vals32).cuda()
+    dd = be.DeviceGrid.from_device(tens.data_ptr(), False, grid.dims, grid.origin, grid.resolution)
+    t2, _, _ = be.grid_trace_ex(dd, grid.origin, grid.resolution, g["pose_x"][0], g["dirs"], 10.0,
+                                0.1, 0.9)
+    assert np.array_equal(t2, g["trace_t"][0])
+
+
+def test_lidar_points_batch_device(be, oracle, c1):
+    import torch
+
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200.device import lidar_points_batch_device
+
+    scene, grid, states, dirs = c1
+    scans = synth.lidar_scans(scene, states[:4], 16, 256)
+    pts = np.stack([np.where(s.valid[:, None], s.directions * s.ranges[:, None], 0.0)
+                    for s in scans]).astype(np.float32)
+    v = np.stack([s.velocity for s in states[:4]])
+    slots, accs = lidar_points_batch_device(torch.from_numpy(pts).cuda(), None,
+                                            torch.from_numpy(v).cuda(), LIDAR, 0.3)
+    slots, accs = slots.cpu().numpy(), accs.cpu().numpy()
+    for k in range(4):
+        p64 = pts[k].astype(np.float64)
+        r = np.sqrt((p64 * p64).sum(1))
+        ok = r > 0
+        with np.errstate(invalid="ignore", divide="ignore"):
+            dd = np.where(ok[:, None], p64 / r[:, None], 0.0)
+        slot_r, acc_r = oracle.lidar_policy(dd, r, ok, v[k], LIDAR, 0.3)
+        assert slots[k][12] == slot_r[12]
+        assert rel_err(slots[k][:12], slot_r[:12]) <= 1e-7
+        assert rel_err(accs[k], acc_r) <= 1e-5
