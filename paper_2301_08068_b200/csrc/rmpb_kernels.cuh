@@ -200,6 +200,9 @@ __device__ __forceinline__ void policy_flush(K2Smem& sm, int warp, int lane, boo
 #ifndef RMPB_MINB
 #define RMPB_MINB 4
 #endif
+#ifndef RMPB_UNROLL
+#define RMPB_UNROLL 3  // steps per lane between bookkeeping rounds
+#endif
 #ifndef RMPB_REFILL
 #define RMPB_REFILL 8  // refill when at least this many lanes are idle (or none alive)
 #endif
@@ -321,8 +324,11 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
       if (need == FULL && pcount == 0 && chunk >= nchunks) break;
     }
     if (need == FULL) break;  // (only reachable once every ray is done)
-    // ---- one sphere-trace step per live lane
+    // ---- RMPB_UNROLL sphere-trace steps per live lane between bookkeeping
+    // rounds (a lane that finishes idles for the rest of the round)
     bool enq = false, hit_now = false;
+#pragma unroll
+    for (int u = 0; u < RMPB_UNROLL; ++u) {
     if (alive) {
       int ix = -1, iy = -1, iz = -1;
       real d;
@@ -358,6 +364,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
           if (ro.steps) ro.steps[o] = steps;
         }
       }
+    }
     }
     // ---- queue policy work; evaluate in full-warp batches of 32
     cnt += __popc(__ballot_sync(FULL, hit_now));  // warp-uniform; min_range = 0: every hit counts
