@@ -166,9 +166,6 @@ constexpr int kQueue = 64;
 constexpr int kPrep = 32;
 
 struct K2Smem {
-  double pose[4];  // the unit's robot position (read per step: saves registers)
-  double exit_lo[3], exit_hi[3];  // (lo - s), (hi - s) per axis, for inside poses
-  int inside;      // pose inside the node domain: slab entry is t = 0 exactly
   double acc[kWarps][9];
   double qt[kWarps][kQueue];
   int qr[kWarps][kQueue];
@@ -222,15 +219,11 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   if (io.active && !io.active[pose]) return;  // whole CTA: finished rollout
   double sx, sy, sz;
   io.pose(pose, sx, sy, sz);
-  if (tid == 0) {
-    sm.pose[0] = sx; sm.pose[1] = sy; sm.pose[2] = sz;
-    // Inside the domain every axis' entry quotient is <= 0, so the reference's
-    // t = max(t0, 0) is exactly 0 and only the exit side is needed:
-    // (hi - s)/d for d > 0, (lo - s)/d for d < 0 (_ckern.pyx:171-212).
-    sm.inside = sx >= g.ox && sx <= g.hx && sy >= g.oy && sy <= g.hy && sz >= g.oz && sz <= g.hz;
-    sm.exit_lo[0] = g.ox - sx; sm.exit_lo[1] = g.oy - sy; sm.exit_lo[2] = g.oz - sz;
-    sm.exit_hi[0] = g.hx - sx; sm.exit_hi[1] = g.hy - sy; sm.exit_hi[2] = g.hz - sz;
-  }
+  // Inside the domain every axis' entry quotient is <= 0, so the reference's
+  // t = max(t0, 0) is exactly 0 and only the exit side is needed:
+  // (hi - s)/d for d > 0, (lo - s)/d for d < 0 (_ckern.pyx:171-212).
+  const bool inside =
+      sx >= g.ox && sx <= g.hx && sy >= g.oy && sy <= g.hy && sz >= g.oz && sz <= g.hz;
   if (lane < 9) sm.acc[warp][lane] = 0.0;
   __syncthreads();
   const int begin = seg * seg_rays;
@@ -262,26 +255,26 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
         double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
         if (ok) {
           ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
-          if (sm.inside) {
+          if (inside) {
             const RecipDir q = b.recip(r);
             double thi = CUDART_INF;
             if (ex != 0.0) {
-              const double tb = exdiv(ex > 0.0 ? sm.exit_hi[0] : sm.exit_lo[0], ex, q.hx, q.lx);
+              const double tb = exdiv((ex > 0.0 ? g.hx : g.ox) - sx, ex, q.hx, q.lx);
               thi = tb < thi ? tb : thi;
             }
             if (ey != 0.0) {
-              const double tb = exdiv(ey > 0.0 ? sm.exit_hi[1] : sm.exit_lo[1], ey, q.hy, q.ly);
+              const double tb = exdiv((ey > 0.0 ? g.hy : g.oy) - sy, ey, q.hy, q.ly);
               thi = tb < thi ? tb : thi;
             }
             if (ez != 0.0) {
-              const double tb = exdiv(ez > 0.0 ? sm.exit_hi[2] : sm.exit_lo[2], ez, q.hz, q.lz);
+              const double tb = exdiv((ez > 0.0 ? g.hz : g.oz) - sz, ez, q.hz, q.lz);
               thi = tb < thi ? tb : thi;
             }
             t0 = 0.0;
             t1 = thi < max_range ? thi : max_range;
             ok = !(t0 > t1);
           } else {
-            ok = box_span_fast(g, sm.pose[0], sm.pose[1], sm.pose[2], ex, ey, ez, b.recip(r), t0,
+            ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, b.recip(r), t0,
                                t1);
             if (ok) {
               t0 = t0 > 0.0 ? t0 : 0.0;
@@ -325,46 +318,45 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     }
     if (need == FULL) break;  // (only reachable once every ray is done)
     // ---- RMPB_UNROLL sphere-trace steps per live lane between bookkeeping
-    // rounds (a lane that finishes idles for the rest of the round)
-    bool enq = false, hit_now = false;
+    // rounds (a lane that finishes idles for the rest of the round).  Steps
+    // carry only (t, alive, hit); the end-of-ray bookkeeping runs once per
+    // round for the lanes whose ray ended in it.
+    const bool was_alive = alive;
+    bool hit_now = false;
+    int hx = -1, hy = -1, hz = -1;
 #pragma unroll
     for (int u = 0; u < RMPB_UNROLL; ++u) {
-    if (alive) {
-      int ix = -1, iy = -1, iz = -1;
-      real d;
-      if constexpr (FAST) {
-        const float px = (float)sm.pose[0], py = (float)sm.pose[1], pz = (float)sm.pose[2];
-        d = interp_f(grid, gf, __fmaf_rn(t, dx, px), __fmaf_rn(t, dy, py), __fmaf_rn(t, dz, pz));
-      } else {
-        const double px = sm.pose[0], py = sm.pose[1], pz = sm.pose[2];
-        d = interp_fast(grid, g, px + t * dx, py + t * dy, pz + t * dz, ix, iy, iz);
-      }
-      if (RAYOUT) ++steps;
-      bool fin, hit = false;
-      if (d < (real)eps) {
-        hit = true;
-        fin = true;
-      } else {
-        if constexpr (FAST) t = __fmaf_rn((float)step_scale, d, t);
-        else t += step_scale * d;
-        fin = !(t <= tend);  // == (t > tend) for numbers; a NaN t ends the ray
-      }
-      if (fin) {
-        alive = false;
-        hit_now = hit;
-        if (RAYOUT) my_steps += steps;
-        if (hit) enq = (double)t < p.radius;
-        if (RAYOUT && ro.t) {
-          const int o = b.perm ? b.perm[ray] : ray;
-          ro.t[o] = hit ? (double)t : CUDART_INF;
-          if (ro.cell) {
-            ro.cell[3 * o] = hit ? ix : -1; ro.cell[3 * o + 1] = hit ? iy : -1;
-            ro.cell[3 * o + 2] = hit ? iz : -1;
-          }
-          if (ro.steps) ro.steps[o] = steps;
+      if (alive) {
+        int ix = -1, iy = -1, iz = -1;
+        real d;
+        if constexpr (FAST) {
+          const float px = (float)sx, py = (float)sy, pz = (float)sz;
+          d = interp_f(grid, gf, __fmaf_rn(t, dx, px), __fmaf_rn(t, dy, py), __fmaf_rn(t, dz, pz));
+        } else {
+          // pose in (uniform) registers: no shared-memory reload per step
+          d = interp_fast(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
         }
+        if (RAYOUT) { ++steps; hx = ix; hy = iy; hz = iz; }
+        hit_now = d < (real)eps;
+        real tn;
+        if constexpr (FAST) tn = __fmaf_rn((float)step_scale, d, t);
+        else tn = t + step_scale * d;
+        if (!hit_now) t = tn;
+        alive = !hit_now && t <= tend;  // !(t > tend); a NaN t ends the ray
       }
     }
+    const bool enq = hit_now && (double)t < p.radius;
+    if (RAYOUT && was_alive && !alive) {
+      my_steps += steps;
+      if (ro.t) {
+        const int o = b.perm ? b.perm[ray] : ray;
+        ro.t[o] = hit_now ? (double)t : CUDART_INF;
+        if (ro.cell) {
+          ro.cell[3 * o] = hit_now ? hx : -1; ro.cell[3 * o + 1] = hit_now ? hy : -1;
+          ro.cell[3 * o + 2] = hit_now ? hz : -1;
+        }
+        if (ro.steps) ro.steps[o] = steps;
+      }
     }
     // ---- queue policy work; evaluate in full-warp batches of 32
     cnt += __popc(__ballot_sync(FULL, hit_now));  // warp-uniform; min_range = 0: every hit counts
