@@ -66,8 +66,11 @@ class ClockSampler:
 
     def start(self):
         try:
+            import shutil
+
+            pre = ["stdbuf", "-oL"] if shutil.which("stdbuf") else []  # line-buffered pipe
             self.proc = subprocess.Popen(
-                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
+                pre + ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "50"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
@@ -78,6 +81,14 @@ class ClockSampler:
     def _read(self):
         for line in self.proc.stdout:
             self.lines.append(line.strip())
+
+    def wait_first(self, timeout=5.0):
+        """Block until nvidia-smi delivered its first sample (it takes ~0.5 s
+        to start; the timed region is shorter than that)."""
+        t0 = time.perf_counter()
+        while self.proc is not None and not self.lines and time.perf_counter() - t0 < timeout:
+            time.sleep(0.02)
+        self.n0 = len(self.lines)
 
     def stop(self):
         if self.proc is None:
@@ -90,7 +101,9 @@ class ClockSampler:
         self.t.join(timeout=2)
         sm, mx, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
+        n0 = getattr(self, "n0", 0)
+        lines = self.lines[n0:] if len(self.lines) > n0 else self.lines
+        for ln in lines:
             parts = [p.strip() for p in ln.split(",")]
             if len(parts) < 7:
                 continue
@@ -195,6 +208,7 @@ def run_b200(args):
     torch.cuda.synchronize()
     clocks = ClockSampler(local)
     clocks.start()
+    clocks.wait_first()
     n0 = _lib.launch_count()
     total_ms = 0.0
     for _ in range(args.steps):
@@ -210,7 +224,6 @@ def run_b200(args):
     launches = _lib.launch_count() - n0
     if world > 1:
         dist.barrier()
-    clk = clocks.stop()
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -233,6 +246,7 @@ def run_b200(args):
         t0 = time.perf_counter()
         acc_h, met_h, nh = ray_policy_batch((x_h, v_h), grid, bundle, params, MAX_RANGE)
         e2e_s += time.perf_counter() - t0
+    clk = clocks.stop()  # sampled over the device-timed and the e2e steps
     t = torch.tensor([e2e_s], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -249,6 +263,9 @@ def run_b200(args):
             lat.append(time.perf_counter() - t0)
     lat_med = statistics.median(lat)
 
+    # measured L2 read ceiling (untimed), CUDA events
+    l2 = l2_peaks(dev, stream)
+
     # live kernel duration = step time (one k_ray_policy launch per step)
     kern_ms = ms_per_step
     peaks, peak_src = measured_peaks()
@@ -263,6 +280,9 @@ def run_b200(args):
             "traffic": traffic, "peak_source": peak_src,
             "traffic_source": (ncu or {}).get("file"),
             "l2_read_GBps_ncu": (ncu or {}).get("l2_read_GBps"),
+            "l2_stream_peak_GBps": l2.get("stream"),
+            "frac_of_l2_stream_peak": (round(achieved / l2["stream"], 4)
+                                       if l2.get("stream") else None),
             "kernel": "k_ray_policy2<QuadGridF32>",
             "algorithmic_bytes_per_launch": algo_bytes,
             "voxel_steps_per_launch": vox_steps,
@@ -303,6 +323,34 @@ def run_b200(args):
     return out
 
 
+def l2_peaks(dev, stream, mib=32):
+    """Best-of-6 GB/s of rmpb_l2_probe mode 0 (streaming 16-B reads, L1
+    bypassed, 32 MiB L2-resident buffer)."""
+    import ctypes
+
+    import torch
+
+    from paper_2301_08068_b200 import _lib
+
+    buf = torch.ones(mib * 1024 * 1024, dtype=torch.uint8, device=dev)
+    out = {}
+    for mode, name, reps in ((0, "stream", 40),):
+        nbytes = ctypes.c_int64(0)
+        best = None
+        for _ in range(6):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            _lib.call("rmpb_l2_probe", buf.data_ptr(), buf.numel(), reps, mode,
+                      ctypes.byref(nbytes), stream.cuda_stream)
+            e1.record(stream)
+            e1.synchronize()
+            ms = e0.elapsed_time(e1)
+            best = ms if best is None else min(best, ms)
+        out[name] = round(nbytes.value / (best * 1e-3) / 1e9, 1)
+    return out
+
+
 # ----------------------------------------------------------------------------
 # CPU legs (reference kernels from oracle/_ref; C port fallback)
 
@@ -313,7 +361,7 @@ def _cpu_threads():
         return os.cpu_count() or 1
 
 
-def cpu_baseline(grid, states, seconds=10.0, threads=None):
+def cpu_baseline(grid, states, seconds=10.0, threads=None, seconds_1t=4.0):
     """Times the reference's CPU path (oracle/_ref compiled kernels driven as
     rmpnav's ckern.py/_pool.py do) on a bounded sample of this workload."""
     sys.path.insert(0, os.path.join(ROOT, "oracle"))
@@ -341,8 +389,27 @@ def cpu_baseline(grid, states, seconds=10.0, threads=None):
     finally:
         pool.close()
     rays_s = done * N_RAYS / el
+    # W = 1 (the reference harness at one worker and at all cores)
+    one, t1 = 0, time.perf_counter()
+    pool1 = O.RefPool(1)
+    try:
+        while True:
+            st = states[one % len(states)]
+            if kind == "reference":
+                O.ref_ray_policy(vals, grid.origin, grid.resolution, st.position, st.velocity,
+                                 dirs, PARAMS, MAX_RANGE, pool1)
+            else:
+                O.ray_policy(vals, grid.origin, grid.resolution, st.position, st.velocity, dirs,
+                             PARAMS, MAX_RANGE, workers=1)
+            one += 1
+            el1 = time.perf_counter() - t1
+            if el1 >= seconds_1t and one >= 2:
+                break
+    finally:
+        pool1.close()
     return {"value": round(rays_s, 1), "unit": "rays/s", "cores": threads, "kind": kind,
             "hz": round(done / el, 2),
+            "value_1_thread": round(one * N_RAYS / el1, 1), "hz_1_thread": round(one / el1, 2),
             "sample": f"{done} poses x {N_RAYS} rays of the same workload in {el:.1f} s "
                       f"({threads} threads, reference chunk pool, CHUNK=2048)"}
 

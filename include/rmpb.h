@@ -270,6 +270,14 @@ RMPB_EXPORT int rmpb_ray_policy_dda_batch_device(const rmpb_occupancy* o, const 
                                      const double params[7], double max_range, double* d_slot,
                                      double* d_accel, void* stream);
 
+/* ---- measurement helper (not part of the reference interface) ----------
+ * L2 bandwidth probe over a caller-owned device buffer (keep it well below
+ * the 126 MB L2): mode 0 streams 16-B reads, mode 1 issues independent
+ * pseudo-random 16-B reads (the trace kernel's gather shape).  Enqueued on
+ * `stream`; the caller times it.  *bytes_read = bytes the launch requests. */
+RMPB_EXPORT int rmpb_l2_probe(const void* d_buf, int64_t bytes, int reps, int mode,
+                              int64_t* bytes_read, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -84,6 +84,7 @@ _SIGS = {
     "rmpb_bake_grid_tsdf": (_i, [_vp, _d, _d, _d, _d, _i64, _i64, _i64, _d, _i, _i, _i, _vp]),
     "rmpb_grid_values": (_i, [_vp, _vp]),
     "rmpb_esdf_sample": (_i, [_vp, _vp, _i64, _vp, _vp, _vp, _vp]),
+    "rmpb_l2_probe": (_i, [_vp, _i64, _i, _i, _vp, _vp]),
     "rmpb_rollout_create": (_i, [_vp, _vp, _vp, _i64, _vp, _vp, _vp, _vp, _vp, _i64, _vp]),
     "rmpb_rollout_run": (_i, [_vp, _i64, _vp, _vp]),
     "rmpb_rollout_result": (_i, [_vp, _vp, _vp, _vp, _vp, _vp]),

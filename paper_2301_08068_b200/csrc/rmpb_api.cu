@@ -7,6 +7,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_scan.cuh>
 
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstdio>
@@ -33,6 +34,9 @@ static thread_local std::string g_err;
 static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int64_t> g_opt_seg_rays{0};
 static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread per pass, 2 lane refill
+static std::atomic<int64_t> g_opt_carveout{-1};
+static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (v3 warp units), 1, 2, 3
+static std::atomic<int64_t> g_opt_lidar_warps{76000};  // v3: target warp units per launch  // shared-memory carveout % for the trace kernel
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -283,6 +287,21 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
   if (!name) return fail(RMPB_ERR_INVALID, "name is NULL");
   if (!strcmp(name, "seg_rays")) {
     g_opt_seg_rays.store(value);
+    return RMPB_OK;
+  }
+  if (!strcmp(name, "lidar_warps")) {
+    if (value < 1) return fail(RMPB_ERR_INVALID, "lidar_warps must be >= 1");
+    g_opt_lidar_warps.store(value);
+    return RMPB_OK;
+  }
+  if (!strcmp(name, "lidar_kernel")) {
+    if (value < 0 || value > 3) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..3");
+    g_opt_lidar_kernel.store(value);
+    return RMPB_OK;
+  }
+  if (!strcmp(name, "carveout")) {
+    if (value < -1 || value > 100) return fail(RMPB_ERR_INVALID, "carveout must be -1..100");
+    g_opt_carveout.store(value);
     return RMPB_OK;
   }
   if (!strcmp(name, "kernel")) {
@@ -789,6 +808,25 @@ static Bundle bundle_view(const rmpb_bundle* b) {
 // ---------------------------------------------------------------------------
 // fused ray policy
 
+// Shared-memory carveout of a trace kernel (the rest of the 256 KB is L1,
+// which caches the map corners): applied once per (kernel, device, value).
+template <class K>
+static void apply_carveout(K* kern) {
+  const int64_t pct = g_opt_carveout.load();
+  if (pct < 0) return;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, int64_t> done;
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(mu);
+  auto key = std::make_pair((const void*)kern, dev);
+  auto it = done.find(key);
+  if (it != done.end() && it->second == pct) return;
+  cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, (int)pct);
+  cudaGetLastError();
+  done[key] = pct;
+}
+
 static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io, int64_t P,
                              const PolicyParams& pp, double max_range, double eps,
                              double step_scale, int segs, int seg_rays, RayOut ro,
@@ -801,6 +839,12 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
   const bool v2 = kopt == 2 || (kopt == 0 && seg_rays > kBlock) || mode == RMPB_MODE_FAST;
   return with_grid(g, [&](auto acc) -> int {
     using G = decltype(acc);
+    if (v2) {
+      apply_carveout(k_ray_policy2<G, true, true>);
+      apply_carveout(k_ray_policy2<G, false, true>);
+      apply_carveout(k_ray_policy2<G, true>);
+      apply_carveout(k_ray_policy2<G, false>);
+    }
     if (!v2)
       k_ray_policy<<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
                                                        step_scale, segs, seg_rays, ro);
@@ -1031,6 +1075,44 @@ extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double
 static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
                         const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                         cudaStream_t st) {
+  const int64_t kopt = g_opt_lidar_kernel.load();
+  if (kopt == 0 || kopt == 3) {
+    // warp units: ~16 waves of 32 warps per SM (measured best on C3), <= 1024
+    // warps per scan,
+    // segments a multiple of 128 beams (the 4-beam-per-lane vector groups)
+    const int64_t n = sc.n;
+    const int64_t target = g_opt_lidar_warps.load();
+    int64_t wps = (target + S_ - 1) / S_;
+    wps = std::min<int64_t>(wps, 1024);
+    wps = std::min<int64_t>(wps, (n + 255) / 256);
+    wps = std::max<int64_t>(wps, 1);
+    const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
+    wps = (n + seg - 1) / seg;
+    const long long nunits = (long long)S_ * wps;
+    if (wps > 1) {
+      TRY(ws->partials.ensure((size_t)nunits * kAcc * sizeof(double)));
+      TRY(ws->ensure_tickets((size_t)S_));
+    }
+    PoseIO io{};
+    io.x = nullptr; io.v = d_v;
+    if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
+    io.slot = d_slot; io.accel = d_accel;
+    io.partials = (double*)ws->partials.p;
+    io.tickets = (unsigned*)ws->tickets.p;
+    const long long blocks = (nunits + kWarps - 1) / kWarps;
+    if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
+    const size_t smem = sizeof(LidarWarpSmem) * kWarps;
+    static std::once_flag once[64];
+    int dev = 0;
+    CK(cudaGetDevice(&dev));
+    std::call_once(once[dev & 63], [&] {
+      cudaFuncSetAttribute(k_lidar_policy3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    });
+    k_lidar_policy3<<<(unsigned)blocks, kBlock, smem, st>>>(sc, io, pp, (int)wps, (int)seg,
+                                                             nunits);
+    CKL();
+    return RMPB_OK;
+  }
   int segs, seg_rays;
   choose_segments(S_, sc.n, &segs, &seg_rays);
   if (segs > 1) {
@@ -1044,7 +1126,7 @@ static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
   io.partials = (double*)ws->partials.p;
   io.tickets = (unsigned*)ws->tickets.p;
   const long long units = (long long)S_ * segs;
-  if (g_opt_kernel.load() == 1)
+  if (kopt == 1)
     k_lidar_policy<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
   else
     k_lidar_policy2<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
@@ -1737,5 +1819,31 @@ extern "C" int rmpb_ray_policy_dda_batch_device(const rmpb_occupancy* oc, const 
   k_ray_policy_dda<<<(unsigned)(P * segs), kBlock, 0, S(stream)>>>(
       oc->o, bundle_view(b), io, make_params(params, 0.0), (float)max_range, segs, seg_rays);
   CKL();
+  return RMPB_OK;
+}
+
+// ---------------------------------------------------------------------------
+// measurement helper: L2 bandwidth probe over a caller-owned device buffer
+
+extern "C" int rmpb_l2_probe(const void* d_buf, int64_t bytes, int reps, int mode,
+                             int64_t* bytes_read, void* stream) {
+  if (!d_buf || bytes < 4096 || reps < 1 || (mode != 0 && mode != 1))
+    return fail(RMPB_ERR_INVALID, "l2_probe: need a device buffer >= 4096 B, reps >= 1, mode 0/1");
+  int dev = 0, sms = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  static thread_local unsigned* sink = nullptr;
+  if (!sink) CK(cudaMalloc(&sink, sizeof(unsigned)));
+  const unsigned long long n16 = (unsigned long long)bytes / 16;
+  const int blocks = sms * 8, threads = 256;
+  rmpb::k_l2_probe<<<blocks, threads, 0, (cudaStream_t)stream>>>((const uint4*)d_buf, n16, reps,
+                                                                 mode, sink);
+  CKL();
+  if (bytes_read) {
+    const unsigned long long nth = (unsigned long long)blocks * threads;
+    const unsigned long long per = (n16 + nth - 1) / nth;
+    *bytes_read = mode == 0 ? (int64_t)(n16 * 16ULL * reps)
+                            : (int64_t)(((per + 3) / 4) * 4 * nth * 16ULL * reps);
+  }
   return RMPB_OK;
 }

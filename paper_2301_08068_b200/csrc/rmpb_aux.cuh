@@ -420,4 +420,37 @@ __global__ void k_esdf_sample(G grid, GridGeom g, const double* __restrict__ pts
   }
 }
 
+// ---------------------------------------------------------------------------
+// L2 bandwidth probes (measurement only: the roofline denominators bench.py
+// reports beside the HBM peak; SURVEY.md §8d "a measured L2 peak").
+// mode 0: streaming 16-B reads (L1 bypassed) over an L2-resident buffer;
+// mode 1: independent pseudo-random 16-B reads -- the access shape of the
+// trace kernel's corner gathers (one 32-B sector per load).
+__global__ void k_l2_probe(const uint4* __restrict__ buf, unsigned long long n16, int reps,
+                           int mode, unsigned* __restrict__ sink) {
+  const unsigned long long tid = blockIdx.x * (unsigned long long)blockDim.x + threadIdx.x;
+  const unsigned long long nth = (unsigned long long)gridDim.x * blockDim.x;
+  unsigned acc = 0u;
+  if (mode == 0) {
+    for (int r = 0; r < reps; ++r)
+      for (unsigned long long i = tid; i < n16; i += nth) {
+        const uint4 v = __ldcg(buf + i);
+        acc ^= v.x ^ v.y ^ v.z ^ v.w;
+      }
+  } else {
+    unsigned h = (unsigned)tid * 2654435761u + 12345u;
+    const unsigned long long per = (n16 + nth - 1) / nth;
+    for (int r = 0; r < reps; ++r)
+      for (unsigned long long k = 0; k < per; k += 4) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          h = h * 1664525u + 1013904223u;
+          const uint4 v = __ldcg(buf + (h % (unsigned)n16));
+          acc ^= v.x ^ v.w;
+        }
+      }
+  }
+  if (acc == 0x9e3779b9u) sink[0] = acc;  // keeps the loads; practically never taken
+}
+
 }  // namespace rmpb

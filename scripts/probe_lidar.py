@@ -1,0 +1,53 @@
+"""LiDAR kernel variants on C3 (1024 scans x 128x1024 beams, GPU box):
+best-of-5 ms per launch and max relative slot difference vs variant 2."""
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+from paper_2301_08068_b200 import _lib, synth  # noqa: E402
+from paper_2301_08068_b200.device import lidar_policy_batch_device  # noqa: E402
+from paper_2301_08068_b200.rays import scan_pattern  # noqa: E402
+
+scene = synth.c1_scene()
+states = synth.bench_states(scene, count=10, seed=123, distance=synth.host_box_distance(scene))
+scans = synth.lidar_scans(scene, states, 128, 1024, 20.0)
+S = 1024
+dirs = torch.from_numpy(np.ascontiguousarray(scan_pattern(128, 1024)).copy()).cuda()
+rg = torch.from_numpy(np.stack([scans[i % 10].ranges for i in range(S)])).cuda()
+vl = torch.from_numpy(np.stack([scans[i % 10].valid for i in range(S)]).astype(np.uint8)).cuda()
+R = torch.from_numpy(np.stack([scans[i % 10].orientation for i in range(S)]).reshape(S, 9).copy()).cuda()
+v = torch.from_numpy(np.stack([states[i % 10].velocity for i in range(S)])).cuda()
+LIDAR = (1.2, 1.5, 3.0, 1.0, 1e-6, 1.3, 1.0)
+out, ref = {}, None
+# args: "2" (kernel 2) or "3:19000" (kernel 3, target warp units)
+for arg in sys.argv[1:] or ["2", "3"]:
+    k, _, wt = arg.partition(":")
+    k = int(k)
+    _lib.call("rmpb_set_option", b"lidar_kernel", k)
+    if wt:
+        _lib.call("rmpb_set_option", b"lidar_warps", int(wt))
+    k = arg
+    s, a = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
+    torch.cuda.synchronize()
+    if ref is None:
+        ref = s.clone()
+    rel = float(((s - ref).abs().max() / ref.abs().max()).item())
+    s2, _ = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
+    ts = []
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    out[f"k{k}_ms"] = min(ts)
+    out[f"k{k}_rel_vs_first"] = rel
+    out[f"k{k}_repeat_bitexact"] = bool(torch.equal(s, s2))
+    out[f"k{k}_nhits_equal"] = bool(torch.equal(s[:, 12], ref[:, 12]))
+print(json.dumps(out))
