@@ -616,3 +616,55 @@ def test_lidar_points_batch_device(be, oracle, c1):
         assert slots[k][12] == slot_r[12]
         assert rel_err(slots[k][:12], slot_r[:12]) <= 1e-7
         assert rel_err(accs[k], acc_r) <= 1e-5
+
+
+@pytest.mark.parametrize("n,S", [(131072, 1), (1000, 5), (131, 3), (97, 2), (4096, 40)])
+def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
+    """All LiDAR kernel variants (1: per-thread, 2: CTA streaming, 3: warp
+    units) vs the oracle on ragged beam counts, odd rows (16-B misaligned
+    range rows / 4-B misaligned validity rows -> scalar path), with and
+    without rotation / validity; variant 3 with the default warp targets
+    also exercises the multi-warp fold (S = 1: 512 warp partials)."""
+    import torch
+
+    from paper_2301_08068_b200 import _lib
+    from paper_2301_08068_b200.device import lidar_policy_batch_device
+
+    rng = np.random.default_rng(n * 7 + S)
+    dirs = rng.standard_normal((n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    ranges = rng.uniform(0.0, 4.0, (S, n))
+    ranges[:, ::17] = np.inf
+    ranges[:, 3::29] = np.nan
+    valid = rng.random((S, n)) < 0.8
+    v = rng.standard_normal((S, 3))
+    Rs = []
+    for _ in range(S):
+        q, _r = np.linalg.qr(rng.standard_normal((3, 3)))
+        Rs.append(q)
+    Rs = np.stack(Rs)
+    d_dirs = torch.from_numpy(dirs).cuda()
+    d_rg = torch.from_numpy(ranges).cuda()
+    d_v = torch.from_numpy(v).cuda()
+    try:
+        for use_R in (True, False):
+            for use_valid in (True, False):
+                d_R = torch.from_numpy(Rs.reshape(S, 9).copy()).cuda() if use_R else None
+                d_vl = torch.from_numpy(valid.astype(np.uint8)).cuda() if use_valid else None
+                outs = {}
+                for k in (1, 2, 3):
+                    _lib.call("rmpb_set_option", b"lidar_kernel", k)
+                    sl, ac = lidar_policy_batch_device(d_dirs, d_R, d_rg, d_vl, d_v, LIDAR, 0.3)
+                    outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
+                for s in range(S):
+                    wd = dirs @ Rs[s].T if use_R else dirs
+                    vv = valid[s] if use_valid else np.ones(n, bool)
+                    slot_r, acc_r = oracle.lidar_policy(wd, ranges[s], vv, v[s], LIDAR, 0.3)
+                    for k in (1, 2, 3):
+                        sl, ac = outs[k]
+                        assert sl[s][12] == slot_r[12], (k, s)
+                        assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
+                        if slot_r[12] > 0 and np.abs(slot_r[:9]).max() > 0:
+                            assert rel_err(ac[s], acc_r) <= ACC_TOL, (k, s)
+    finally:
+        _lib.call("rmpb_set_option", b"lidar_kernel", 0)
