@@ -1072,46 +1072,55 @@ extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double
 // ---------------------------------------------------------------------------
 // LiDAR
 
+// K2 v3 / K2b: warp-unit LiDAR kernel.  ~16 waves of 32 warps per SM
+// (measured best on C3), <= 1024 warps per scan, segments a multiple of 128
+// beams (the 4-beam-per-lane vector groups).
+template <class Src>
+static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
+                             const PolicyParams& pp, double* d_slot, double* d_accel,
+                             Workspace* ws, cudaStream_t st) {
+  const int64_t target = g_opt_lidar_warps.load();
+  int64_t wps = (target + S_ - 1) / S_;
+  wps = std::min<int64_t>(wps, 1024);
+  wps = std::min<int64_t>(wps, (n + 255) / 256);
+  wps = std::max<int64_t>(wps, 1);
+  const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
+  wps = (n + seg - 1) / seg;
+  const long long nunits = (long long)S_ * wps;
+  if (wps > 1) {
+    TRY(ws->partials.ensure((size_t)nunits * kAcc * sizeof(double)));
+    TRY(ws->ensure_tickets((size_t)S_));
+  }
+  PoseIO io{};
+  io.x = nullptr; io.v = d_v;
+  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
+  io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  const long long blocks = (nunits + kWarps - 1) / kWarps;
+  if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
+  const size_t smem = sizeof(LidarWarpSmem) * kWarps;
+  static std::once_flag once[64];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [&] {
+    cudaFuncSetAttribute(k_lidar_warp<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  });
+  k_lidar_warp<Src><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps, (int)seg,
+                                                             nunits);
+  CKL();
+  return RMPB_OK;
+}
+
 static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
                         const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                         cudaStream_t st) {
   const int64_t kopt = g_opt_lidar_kernel.load();
   if (kopt == 0 || kopt == 3) {
-    // warp units: ~16 waves of 32 warps per SM (measured best on C3), <= 1024
-    // warps per scan,
-    // segments a multiple of 128 beams (the 4-beam-per-lane vector groups)
-    const int64_t n = sc.n;
-    const int64_t target = g_opt_lidar_warps.load();
-    int64_t wps = (target + S_ - 1) / S_;
-    wps = std::min<int64_t>(wps, 1024);
-    wps = std::min<int64_t>(wps, (n + 255) / 256);
-    wps = std::max<int64_t>(wps, 1);
-    const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
-    wps = (n + seg - 1) / seg;
-    const long long nunits = (long long)S_ * wps;
-    if (wps > 1) {
-      TRY(ws->partials.ensure((size_t)nunits * kAcc * sizeof(double)));
-      TRY(ws->ensure_tickets((size_t)S_));
-    }
-    PoseIO io{};
-    io.x = nullptr; io.v = d_v;
-    if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
-    io.slot = d_slot; io.accel = d_accel;
-    io.partials = (double*)ws->partials.p;
-    io.tickets = (unsigned*)ws->tickets.p;
-    const long long blocks = (nunits + kWarps - 1) / kWarps;
-    if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
-    const size_t smem = sizeof(LidarWarpSmem) * kWarps;
-    static std::once_flag once[64];
-    int dev = 0;
-    CK(cudaGetDevice(&dev));
-    std::call_once(once[dev & 63], [&] {
-      cudaFuncSetAttribute(k_lidar_policy3, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    });
-    k_lidar_policy3<<<(unsigned)blocks, kBlock, smem, st>>>(sc, io, pp, (int)wps, (int)seg,
-                                                             nunits);
-    CKL();
-    return RMPB_OK;
+    LatticeSrc src{};
+    src.sc = sc;
+    return launch_lidar_warp(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
   }
   int segs, seg_rays;
   choose_segments(S_, sc.n, &segs, &seg_rays);
@@ -1222,6 +1231,12 @@ extern "C" int rmpb_lidar_policy_batch_device(const double* d_dirs, const double
 static int points_launch(PointsIO pt, int64_t S_, const double* d_v, double v0[3],
                          const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                          cudaStream_t st) {
+  const int64_t kopt = g_opt_lidar_kernel.load();
+  if (kopt == 0 || kopt == 3) {
+    PointSrc src{};
+    src.pt = pt;
+    return launch_lidar_warp(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+  }
   int segs, seg_rays;
   choose_segments(S_, pt.n, &segs, &seg_rays);
   if (segs > 1) {

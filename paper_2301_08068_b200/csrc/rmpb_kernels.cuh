@@ -569,7 +569,7 @@ k_lidar_policy2(ScanIO sc, PoseIO io, PolicyParams p, int segs, int seg_rays) {
   finish_unit(acc, io, scan, seg, segs);
 }
 
-// K2 v3: warp units.  A warp owns `seg` consecutive beams of one scan (no
+// K2 v3 (and K2b): warp units.  A warp owns `seg` consecutive beams of one scan (no
 // CTA-wide barrier anywhere: warps never wait for each other).  Streaming:
 // each lane loads 4 consecutive beams per group (2 x 16-B range loads + one
 // 4-B validity word).  Beams inside the activation
@@ -591,34 +591,34 @@ struct LidarWarpSmem {
   double q2d[kRing2], q2x[kRing2], q2y[kRing2], q2z[kRing2];
 };
 
-__global__ void __launch_bounds__(kBlock, 4)
-k_lidar_policy3(ScanIO sc, PoseIO io, PolicyParams p, int wps, int seg, long long nunits) {
-  extern __shared__ __align__(16) unsigned char lidar_dsm[];  // kWarps x LidarWarpSmem
-  LidarWarpSmem* smw = reinterpret_cast<LidarWarpSmem*>(lidar_dsm);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const long long unit = (long long)blockIdx.x * kWarps + warp;
-  if (unit >= nunits) return;
-  const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
-  LidarWarpSmem& w = smw[warp];
-  const bool rot = sc.R != nullptr;
-  if (rot && lane < 9) w.R[lane] = sc.R[9 * scan + lane];
-  if (lane == 0) io.vel(scan, w.v[0], w.v[1], w.v[2]);
-#pragma unroll
-  for (int k = 0; k < 9; ++k) w.acc[k][lane] = 0.0;
-  const double* rg = sc.ranges + (size_t)scan * sc.n;
-  const unsigned char* vl = sc.valid ? sc.valid + (size_t)scan * sc.n : nullptr;
-  const bool vec = ((reinterpret_cast<uintptr_t>(rg) & 15) == 0) &&
-                   (!vl || (reinterpret_cast<uintptr_t>(vl) & 3) == 0);
-  const int begin = wu * seg;
-  const int end = min(begin + seg, sc.n);
-  int h1 = 0, q1n = 0, h2 = 0, q2n = 0, cnt = 0;
-  int base = begin;
-  __syncwarp();
-  // 4 consecutive beams per lane: 2 x 16-B range loads + one 4-B validity
-  // word (scalar fallback for misaligned scans and the ragged tail)
-  auto load4 = [&](int b0, double (&o)[4]) {
-    const int i0 = b0 + 4 * lane;
+// K2b: raw sensor-frame points (no map, no lattice): the
+// beam direction is p/|p| and its range |p|; zero / non-finite points are
+// invalid.  Float32 xyz as delivered by the sensor driver.
+struct PointsIO {
+  const float* __restrict__ xyz;  // [S][N][3]
+  const double* __restrict__ R;   // [S][9] or null
+  int n;
+};
+
+
+// Beam sources of the warp-unit kernel: a lattice scan (sensor directions +
+// ranges + validity, policies.py:195-205) or raw sensor-frame points (K2b).
+struct LatticeSrc {
+  ScanIO sc;
+  const double* rg;
+  const unsigned char* vl;
+  bool vec;
+  __device__ __forceinline__ const double* rot() const { return sc.R; }
+  __device__ __forceinline__ int count() const { return sc.n; }
+  __device__ __forceinline__ void bind(int scan) {
+    rg = sc.ranges + (size_t)scan * sc.n;
+    vl = sc.valid ? sc.valid + (size_t)scan * sc.n : nullptr;
+    vec = ((reinterpret_cast<uintptr_t>(rg) & 15) == 0) &&
+          (!vl || (reinterpret_cast<uintptr_t>(vl) & 3) == 0);
+  }
+  // beams i0..i0+3: 2 x 16-B range loads + one 4-B validity word (scalar
+  // fallback for misaligned rows and the ragged tail); invalid -> +inf
+  __device__ __forceinline__ void load4(int i0, int end, double (&o)[4]) const {
     if (vec && i0 + 3 < end) {
       const double2 x0 = __ldcs(reinterpret_cast<const double2*>(rg + i0));
       const double2 x1 = __ldcs(reinterpret_cast<const double2*>(rg + i0 + 2));
@@ -636,7 +636,70 @@ k_lidar_policy3(ScanIO sc, PoseIO io, PolicyParams p, int wps, int seg, long lon
         o[j] = (i < end && (!vl || vl[i])) ? rg[i] : CUDART_INF;
       }
     }
-  };
+  }
+  __device__ __forceinline__ void dir(int i, double, double& ex, double& ey, double& ez) const {
+    ex = sc.dirs[3 * i]; ey = sc.dirs[3 * i + 1]; ez = sc.dirs[3 * i + 2];
+  }
+};
+
+struct PointSrc {
+  PointsIO pt;
+  const float* P;
+  bool vec;
+  __device__ __forceinline__ const double* rot() const { return pt.R; }
+  __device__ __forceinline__ int count() const { return pt.n; }
+  __device__ __forceinline__ void bind(int scan) {
+    P = pt.xyz + (size_t)scan * pt.n * 3;
+    vec = (reinterpret_cast<uintptr_t>(P) & 15) == 0;
+  }
+  static __device__ __forceinline__ double range(float x, float y, float z) {
+    const double px = x, py = y, pz = z;
+    const double d = sqrt(px * px + py * py + pz * pz);
+    return d > 0.0 ? d : CUDART_INF;  // zero ("no return") or NaN point: invalid beam
+  }
+  // points i0..i0+3 (48 B = 3 x 16-B loads when aligned); range = |p|
+  __device__ __forceinline__ void load4(int i0, int end, double (&o)[4]) const {
+    if (vec && i0 + 3 < end) {
+      const float4* q = reinterpret_cast<const float4*>(P + 3 * (size_t)i0);
+      const float4 a = __ldcs(q), b = __ldcs(q + 1), c = __ldcs(q + 2);
+      o[0] = range(a.x, a.y, a.z); o[1] = range(a.w, b.x, b.y);
+      o[2] = range(b.z, b.w, c.x); o[3] = range(c.y, c.z, c.w);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int i = i0 + j;
+        o[j] = i < end ? range(P[3 * i], P[3 * i + 1], P[3 * i + 2]) : CUDART_INF;
+      }
+    }
+  }
+  __device__ __forceinline__ void dir(int i, double d, double& ex, double& ey, double& ez) const {
+    ex = (double)P[3 * i] / d; ey = (double)P[3 * i + 1] / d; ez = (double)P[3 * i + 2] / d;
+  }
+};
+
+template <class Src>
+__global__ void __launch_bounds__(kBlock, 4)
+k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits) {
+  extern __shared__ __align__(16) unsigned char lidar_dsm[];  // kWarps x LidarWarpSmem
+  LidarWarpSmem* smw = reinterpret_cast<LidarWarpSmem*>(lidar_dsm);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+  const long long unit = (long long)blockIdx.x * kWarps + warp;
+  if (unit >= nunits) return;
+  const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
+  LidarWarpSmem& w = smw[warp];
+  const double* Rall = src.rot();
+  const bool rot = Rall != nullptr;
+  if (rot && lane < 9) w.R[lane] = Rall[9 * scan + lane];
+  if (lane == 0) io.vel(scan, w.v[0], w.v[1], w.v[2]);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) w.acc[k][lane] = 0.0;
+  src.bind(scan);
+  const int begin = wu * seg;
+  const int end = min(begin + seg, src.count());
+  int h1 = 0, q1n = 0, h2 = 0, q2n = 0, cnt = 0;
+  int base = begin;
+  __syncwarp();
   while (true) {
     const bool draining = base >= end;
     if (!draining) {
@@ -644,7 +707,7 @@ k_lidar_policy3(ScanIO sc, PoseIO io, PolicyParams p, int wps, int seg, long lon
       // ring 1 (no flush here).  (Prefetching the next group into registers
       // measured slower: 0.58 vs 0.50 ms on C3 -- more spills.)
       double cur[4];
-      load4(base, cur);
+      src.load4(base + 4 * lane, end, cur);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         const double d = cur[j];
@@ -673,7 +736,8 @@ k_lidar_policy3(ScanIO sc, PoseIO io, PolicyParams p, int wps, int seg, long lon
         if (e >= kRing1) e -= kRing1;
         const int i = w.q1i[e];
         d = w.q1d[e];
-        const double ex = sc.dirs[3 * i], ey = sc.dirs[3 * i + 1], ez = sc.dirs[3 * i + 2];
+        double ex, ey, ez;
+        src.dir(i, d, ex, ey, ez);
         wx = ex; wy = ey; wz = ez;
         if (rot) {  // directions @ orientation.T  (rays.py:172-173)
           wx = ex * w.R[0] + ey * w.R[1] + ez * w.R[2];
@@ -758,15 +822,8 @@ k_lidar_policy3(ScanIO sc, PoseIO io, PolicyParams p, int wps, int seg, long lon
   }
 }
 
-// K2b: LiDAR-direct from raw sensor-frame points (no map, no lattice): the
-// beam direction is p/|p| and its range |p|; zero / non-finite points are
-// invalid.  Float32 xyz as delivered by the sensor driver.
-struct PointsIO {
-  const float* __restrict__ xyz;  // [S][N][3]
-  const double* __restrict__ R;   // [S][9] or null
-  int n;
-};
-
+// K2b v1: one point per thread per pass (kept as a measured alternative,
+// option lidar_kernel = 1 or 2).
 __global__ void __launch_bounds__(kBlock)
 k_lidar_points(PointsIO pt, PoseIO io, PolicyParams p, int segs, int seg_rays) {
   const int unit = blockIdx.x;

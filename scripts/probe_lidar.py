@@ -50,4 +50,23 @@ for arg in sys.argv[1:] or ["2", "3"]:
     out[f"k{k}_rel_vs_first"] = rel
     out[f"k{k}_repeat_bitexact"] = bool(torch.equal(s, s2))
     out[f"k{k}_nhits_equal"] = bool(torch.equal(s[:, 12], ref[:, 12]))
+# raw points (K2b): the same scans as f32 xyz (invalid -> 0)
+from paper_2301_08068_b200.device import lidar_points_batch_device  # noqa: E402
+
+pts = torch.where(vl.bool()[:, :, None], dirs[None] * rg[:, :, None], 0.0).float().contiguous()
+pts = torch.nan_to_num(pts, nan=0.0, posinf=0.0, neginf=0.0)
+for k in (1, 3):
+    _lib.call("rmpb_set_option", b"lidar_kernel", k)
+    lidar_points_batch_device(pts, R, v, LIDAR, 0.3)
+    ts = []
+    for _ in range(5):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        lidar_points_batch_device(pts, R, v, LIDAR, 0.3)
+        e1.record()
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    out[f"points_k{k}_ms"] = min(ts)
+_lib.call("rmpb_set_option", b"lidar_kernel", 0)
 print(json.dumps(out))

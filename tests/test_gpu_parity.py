@@ -668,3 +668,44 @@ def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
                             assert rel_err(ac[s], acc_r) <= ACC_TOL, (k, s)
     finally:
         _lib.call("rmpb_set_option", b"lidar_kernel", 0)
+
+
+@pytest.mark.parametrize("n,S", [(131072, 1), (1001, 4), (131, 3)])
+def test_lidar_points_kernels_ragged(be, oracle, n, S):
+    """Raw-point kernels (1: per-thread, 3: warp units) vs the oracle on
+    ragged / misaligned rows (12-B points: odd n -> scalar path), zero and
+    non-finite points, with and without rotation."""
+    import torch
+
+    from paper_2301_08068_b200 import _lib
+    from paper_2301_08068_b200.device import lidar_points_batch_device
+
+    rng = np.random.default_rng(n + 11 * S)
+    pts = rng.uniform(-3.0, 3.0, (S, n, 3)).astype(np.float32)
+    pts[:, ::13] = 0.0
+    pts[:, 5::31, 1] = np.nan
+    v = rng.standard_normal((S, 3))
+    Rs = np.stack([np.linalg.qr(rng.standard_normal((3, 3)))[0] for _ in range(S)])
+    try:
+        for use_R in (True, False):
+            d_R = torch.from_numpy(Rs.reshape(S, 9).copy()).cuda() if use_R else None
+            outs = {}
+            for k in (1, 3):
+                _lib.call("rmpb_set_option", b"lidar_kernel", k)
+                sl, ac = lidar_points_batch_device(torch.from_numpy(pts).cuda(), d_R,
+                                                   torch.from_numpy(v).cuda(), LIDAR, 0.3)
+                outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
+            for s in range(S):
+                p64 = pts[s].astype(np.float64)
+                r = np.sqrt((p64 * p64).sum(1))
+                ok = r > 0
+                with np.errstate(invalid="ignore", divide="ignore"):
+                    dd = np.where(ok[:, None], p64 / r[:, None], 0.0)
+                wd = dd @ Rs[s].T if use_R else dd
+                slot_r, acc_r = oracle.lidar_policy(wd, r, ok, v[s], LIDAR, 0.3)
+                for k in (1, 3):
+                    sl, ac = outs[k]
+                    assert sl[s][12] == slot_r[12], (k, s)
+                    assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
+    finally:
+        _lib.call("rmpb_set_option", b"lidar_kernel", 0)
