@@ -1082,7 +1082,7 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
   const int64_t target = g_opt_lidar_warps.load();
   int64_t wps = (target + S_ - 1) / S_;
   wps = std::min<int64_t>(wps, 1024);
-  wps = std::min<int64_t>(wps, (n + 255) / 256);
+  wps = std::min<int64_t>(wps, (n + 127) / 128);
   wps = std::max<int64_t>(wps, 1);
   const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
   wps = (n + seg - 1) / seg;

@@ -132,7 +132,7 @@ def c3(args, out):
 
     import oracle as O
     from paper_2301_08068_b200 import synth
-    from paper_2301_08068_b200.device import lidar_policy_batch_device
+    from paper_2301_08068_b200.device import lidar_points_batch_device, lidar_policy_batch_device
     from paper_2301_08068_b200.policies import lidar_policy, preset
     from paper_2301_08068_b200.rays import scan_pattern
 
@@ -149,7 +149,8 @@ def c3(args, out):
     dirs = torch.from_numpy(np.ascontiguousarray(scan_pattern(128, 1024))).cuda()
     rg = torch.from_numpy(np.stack([scans[i % 10].ranges for i in range(S)])).cuda()
     vl = torch.from_numpy(np.stack([scans[i % 10].valid for i in range(S)]).astype(np.uint8)).cuda()
-    R = torch.eye(3, dtype=torch.float64, device="cuda").reshape(1, 9).repeat(S, 1).contiguous()
+    R = torch.from_numpy(np.stack([scans[i % 10].orientation for i in range(S)])
+                         .reshape(S, 9).copy()).cuda()
     v = torch.from_numpy(np.stack([states[i % 10].velocity for i in range(S)])).cuda()
     flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
     best, med = ev_time(lambda: lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3),
@@ -162,6 +163,15 @@ def c3(args, out):
            "stream_GBps": round(gbs, 1), "hbm_frac": round(gbs / 6541.8, 3),
            "single_scan_api_us_median": round(lat * 1e6, 1),
            "single_scan_hz": round(1.0 / lat, 1)}
+    # K2b: the same scans as raw f32 sensor-frame points (invalid -> 0)
+    pts = torch.where(vl.bool()[:, :, None], dirs[None] * rg[:, :, None], 0.0).float()
+    pts = torch.nan_to_num(pts, nan=0.0, posinf=0.0, neginf=0.0).contiguous()
+    _bp, mp = ev_time(lambda: lidar_points_batch_device(pts, R, v, LIDAR, 0.3), reps=5,
+                      flush=flush)
+    pgbs = S * n * 12 / (mp * 1e-3) / 1e9
+    rec["points"] = {"ms_per_launch": round(mp, 4), "scans_per_s": round(S / (mp * 1e-3), 1),
+                     "stream_GBps": round(pgbs, 1), "hbm_frac": round(pgbs / 6541.8, 3),
+                     "bytes_per_point": 12}
     if O.ref_available():
         pool = O.RefPool(cpu_threads())
         wd = [np.ascontiguousarray(s.world_directions()) for s in scans]
