@@ -1,10 +1,11 @@
 """Summarise one `ncu --set full` capture of the hot kernel into profiles/.
 
-    python scripts/ncu_summary.py gpurun_out/prof_full.ncu-rep [round]
+    python scripts/ncu_summary.py gpurun_out/prof_full.ncu-rep [round] [tag]
 
 Writes profiles/r<round>_ncu_summary.json (the numbers bench.py quotes:
 DRAM bytes per launch, L2 read GB/s, pipe utilisations) and the raw/details
-CSV pages next to it.
+CSV pages next to it; with a tag (e.g. "lidar") r<round>_ncu_<tag>_summary.json
+and r<round>_ncu_full_<tag>_{raw,details}.csv.
 """
 
 import csv
@@ -13,8 +14,12 @@ import json
 import subprocess
 import sys
 
-CAPTURE = ("ncu --set full --clock-control none --import-source on -k regex:k_ray_policy2 "
-           "-s 1 -c 1 python scripts/profile_target.py (4096 poses x 65536 rays, C1 map)")
+CAPTURES = {
+    None: ("ncu --set full --clock-control none --import-source on -k regex:k_ray_policy2 "
+           "-s 1 -c 1 python scripts/profile_target.py (4096 poses x 65536 rays, C1 map)"),
+    "lidar": ("ncu --set full --clock-control none --import-source on -k regex:k_lidar_warp "
+              "-s 1 -c 1 python scripts/profile_lidar.py (1024 C3 scans x 131072 beams)"),
+}
 
 SCALE = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "ns": 1e-6, "us": 1e-3,
          "usecond": 1e-3, "ms": 1.0, "msecond": 1.0, "nsecond": 1e-6}
@@ -43,6 +48,7 @@ def ncu_page(rep, page):
 def main():
     rep = sys.argv[1]
     rnd = sys.argv[2] if len(sys.argv) > 2 else "01"
+    tag = sys.argv[3] if len(sys.argv) > 3 else None
     raw = ncu_page(rep, "raw")
     rows = list(csv.reader(io.StringIO(raw)))
     head, units, vals = rows[0], rows[1], rows[2]
@@ -53,19 +59,22 @@ def main():
         x = float(vals[i].replace(",", ""))
         return x * SCALE.get(units[i], 1.0)
 
-    out = {"kernel": vals[col["Kernel Name"]].split("(")[0], "capture": CAPTURE,
+    out = {"kernel": vals[col["Kernel Name"]].split("(")[0], "capture": CAPTURES.get(tag),
            "duration_ms": get("gpu__time_duration.sum")}
     for k, name in FIELDS.items():
         if name in col:
             out[k] = get(name)
     out["dram_bytes_per_launch"] = out["dram_bytes_read"] + out["dram_bytes_write"]
     out["l2_read_GBps"] = out["l2_read_sectors_from_l1"] * 32 / (out["duration_ms"] * 1e-3) / 1e9
-    with open(f"profiles/r{rnd}_ncu_summary.json", "w") as fh:
+    out["dram_GBps"] = out["dram_bytes_per_launch"] / (out["duration_ms"] * 1e-3) / 1e9
+    summ = f"profiles/r{rnd}_ncu_{tag}_summary.json" if tag else f"profiles/r{rnd}_ncu_summary.json"
+    stem = f"profiles/r{rnd}_ncu_full_{tag or 'k_ray_policy2'}"
+    with open(summ, "w") as fh:
         json.dump(out, fh, indent=1)
         fh.write("\n")
-    with open(f"profiles/r{rnd}_ncu_full_k_ray_policy2_raw.csv", "w") as fh:
+    with open(stem + "_raw.csv", "w") as fh:
         fh.write(raw)
-    with open(f"profiles/r{rnd}_ncu_full_k_ray_policy2_details.csv", "w") as fh:
+    with open(stem + "_details.csv", "w") as fh:
         fh.write(ncu_page(rep, "details"))
     print(json.dumps(out, indent=1))
 
