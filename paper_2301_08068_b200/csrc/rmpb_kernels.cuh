@@ -203,6 +203,13 @@ __device__ __forceinline__ void policy_flush(K2Smem& sm, int warp, int lane, boo
 #ifndef RMPB_REFILL
 #define RMPB_REFILL 8  // refill when at least this many lanes are idle (or none alive)
 #endif
+#ifndef RMPB_TOWARD_FILTER
+#define RMPB_TOWARD_FILTER 1  // queue only hits closing on the obstacle (toward > 0)
+#endif
+#ifndef RMPB_LANE_COUNT
+#define RMPB_LANE_COUNT 1  // lane-private hit count (no per-round ballot)
+#endif
+
 // RAYOUT: per-ray parity outputs (t, cell, steps) and the step counter.
 // FAST: fp32 march (opt-in, not reference-exact; see interp_f).
 template <class G, bool RAYOUT, bool FAST = false>
@@ -294,7 +301,17 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
           const int pos = __popc(m & lt);
           sm.pt[warp][pos] = t0; sm.pe[warp][pos] = t1;
           sm.px[warp][pos] = ex; sm.py[warp][pos] = ey; sm.pz[warp][pos] = ez;
+#if RMPB_TOWARD_FILTER
+          // policy_accumulate adds nothing for toward <= 0 (_ckern.pyx:295-299):
+          // flag the ray (sign bit) so only closing hits are queued.  Same
+          // expression and rounding as policy_accumulate's test.
+          double vx, vy, vz;
+          io.vel(pose, vx, vy, vz);
+          const double toward = ex * vx + ey * vy + ez * vz;
+          sm.pr[warp][pos] = (toward > 0.0) ? (int)((unsigned)r | 0x80000000u) : r;
+#else
           sm.pr[warp][pos] = r;
+#endif
         }
         pcount = __popc(m);
         phead = 0;
@@ -345,11 +362,17 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
         alive = !hit_now && t <= tend;  // !(t > tend); a NaN t ends the ray
       }
     }
+#if RMPB_TOWARD_FILTER
+    const bool enq = hit_now && (double)t < p.radius && ray < 0;
+    const int rid = ray & 0x7fffffff;
+#else
     const bool enq = hit_now && (double)t < p.radius;
+    const int rid = ray;
+#endif
     if (RAYOUT && was_alive && !alive) {
       my_steps += steps;
       if (ro.t) {
-        const int o = b.perm ? b.perm[ray] : ray;
+        const int o = b.perm ? b.perm[rid] : rid;
         ro.t[o] = hit_now ? (double)t : CUDART_INF;
         if (ro.cell) {
           ro.cell[3 * o] = hit_now ? hx : -1; ro.cell[3 * o + 1] = hit_now ? hy : -1;
@@ -359,13 +382,17 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
       }
     }
     // ---- queue policy work; evaluate in full-warp batches of 32
+#if RMPB_LANE_COUNT
+    cnt += hit_now;  // lane-private; min_range = 0: every hit counts
+#else
     cnt += __popc(__ballot_sync(FULL, hit_now));  // warp-uniform; min_range = 0: every hit counts
+#endif
     const unsigned em = __ballot_sync(FULL, enq);
     if (em) {
       if (enq) {
         const int pos = qn + __popc(em & lt);
         qt[pos] = (double)t;
-        qr[pos] = ray;
+        qr[pos] = rid;
       }
       qn += __popc(em);
       if (qn >= 32) {
@@ -392,6 +419,9 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     int s = warp_sum_i(my_steps);
     if (lane == 0) atomicAdd(ro.step_total, (unsigned long long)s);
   }
+#if RMPB_LANE_COUNT
+  cnt = warp_sum_i(cnt);
+#endif
   __syncwarp();
   Acc acc;
   acc.zero();
