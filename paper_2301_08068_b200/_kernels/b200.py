@@ -319,12 +319,69 @@ def invalidate_caches() -> None:
         _grids.clear()
         _bundles.clear()
         _scenes.clear()
+        _fast.clear()
+
+
+# Identity fast path for the control-loop pattern (the same EsdfGrid.values /
+# RayBundle.directions objects passed on every call): id(array) -> entry,
+# valid while the entry holds the array (so the id cannot be reused) and the
+# array still samples the same 72 values the fingerprint hashes.  ~2 us
+# instead of ~12 us for the keyed lookup (ndarray.ctypes alone is ~2 us).
+_fast: "OrderedDict[int, tuple]" = OrderedDict()
+_FAST_MAX = 16
+_sample_idx_cache: dict = {}
+
+
+def _sample_idx(n: int) -> np.ndarray:
+    idx = _sample_idx_cache.get(n)
+    if idx is None:
+        if n <= 512:
+            idx = np.arange(n, dtype=np.intp)
+        else:
+            step = n // 8
+            idx = np.concatenate([np.arange(k * step, k * step + 8) for k in range(8)] +
+                                 [np.arange(n - 8, n)]).astype(np.intp)
+        _sample_idx_cache[n] = idx
+    return idx
+
+
+def _sample(a: np.ndarray) -> bytes:
+    return a.reshape(-1).take(_sample_idx(a.size)).tobytes()
+
+
+def _fast_get(obj, extra):
+    e = _fast.get(id(obj))
+    if e is None or e[0] is not obj or e[1] != extra:
+        return None
+    if e[2] is not None and _sample(obj) != e[2]:
+        return None
+    return e[3]
+
+
+def _fast_put(obj, extra, frozen: bool, dev_obj) -> None:
+    with _lock:
+        if len(_fast) >= _FAST_MAX:
+            _fast.popitem(last=False)
+        _fast[id(obj)] = (obj, extra, None if frozen else _sample(obj), dev_obj)
 
 
 def device_grid(values, origin, res) -> DeviceGrid:
     """Device copy of an EsdfGrid's values (cached)."""
     if isinstance(values, DeviceGrid):
         return values
+    o_l = origin.tolist() if type(origin) is np.ndarray else [float(x) for x in origin]
+    extra = (o_l, res, _device)
+    hit = _fast_get(values, extra)
+    if hit is not None:
+        return hit
+    g = _device_grid_keyed(values, origin, res)
+    if (type(values) is np.ndarray and values.flags.c_contiguous and values.dtype in
+            (np.float64, np.float32)):
+        _fast_put(values, extra, _frozen(values), g)
+    return g
+
+
+def _device_grid_keyed(values, origin, res) -> DeviceGrid:
     v = np.asarray(values)
     if v.dtype != np.float32:
         v = np.ascontiguousarray(v, dtype=np.float64)
@@ -347,6 +404,17 @@ def device_grid(values, origin, res) -> DeviceGrid:
 def device_bundle(dirs) -> DeviceBundle:
     if isinstance(dirs, DeviceBundle):
         return dirs
+    hit = _fast_get(dirs, _device)
+    if hit is not None:
+        return hit
+    b = _device_bundle_keyed(dirs)
+    if (type(dirs) is np.ndarray and dirs.flags.c_contiguous and dirs.dtype == np.float64 and
+            dirs.ndim == 2 and dirs.shape[1] == 3):
+        _fast_put(dirs, _device, _frozen(dirs), b)
+    return b
+
+
+def _device_bundle_keyed(dirs) -> DeviceBundle:
     d = _f64(dirs, (-1, 3))
     key = (d.ctypes.data, d.shape[0], _device, 0 if _frozen(d) else _fingerprint(d))
     with _lock:
@@ -467,15 +535,33 @@ _param_cache: dict = {}
 
 
 def _params_cached(params):
+    """(array, pointer) of the 7 params; cached for hashable params."""
     key = tuple(params) if not isinstance(params, np.ndarray) else None
     if key is not None:
         hit = _param_cache.get(key)
         if hit is None:
-            hit = _params(params)
+            a = _params(params)
+            hit = (a, a.ctypes.data)
             if len(_param_cache) < 64:
                 _param_cache[key] = hit
         return hit
-    return _params(params)
+    a = _params(params)
+    return a, a.ctypes.data
+
+
+_tls = threading.local()
+
+
+def _scratch():
+    """Per-thread pinned-free scratch (pose in, 16 doubles out) with cached
+    addresses: ndarray.ctypes costs ~2 us per access."""
+    s = getattr(_tls, "s", None)
+    if s is None:
+        xv = np.empty(6)
+        out = np.empty(16)
+        s = (xv, xv.ctypes.data, out, out.ctypes.data)
+        _tls.s = s
+    return s
 
 
 def ray_policy_fused(values, origin, res, start, velocity, dirs, params, max_range, eps,
@@ -484,20 +570,19 @@ def ray_policy_fused(values, origin, res, start, velocity, dirs, params, max_ran
     with ``with_rays``, per-ray (t, cells, steps) in original ray order."""
     g = device_grid(values, origin, res)
     b = device_bundle(dirs)
-    xv = np.empty(6)
+    xv, base, out, optr = _scratch()
     xv[0:3] = start
     xv[3:6] = velocity
-    out = np.empty(16)
     t = cells = steps = None
     if with_rays:
         t = np.empty(b.n)
         cells = np.empty((b.n, 3), np.int32)
         steps = np.empty(b.n, np.int32)
-    base = xv.ctypes.data
     L.check(L.load().rmpb_ray_policy(
-        g.handle, b.handle, base, base + 24, _params_cached(params).ctypes.data,
-        float(max_range), float(eps), float(step_scale), out.ctypes.data,
-        out.ctypes.data + 104, _ptr(t), _ptr(cells), _ptr(steps), None), "rmpb_ray_policy")
+        g.handle, b.handle, base, base + 24, _params_cached(params)[1],
+        float(max_range), float(eps), float(step_scale), optr, optr + 104,
+        _ptr(t), _ptr(cells), _ptr(steps), None), "rmpb_ray_policy")
+    out = out.copy()
     slot, acc = out[:13], out[13:]
     if with_rays:
         return slot, acc, t, cells, steps

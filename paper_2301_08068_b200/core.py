@@ -44,6 +44,16 @@ class Policy:
         object.__setattr__(self, "accel", f)
         object.__setattr__(self, "metric", m)
 
+    @classmethod
+    def _trusted(cls, accel: np.ndarray, metric: np.ndarray) -> "Policy":
+        """Construct without re-checking: the caller guarantees a finite
+        (3,) accel and a finite, exactly symmetric (3, 3) metric (what
+        __post_init__ would produce unchanged)."""
+        p = object.__new__(cls)
+        object.__setattr__(p, "accel", accel)
+        object.__setattr__(p, "metric", metric)
+        return p
+
     def is_psd(self, tol: float = _PSD_TOL) -> bool:
         return bool(np.linalg.eigvalsh(self.metric).min() >= -tol)
 

@@ -26,6 +26,8 @@ from __future__ import annotations
 import json
 from dataclasses import asdict, dataclass
 
+import math
+
 import numpy as np
 
 from ._kernels import get_backend
@@ -141,7 +143,23 @@ def esdf_policy(state: RobotState, grid: EsdfGrid, p: ObstacleParams) -> Policy:
     return obstacle_ray_policy(state.velocity, sample.gradient, sample.distance, p)
 
 
+_SYM_SAFE = 8.98e307  # 0.5 * (m + m.T) overflows above DBL_MAX / 2
+
+
 def _policy_from_slot(slot, accel) -> Policy:
+    """Policy from a device slot.  The device writes the metric exactly
+    symmetric (a01 duplicated), so Policy's symmetrisation 0.5 * (m + m.T)
+    returns it unchanged whenever it cannot overflow: such slots take a
+    check-only path (~2 us instead of ~15 us of small NumPy ops); anything
+    else goes through Policy's own construction (and its ValueError)."""
+    if type(slot) is np.ndarray and type(accel) is np.ndarray and slot.dtype == np.float64 \
+            and accel.dtype == np.float64:
+        m = slot[0:9]
+        lm = m.tolist()
+        la = accel.tolist()
+        if (len(lm) == 9 and len(la) == 3 and lm[1] == lm[3] and lm[2] == lm[6] and lm[5] == lm[7]
+                and all(abs(x) < _SYM_SAFE for x in lm) and all(abs(x) < math.inf for x in la)):
+            return Policy._trusted(accel, m.reshape(3, 3))
     return Policy(np.asarray(accel, dtype=float), np.asarray(slot[0:9], dtype=float).reshape(3, 3))
 
 

@@ -12,6 +12,7 @@
 #include "rmpb.h"
 
 __global__ void k_empty() {}
+__global__ void k_flag(volatile unsigned* f, unsigned v) { if (threadIdx.x == 0 && blockIdx.x == 0) { __threadfence_system(); *f = v; } }
 
 static double now_us() {
   return std::chrono::duration<double, std::micro>(
@@ -41,6 +42,13 @@ int main() {
   cudaStream_t s; cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking);
   double e0 = med([&](int) { k_empty<<<1, 32, 0, s>>>(); cudaStreamSynchronize(s); });
   double e1 = med([&](int) { k_empty<<<256, 256, 0, s>>>(); cudaStreamSynchronize(s); });
+  volatile unsigned* hflag; cudaHostAlloc((void**)&hflag, 64, cudaHostAllocMapped);
+  unsigned* dflag; cudaHostGetDevicePointer((void**)&dflag, (void*)hflag, 0);
+  *hflag = 0; unsigned ep = 0;
+  double e2 = med([&](int) { ++ep; k_flag<<<1, 32, 0, s>>>(dflag, ep); while (*hflag != ep) {} });
+  double e3 = med([&](int) { k_empty<<<1, 32, 0, s>>>(); while (cudaStreamQuery(s) == cudaErrorNotReady) {} });
+  double e4 = med([&](int) { k_empty<<<1, 32, 0, s>>>(); });
+  cudaStreamSynchronize(s);
   auto call = [&](int i, double mr, void* st) {
     const double* x = P + 6 * (i % 10);
     int rc = rmpb_ray_policy(g, b, x, x + 3, prm, mr, 0.05, 0.9, slot, acc, nullptr, nullptr, nullptr, st);
@@ -50,6 +58,7 @@ int main() {
   double r10 = med([&](int i) { call(i, 10.0, nullptr); });
   double r0s = med([&](int i) { call(i, 1e-6, s); });
   double r10s = med([&](int i) { call(i, 10.0, s); });
+  printf("{\"flag_spin_us\": %.2f, \"query_spin_us\": %.2f, \"launch_only_us\": %.2f, ", e2, e3, e4);
   printf("{\"empty_1x32_us\": %.2f, \"empty_256x256_us\": %.2f, \"abi_range0_us\": %.2f, "
          "\"abi_range10_us\": %.2f, \"abi_range0_stream_us\": %.2f, \"abi_range10_stream_us\": %.2f}\n",
          e0, e1, r0, r10, r0s, r10s);

@@ -709,3 +709,34 @@ def test_lidar_points_kernels_ragged(be, oracle, n, S):
                     assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
     finally:
         _lib.call("rmpb_set_option", b"lidar_kernel", 0)
+
+
+# --- host fast path: repeated calls with the same arrays -----------------------
+
+def test_public_ray_policy_repeated_and_in_place_edit(be, oracle):
+    """The control-loop pattern: the same EsdfGrid / RayBundle objects every
+    call (identity cache), then an in-place edit of the map is picked up."""
+    import paper_2301_08068_b200 as P
+    from paper_2301_08068_b200 import synth
+
+    scene = synth.c1_scene(n_boxes=20, hi=np.array([5.9, 5.9, 2.9]))
+    vals = be.bake_values(scene.packed(), np.zeros(3), 0.1, (60, 60, 30))
+    vals = vals.astype(np.float32).astype(np.float64)
+    grid = P.EsdfGrid(np.zeros(3), 0.1, (60, 60, 30), vals)
+    dirs = oracle.sample_directions(4096)
+    bundle = P.RayBundle(dirs)
+    params = P.preset("static_map").obstacle
+    st = P.RobotState(np.array([3.0, 3.1, 1.4]), np.array([0.6, -0.3, 0.1]))
+    ref = oracle.ray_policy(grid.values, grid.origin, 0.1, st.position, st.velocity, dirs,
+                            params.as_tuple(), 10.0)
+    for _ in range(3):
+        pol = P.ray_policy(st, grid, bundle, params, 10.0)
+        assert rel_err(pol.metric, ref[0][:9].reshape(3, 3)) <= SUM_TOL
+        assert rel_err(pol.accel, ref[1]) <= ACC_TOL
+    grid.values[...] -= 0.25  # in place: obstacles grow, every sampled node changes
+    ref2 = oracle.ray_policy(grid.values, grid.origin, 0.1, st.position, st.velocity, dirs,
+                             params.as_tuple(), 10.0)
+    pol2 = P.ray_policy(st, grid, bundle, params, 10.0)
+    assert rel_err(pol2.metric, ref2[0][:9].reshape(3, 3)) <= SUM_TOL
+    assert rel_err(pol2.accel, ref2[1]) <= ACC_TOL
+    assert not np.allclose(pol2.metric, pol.metric)
