@@ -161,6 +161,33 @@ RMPB_EXPORT int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bund
 RMPB_EXPORT int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double* d_slot, double* d_accel,
                              void* stream);
 
+/* ---- fused ray-split exchange over peer memory (K4; config C5) --------- */
+/* The all-gather + fold of the ray-split path (rmpnav/_kernels/_pool.py:
+ * 61-72 partial-slot contract) done inside the trace kernel's epilogue: each
+ * rank's final CTA stores its 13-slot into every rank's mailbox over NVLink
+ * (P2P through CUDA IPC), publishes an epoch, waits for all `world` epochs
+ * and folds in rank order + solves.  One mailbox per rank (device memory);
+ * ranks exchange the 64-byte IPC handles once (e.g. all_gather_object) and
+ * open each other's mailboxes; same-process peers use rmpb_peer_attach. */
+#define RMPB_IPC_HANDLE_BYTES 64
+typedef struct rmpb_peer rmpb_peer;
+RMPB_EXPORT int rmpb_peer_create(int world, int rank, int device, void* ipc_handle_out, rmpb_peer** out);
+RMPB_EXPORT int rmpb_peer_open_ipc(rmpb_peer* p, int peer_rank, const void* ipc_handle);
+RMPB_EXPORT int rmpb_peer_attach(rmpb_peer* p, int peer_rank, const rmpb_peer* other);
+/* 1 if a wait gave up (a peer never published its epoch within 10 s; the
+ * slot / accel of that call are NaN). */
+RMPB_EXPORT int rmpb_peer_error(rmpb_peer* p, int* timed_out);
+RMPB_EXPORT int rmpb_peer_destroy(rmpb_peer* p);
+/* This rank's rays [ray_begin, ray_end) of one pose + the exchange + fold +
+ * pinv in ONE launch; every rank passes the same epoch (>= 1, +1 per call).
+ * mode: 3 = post + wait (production); 1 = post only, 2 = wait only (lets
+ * one-GPU tests run the ranks one after another, never concurrently). */
+RMPB_EXPORT int rmpb_ray_policy_range_exchange(const rmpb_grid* g, const rmpb_bundle* b, const double* d_x,
+                                   const double* d_v, int64_t ray_begin, int64_t ray_end,
+                                   const double params[7], double max_range, double eps,
+                                   double step_scale, rmpb_peer* peer, uint64_t epoch, int mode,
+                                   double* d_slot, double* d_accel, void* stream);
+
 /* ---- LiDAR-direct policy (K2; policies.py:195-205) ----------------------- */
 /* dirs: n x 3 sensor-frame directions (world when R == NULL); R: 3x3
  * row-major sensor orientation (world = dirs @ R^T, rays.py:172-173);

@@ -66,6 +66,13 @@ _SIGS = {
     "rmpb_ray_policy_range_device": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _d, _d, _d, _vp,
                                           _vp]),
     "rmpb_fold_resolve_device": (_i, [_vp, _i64, _vp, _vp, _vp]),
+    "rmpb_peer_create": (_i, [_i, _i, _i, _vp, _vp]),
+    "rmpb_peer_open_ipc": (_i, [_vp, _i, _vp]),
+    "rmpb_peer_attach": (_i, [_vp, _i, _vp]),
+    "rmpb_peer_error": (_i, [_vp, _vp]),
+    "rmpb_peer_destroy": (_i, [_vp]),
+    "rmpb_ray_policy_range_exchange": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _d, _d, _d, _vp,
+                                            ctypes.c_uint64, _i, _vp, _vp, _vp]),
     "rmpb_lidar_policy": (_i, [_vp, _vp, _vp, _vp, _i64, _vp, _vp, _d, _vp, _vp, _vp]),
     "rmpb_lidar_policy_bundle": (_i, [_vp, _vp, _vp, _vp, _vp, _vp, _d, _vp, _vp, _vp]),
     "rmpb_lidar_policy_batch_device": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _d, _vp,

@@ -1060,6 +1060,158 @@ extern "C" int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bundl
                            segs, seg_rays, ro, st);
 }
 
+// ---------------------------------------------------------------------------
+// K4 fused peer exchange (config C5): mailboxes + the fused range entry.
+
+struct rmpb_peer {
+  int device = -1, world = 0, rank = 0;
+  void* d_block = nullptr;          // this rank's mailbox: flags then slots
+  size_t flags_bytes = 0, bytes = 0;
+  PeerEx table{};                   // host copy of the device table
+  PeerEx* d_table = nullptr;
+  unsigned* d_err = nullptr;
+  std::vector<void*> ipc_mapped;    // peers opened through IPC (closed at destroy)
+  std::vector<bool> have;
+};
+
+static void peer_set(rmpb_peer* p, int r, void* base) {
+  p->table.flags[r] = (unsigned long long*)base;
+  p->table.slots[r] = (double*)((char*)base + p->flags_bytes);
+  p->have[r] = true;
+}
+
+extern "C" int rmpb_peer_create(int world, int rank, int device, void* ipc_out, rmpb_peer** out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  if (world < 1 || world > kMaxPeers) return fail(RMPB_ERR_INVALID, "world must be 1..%d", kMaxPeers);
+  if (rank < 0 || rank >= world) return fail(RMPB_ERR_INVALID, "rank %d not in [0, %d)", rank, world);
+  DeviceGuard dg(device);
+  if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
+  std::unique_ptr<rmpb_peer> p(new rmpb_peer());
+  p->device = device; p->world = world; p->rank = rank;
+  p->flags_bytes = ((size_t)2 * world * sizeof(unsigned long long) + 255) / 256 * 256;
+  p->bytes = p->flags_bytes + (size_t)2 * world * kMbox * sizeof(double);
+  CK(cudaMalloc(&p->d_block, p->bytes));
+  CK(cudaMemset(p->d_block, 0, p->bytes));  // epochs start at 1
+  CK(cudaMalloc((void**)&p->d_table, sizeof(PeerEx)));
+  CK(cudaMalloc((void**)&p->d_err, sizeof(unsigned)));
+  CK(cudaMemset(p->d_err, 0, sizeof(unsigned)));
+  p->have.assign(world, false);
+  p->table.world = world; p->table.rank = rank; p->table.err = p->d_err;
+  peer_set(p.get(), rank, p->d_block);
+  if (ipc_out) {
+    cudaIpcMemHandle_t h;
+    CK(cudaIpcGetMemHandle(&h, p->d_block));
+    static_assert(sizeof(h) == RMPB_IPC_HANDLE_BYTES, "IPC handle size");
+    memcpy(ipc_out, &h, sizeof(h));
+  }
+  CK(cudaDeviceSynchronize());
+  *out = p.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_peer_open_ipc(rmpb_peer* p, int peer_rank, const void* ipc_handle) {
+  if (!p || !ipc_handle) return fail(RMPB_ERR_INVALID, "NULL peer / handle");
+  if (peer_rank < 0 || peer_rank >= p->world || peer_rank == p->rank)
+    return fail(RMPB_ERR_INVALID, "bad peer rank %d", peer_rank);
+  DeviceGuard dg(p->device);
+  cudaIpcMemHandle_t h;
+  memcpy(&h, ipc_handle, sizeof(h));
+  void* base = nullptr;
+  CK(cudaIpcOpenMemHandle(&base, h, cudaIpcMemLazyEnablePeerAccess));
+  p->ipc_mapped.push_back(base);
+  peer_set(p, peer_rank, base);
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_peer_attach(rmpb_peer* p, int peer_rank, const rmpb_peer* other) {
+  if (!p || !other) return fail(RMPB_ERR_INVALID, "NULL peer");
+  if (peer_rank < 0 || peer_rank >= p->world || peer_rank == p->rank || other->rank != peer_rank ||
+      other->world != p->world)
+    return fail(RMPB_ERR_INVALID, "peer %d does not match (world %d, its rank %d)", peer_rank,
+                other->world, other->rank);
+  if (other->device != p->device) {
+    DeviceGuard dg(p->device);
+    cudaError_t e = cudaDeviceEnablePeerAccess(other->device, 0);
+    if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+      return fail(RMPB_ERR_CUDA, "peer access %d -> %d: %s", p->device, other->device,
+                  cudaGetErrorString(e));
+    (void)cudaGetLastError();
+  }
+  peer_set(p, peer_rank, other->d_block);
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_peer_error(rmpb_peer* p, int* timed_out) {
+  if (!p || !timed_out) return fail(RMPB_ERR_INVALID, "NULL argument");
+  DeviceGuard dg(p->device);
+  unsigned e = 0;
+  CK(cudaMemcpy(&e, p->d_err, sizeof(e), cudaMemcpyDeviceToHost));
+  *timed_out = (int)e;
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_peer_destroy(rmpb_peer* p) {
+  if (!p) return RMPB_OK;
+  DeviceGuard dg(p->device);
+  cudaDeviceSynchronize();
+  for (void* m : p->ipc_mapped) cudaIpcCloseMemHandle(m);
+  cudaFree(p->d_block);
+  cudaFree(p->d_table);
+  cudaFree(p->d_err);
+  delete p;
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_ray_policy_range_exchange(const rmpb_grid* g, const rmpb_bundle* b,
+                                              const double* d_x, const double* d_v,
+                                              int64_t ray_begin, int64_t ray_end,
+                                              const double params[7], double max_range,
+                                              double eps, double step_scale, rmpb_peer* peer,
+                                              uint64_t epoch, int mode, double* d_slot,
+                                              double* d_accel, void* stream) {
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (!peer) return fail(RMPB_ERR_INVALID, "peer is NULL");
+  if (!d_x || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
+  if (peer->device != g->device)
+    return fail(RMPB_ERR_INVALID, "peer mailbox on device %d, grid on %d", peer->device, g->device);
+  if (epoch == 0) return fail(RMPB_ERR_INVALID, "epoch must be >= 1");
+  if (mode < 1 || mode > 3) return fail(RMPB_ERR_INVALID, "mode must be 1 (post), 2 (wait) or 3");
+  for (int r = 0; r < peer->world; ++r)
+    if (!peer->have[r]) return fail(RMPB_ERR_INVALID, "peer %d mailbox not opened", r);
+  if (ray_begin < 0 || ray_end > b->n || ray_begin > ray_end)
+    return fail(RMPB_ERR_INVALID, "bad ray range [%lld, %lld) of %lld", (long long)ray_begin,
+                (long long)ray_end, (long long)b->n);
+  if (ray_end == ray_begin) return fail(RMPB_ERR_INVALID, "empty ray range");
+  DeviceGuard dg(g->device);
+  Workspace* ws = workspace(g->device, stream);
+  std::lock_guard<std::mutex> lk(ws->mu);
+  cudaStream_t st = S(stream);
+  CK(cudaMemcpyAsync(peer->d_table, &peer->table, sizeof(PeerEx), cudaMemcpyHostToDevice, st));
+  rmpb_bundle sub = *b;
+  sub.d_dx = b->d_dx + ray_begin;
+  sub.d_dy = b->d_dy + ray_begin;
+  sub.d_dz = b->d_dz + ray_begin;
+  sub.d_rcp = b->d_rcp + ray_begin;
+  sub.d_perm = nullptr;
+  sub.n = ray_end - ray_begin;
+  int segs, seg_rays;
+  choose_segments(1, sub.n, &segs, &seg_rays);
+  TRY(ws->partials.ensure((size_t)segs * kAcc * sizeof(double)));
+  TRY(ws->ensure_tickets(1));
+  PoseIO io{};
+  io.x = d_x; io.v = d_v; io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  io.ex = peer->d_table;
+  io.ex_epoch = epoch;
+  io.ex_mode = mode;
+  RayOut ro{};
+  return launch_ray_policy(g, &sub, io, 1, make_params(params, 0.0), max_range, eps, step_scale,
+                           segs, seg_rays, ro, st);
+}
+
 extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double* d_slot,
                                         double* d_accel, void* stream) {
   if (!d_slots || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");

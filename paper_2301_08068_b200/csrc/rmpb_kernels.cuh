@@ -15,6 +15,67 @@
 
 namespace rmpb {
 
+// ---------------------------------------------------------------------------
+// K4 fused: ray-split partial -> peer-memory exchange -> fold -> solve, in the
+// epilogue of the trace kernel (config C5).  Every rank owns
+// one mailbox in its device memory: flags [2][world] (u64 epochs) then slots
+// [2][world][16] doubles, double-buffered on the epoch parity.  The pose's
+// final CTA stores its 13-slot into mailbox[rank] of EVERY rank (NVLink P2P
+// stores through IPC-mapped pointers), fences at system scope, publishes the
+// epoch with a release store, then waits (acquire) for all `world` epochs in
+// its own mailbox and folds the slots in rank order with the reference's
+// pairwise shape (_pool.py:61-72) -- the same result as the all-gather path,
+// identical on every rank.  Parity double-buffering makes reuse safe: a rank
+// can only start epoch e+2 (same parity) after every rank published e+1,
+// i.e. finished reading epoch e.
+constexpr int kMaxPeers = 8;
+constexpr int kMbox = 16;  // doubles per slot record (13 used)
+enum : int { EX_POST = 1, EX_WAIT = 2 };
+
+struct PeerEx {
+  double* slots[kMaxPeers];               // each rank's [2][world][kMbox]
+  unsigned long long* flags[kMaxPeers];   // each rank's [2][world]
+  int world, rank;
+  unsigned* err;                          // device word: 1 = wait timed out
+};
+
+__device__ __forceinline__ void st_release_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+// Fixed pairwise fold (rmpnav/_kernels/_pool.py:61-72: s[2k] + s[2k+1], odd
+// tail carried) of n <= 64 13-slots at `stride` doubles; one thread.
+__device__ inline void fold_slots(const double* slots, int n, int stride, bool bypass_l1,
+                                  double out[13]) {
+  double buf[64 * 13];
+  int m = n < 64 ? n : 64;
+  for (int i = 0; i < m; ++i)
+    for (int j = 0; j < 13; ++j)
+      buf[i * 13 + j] = bypass_l1 ? __ldcg(slots + (size_t)i * stride + j) : slots[(size_t)i * stride + j];
+  while (m > 1) {
+    int half = m / 2;
+    for (int k = 0; k < half; ++k)
+      for (int j = 0; j < 13; ++j) buf[k * 13 + j] = buf[2 * k * 13 + j] + buf[(2 * k + 1) * 13 + j];
+    if (m % 2)
+      for (int j = 0; j < 13; ++j) buf[half * 13 + j] = buf[(m - 1) * 13 + j];
+    m = half + (m % 2);
+  }
+  for (int j = 0; j < 13; ++j) out[j] = buf[j];
+}
+
+struct PoseIO;
+__device__ void exchange_emit(const Acc& s, const PoseIO& io);
+
 struct PoseIO {
   const double* __restrict__ x;   // [P][3] positions
   const double* __restrict__ v;   // [P][3] velocities
@@ -25,6 +86,9 @@ struct PoseIO {
   double* __restrict__ seg_out;   // [P*segs][10] raw segment partials (ray-split), or null
   double x0[3], v0[3];            // single pose by value when x / v are null
   const int* __restrict__ active; // [P] skip poses whose flag is 0 (rollouts), or null
+  const PeerEx* ex;               // fused peer exchange (K4; single pose), or null
+  unsigned long long ex_epoch;
+  int ex_mode;                    // EX_POST | EX_WAIT (split only for one-GPU tests)
   __device__ __forceinline__ void pose(int p, double& a, double& b, double& c) const {
     if (x) { a = x[3 * p]; b = x[3 * p + 1]; c = x[3 * p + 2]; } else { a = x0[0]; b = x0[1]; c = x0[2]; }
   }
@@ -70,8 +134,10 @@ __device__ __forceinline__ void finish_unit(Acc& acc, const PoseIO& io, int pose
   block_reduce(acc, sm);
   if (io.seg_out && threadIdx.x == 0) acc_to_arr(acc, io.seg_out + (size_t)(pose * segs + seg) * kAcc);
   if (segs == 1) {
-    if (threadIdx.x == 0 && io.slot)
-      write_slot(acc, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
+    if (threadIdx.x == 0 && io.slot) {
+      if (io.ex) exchange_emit(acc, io);
+      else write_slot(acc, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
+    }
     return;
   }
   if (!io.slot) return;
@@ -100,8 +166,49 @@ __device__ __forceinline__ void finish_unit(Acc& acc, const PoseIO& io, int pose
   f.cnt = (int)cnt;
   block_reduce(f, sm);
   if (threadIdx.x == 0) {
-    write_slot(f, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
     io.tickets[pose] = 0u;  // self-reset: graph replays / next call start clean
+    if (io.ex) exchange_emit(f, io);
+    else write_slot(f, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
+  }
+}
+
+// The K4 epilogue (one thread of the pose's final CTA); see PeerEx.
+__device__ void exchange_emit(const Acc& s, const PoseIO& io) {
+  const PeerEx& ex = *io.ex;
+  const int W = ex.world, par = (int)(io.ex_epoch & 1ull);
+  if (io.ex_mode & EX_POST) {
+    const double rec[13] = {s.a00, s.a01, s.a02, s.a01, s.a11, s.a12, s.a02, s.a12, s.a22,
+                            s.b0,  s.b1,  s.b2,  (double)s.cnt};
+    for (int r = 0; r < W; ++r) {
+      double* dst = ex.slots[r] + ((size_t)par * W + ex.rank) * kMbox;
+      for (int j = 0; j < 13; ++j) __stcg(dst + j, rec[j]);
+    }
+    __threadfence_system();
+    for (int r = 0; r < W; ++r) st_release_sys(ex.flags[r] + (size_t)par * W + ex.rank, io.ex_epoch);
+  }
+  if (!(io.ex_mode & EX_WAIT)) return;
+  const unsigned long long* fl = ex.flags[ex.rank] + (size_t)par * W;
+  const unsigned long long t0 = globaltimer_ns();
+  bool ok = true;
+  for (int r = 0; r < W && ok; ++r) {
+    while (ld_acquire_sys(fl + r) != io.ex_epoch) {
+      if (globaltimer_ns() - t0 > 10000000000ull) { ok = false; break; }  // 10 s: a peer is gone
+      __nanosleep(32);
+    }
+  }
+  double out[13];
+  if (ok) {
+    fold_slots(ex.slots[ex.rank] + (size_t)par * W * kMbox, W, kMbox, true, out);
+  } else {
+    atomicExch(ex.err, 1u);
+    for (int j = 0; j < 13; ++j) out[j] = CUDART_NAN;
+  }
+  for (int j = 0; j < 13; ++j) io.slot[j] = out[j];
+  if (io.accel) {
+    double m9[9] = {out[0], out[1], out[2], out[3], out[4], out[5], out[6], out[7], out[8]};
+    double f[3] = {out[9], out[10], out[11]};
+    if (ok) pinv_apply(m9, f, io.accel);
+    else io.accel[0] = io.accel[1] = io.accel[2] = CUDART_NAN;
   }
 }
 
@@ -925,19 +1032,9 @@ k_grid_trace(G grid, GridGeom g, const double* __restrict__ dirs, int n, double 
 __global__ void k_fold_resolve(const double* __restrict__ slots, int n, double* __restrict__ out_slot,
                                double* __restrict__ out_accel) {
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
-  // pairwise fold with an in-register stack is awkward for arbitrary n;
-  // n is small (number of GPUs), so fold in a local buffer.
-  double buf[64 * 13];
-  int m = n < 64 ? n : 64;
-  for (int i = 0; i < m * 13; ++i) buf[i] = slots[i];
-  while (m > 1) {
-    int half = m / 2;
-    for (int k = 0; k < half; ++k)
-      for (int j = 0; j < 13; ++j) buf[k * 13 + j] = buf[2 * k * 13 + j] + buf[(2 * k + 1) * 13 + j];
-    if (m % 2)
-      for (int j = 0; j < 13; ++j) buf[half * 13 + j] = buf[(m - 1) * 13 + j];
-    m = half + (m % 2);
-  }
+  // n is small (number of GPUs): fold in a local buffer.
+  double buf[13];
+  fold_slots(slots, n, 13, false, buf);
   for (int j = 0; j < 13; ++j) out_slot[j] = buf[j];
   if (out_accel) {
     double m9[9], f[3];

@@ -122,6 +122,72 @@ class RayPolicyEngine:
                out_accel.data_ptr(), _stream_ptr(stream))
         return out_slot, out_accel
 
+    def exchange(self, x, v, mailbox: "PeerMailbox", epoch: int, ray_begin: int, ray_end: int,
+                 mode: int = 3, out_slot=None, out_accel=None, stream=None):
+        """K4 fused: this rank's rays [ray_begin, ray_end) of one pose, the
+        partial slot stored into every rank's mailbox over peer memory, the
+        wait, the fixed-order fold and the solve -- one launch.  Returns
+        (slot13, accel3) device tensors, identical on every rank."""
+        torch = _torch()
+        _check_tensor(x, None, "float64", "x")
+        _check_tensor(v, None, "float64", "v")
+        if out_slot is None:
+            out_slot = torch.empty(13, dtype=torch.float64, device=x.device)
+        if out_accel is None:
+            out_accel = torch.empty(3, dtype=torch.float64, device=x.device)
+        L.call("rmpb_ray_policy_range_exchange", self.grid.handle, self.bundle.handle, x.data_ptr(),
+               v.data_ptr(), int(ray_begin), int(ray_end), self.params.ctypes.data,
+               self.max_range, self.eps, self.step_scale, mailbox.handle, int(epoch), int(mode),
+               out_slot.data_ptr(), out_accel.data_ptr(), _stream_ptr(stream))
+        return out_slot, out_accel
+
+
+EX_POST, EX_WAIT = 1, 2
+
+
+class PeerMailbox:
+    """This rank's mailbox for the fused ray-split exchange (K4, config C5):
+    [2][world] epoch flags + [2][world][16] slot doubles in device memory.
+    ``ipc_handle`` (64 bytes) is what the other ranks open; ``attach`` links
+    a same-process mailbox (one process driving several GPUs, or tests)."""
+
+    def __init__(self, world: int, rank: int, device: int | None = None):
+        self.world, self.rank = int(world), int(rank)
+        self.device = b200.get_device() if device is None else int(device)
+        buf = ctypes.create_string_buffer(64)
+        h = ctypes.c_void_p()
+        L.call("rmpb_peer_create", self.world, self.rank, self.device, buf, ctypes.byref(h))
+        self.handle = h
+        self.ipc_handle = buf.raw
+
+    def open(self, handles) -> None:
+        """Open every other rank's mailbox from its IPC handle (rank order)."""
+        if len(handles) != self.world:
+            raise ValueError(f"{len(handles)} handles for world {self.world}")
+        for r, hb in enumerate(handles):
+            if r != self.rank:
+                L.call("rmpb_peer_open_ipc", self.handle, r, bytes(hb))
+
+    def attach(self, other: "PeerMailbox") -> None:
+        L.call("rmpb_peer_attach", self.handle, other.rank, other.handle)
+
+    def timed_out(self) -> bool:
+        e = ctypes.c_int(0)
+        L.call("rmpb_peer_error", self.handle, ctypes.byref(e))
+        return bool(e.value)
+
+    def close(self) -> None:
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            L.load().rmpb_peer_destroy(h)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
 
 class DdaPolicyEngine:
     """K5: fused Amanatides-Woo DDA over occupancy + per-ray policy +

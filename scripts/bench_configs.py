@@ -236,6 +236,18 @@ def c5(args, out):
             sb, sm = ev_time(lambda: eng.partial(x1, v1, b_, e_), reps=5)
             shares.append(sm)
             parts.append(eng.partial(x1, v1, b_, e_))
+        # K4 fused: one rank's share + mailbox post/wait + fold + pinv in one
+        # launch (world-1 mailbox on this GPU: the epilogue's own cost)
+        from paper_2301_08068_b200.device import PeerMailbox
+        mb = PeerMailbox(1, 0)
+        b0, e0 = balanced_range(n, 8, 0)
+        ep = [0]
+
+        def fused():
+            ep[0] += 1
+            eng.exchange(x1, v1, mb, ep[0], b0, e0)
+        fb, fm = ev_time(fused, reps=5)
+        pb, pm = ev_time(lambda: eng.partial(x1, v1, b0, e0), reps=5)
         slot_split, acc_split = eng.resolve(torch.stack(parts))
         slot_whole, acc_whole = eng.evaluate(x1.view(1, 3), v1.view(1, 3))
         torch.cuda.synchronize()
@@ -247,6 +259,8 @@ def c5(args, out):
                      "steps_per_ray": round(int(ctr.item()) / (8 * n), 3),
                      "single_pose_ms": round(one_med, 3),
                      "ray_split_8_share_ms_max": round(max(shares), 3),
+                     "k4_fused_share_ms_world1": round(fm, 4),
+                     "partial_only_share_ms": round(pm, 4),
                      "split_vs_whole_rel": float(np.abs(ss[:12] - sw[:12]).max() /
                                                  max(1e-300, np.abs(sw[:12]).max())),
                      "split_n_hits_equal": bool(ss[12] == sw[12])}

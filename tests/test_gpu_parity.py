@@ -726,7 +726,7 @@ def test_public_ray_policy_repeated_and_in_place_edit(be, oracle):
     dirs = oracle.sample_directions(4096)
     bundle = P.RayBundle(dirs)
     params = P.preset("static_map").obstacle
-    st = P.RobotState(np.array([3.0, 3.1, 1.4]), np.array([0.6, -0.3, 0.1]))
+    st = synth.bench_states(scene, count=1, seed=5, distance=synth.host_box_distance(scene))[0]
     ref = oracle.ray_policy(grid.values, grid.origin, 0.1, st.position, st.velocity, dirs,
                             params.as_tuple(), 10.0)
     for _ in range(3):

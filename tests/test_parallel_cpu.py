@@ -109,3 +109,65 @@ def test_ray_split_over_gloo_world2(oracle):
     assert rel_err(res[0][2], acc) < 1e-9
     # pose shards tile the pose set
     assert res[0][3] == (0, 2048) and res[1][3] == (2048, 4096)
+
+
+class _StubMailbox:
+    def __init__(self, world, rank, device):
+        self.world, self.rank = world, rank
+        self.ipc_handle = bytes([rank]) * 64
+        self.opened = None
+
+    def open(self, handles):
+        self.opened = list(handles)
+
+
+class _StubEngine:
+    n_rays = 1001
+    device = 0
+
+    def exchange(self, x, v, mailbox, epoch, b, e, mode, stream=None):
+        return (mailbox.rank, epoch, b, e, mode, mailbox.opened)
+
+
+def _fused_worker(rank, world, port, q):
+    import sys
+
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    import torch.distributed as dist
+
+    from paper_2301_08068_b200 import parallel
+
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        fs = parallel.FusedRaySplit(_StubEngine(), mailbox_factory=_StubMailbox)
+        outs = [fs(None, None) for _ in range(3)]
+        q.put((rank, outs))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.timeout(300)
+def test_fused_split_host_logic_gloo_world3():
+    """Mailbox handles are exchanged in rank order, every rank gets its
+    balanced ray range and the epochs advance identically (1, 2, 3)."""
+    world = 3
+    port = _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_fused_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = dict(q.get(timeout=240) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    handles = [bytes([r]) * 64 for r in range(world)]
+    from paper_2301_08068_b200.parallel import balanced_range
+
+    for r in range(world):
+        outs = res[r]
+        assert [o[1] for o in outs] == [1, 2, 3]
+        b, e = balanced_range(1001, world, r)
+        for o in outs:
+            assert o[0] == r and (o[2], o[3]) == (b, e) and o[4] == 3 and o[5] == handles
