@@ -262,6 +262,19 @@ def run_b200(args):
         if i >= 20:
             lat.append(time.perf_counter() - t0)
     lat_med = statistics.median(lat)
+    # the same call through the resident-kernel latency server (no launch /
+    # stream sync per call; bitwise the same results)
+    from paper_2301_08068_b200 import LatencyServer
+
+    lat_s = []
+    with LatencyServer(grid, bundle, params, MAX_RANGE) as srv:
+        for i in range(args.latency_calls + 20):
+            st = states[i % len(states)]
+            t0 = time.perf_counter()
+            srv.policy(st)
+            if i >= 20:
+                lat_s.append(time.perf_counter() - t0)
+    lat_srv = statistics.median(lat_s)
 
     # measured L2 read ceiling (untimed), CUDA events
     l2 = l2_peaks(dev, stream)
@@ -309,6 +322,8 @@ def run_b200(args):
             "voxel_steps_per_s": round(vox_steps * world / (ms_per_step * 1e-3), 1),
             "latency_hz": round(1.0 / lat_med, 1),
             "latency_us_median": round(lat_med * 1e6, 2),
+            "latency_server_hz": round(1.0 / lat_srv, 1),
+            "latency_server_us_median": round(lat_srv * 1e6, 2),
             "roofline": roof,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 1), "unit": "rays/s",

@@ -161,6 +161,23 @@ RMPB_EXPORT int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bund
 RMPB_EXPORT int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double* d_slot, double* d_accel,
                              void* stream);
 
+/* ---- latency server (single-pose ray_policy without per-call launches) -- */
+/* One resident cooperative kernel on its own stream serves ray_policy
+ * requests (the reference's control-loop call, policies.py:182-192) posted
+ * through pinned mapped host memory: no kernel launch and no stream
+ * synchronisation per call.  Results are bitwise those of rmpb_ray_policy
+ * (same kernel body and segmentation).  The kernel holds its CTAs' SM
+ * resources while it runs and exits after idle_timeout_s without a request
+ * (the next eval relaunches it) or at rmpb_server_stop.  One caller thread
+ * per server. */
+typedef struct rmpb_server rmpb_server;
+RMPB_EXPORT int rmpb_server_start(const rmpb_grid* g, const rmpb_bundle* b, const double params[7],
+                      double max_range, double eps, double step_scale, double idle_timeout_s,
+                      rmpb_server** out);
+RMPB_EXPORT int rmpb_server_eval(rmpb_server* s, const double x[3], const double v[3],
+                     double out_slot[13], double out_accel[3]);
+RMPB_EXPORT int rmpb_server_stop(rmpb_server* s);
+
 /* ---- fused ray-split exchange over peer memory (K4; config C5) --------- */
 /* The all-gather + fold of the ray-split path (rmpnav/_kernels/_pool.py:
  * 61-72 partial-slot contract) done inside the trace kernel's epilogue: each

@@ -66,6 +66,9 @@ _SIGS = {
     "rmpb_ray_policy_range_device": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _d, _d, _d, _vp,
                                           _vp]),
     "rmpb_fold_resolve_device": (_i, [_vp, _i64, _vp, _vp, _vp]),
+    "rmpb_server_start": (_i, [_vp, _vp, _vp, _d, _d, _d, _d, _vp]),
+    "rmpb_server_eval": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "rmpb_server_stop": (_i, [_vp]),
     "rmpb_peer_create": (_i, [_i, _i, _i, _vp, _vp]),
     "rmpb_peer_open_ipc": (_i, [_vp, _i, _vp]),
     "rmpb_peer_attach": (_i, [_vp, _i, _vp]),

@@ -9,7 +9,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <cstdarg>
+#include <cstddef>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -1058,6 +1060,147 @@ extern "C" int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bundl
   RayOut ro{};
   return launch_ray_policy(g, &sub, io, 1, make_params(params, 0.0), max_range, eps, step_scale,
                            segs, seg_rays, ro, st);
+}
+
+// ---------------------------------------------------------------------------
+// Latency server (k_ray_server): one resident cooperative launch serving
+// single-pose requests through pinned mapped host memory.
+
+static_assert(offsetof(ServerMail, x) == 16 && offsetof(ServerMail, stop) == 8,
+              "ServerMail layout: (req, stop) and x / v must be 16-B aligned pairs");
+
+struct rmpb_server {
+  int device = -1;
+  const rmpb_grid* g = nullptr;
+  const rmpb_bundle* b = nullptr;
+  PolicyParams pp{};
+  double max_range = 0, eps = 0, step_scale = 0;
+  unsigned long long idle_ns = 0;
+  int segs = 0, seg_rays = 0;
+  cudaStream_t st = nullptr;
+  ServerMail* mail = nullptr;   // host pointer (pinned, mapped)
+  ServerMail* d_mail = nullptr; // its device alias
+  ServerDev* d_dev = nullptr;
+  double* d_partials = nullptr;
+  unsigned* d_tickets = nullptr;
+  unsigned long long epoch = 0;
+  bool running = false;
+};
+
+static int server_launch(rmpb_server* s) {
+  volatile ServerMail* m = s->mail;
+  m->stop = 0; m->exited = 0;
+  m->req = s->epoch; m->done = s->epoch;
+  CK(cudaMemsetAsync(s->d_dev, 0, sizeof(ServerDev), s->st));
+  CK(cudaMemcpyAsync(&s->d_dev->go, &s->epoch, sizeof(s->epoch), cudaMemcpyHostToDevice, s->st));
+  CK(cudaStreamSynchronize(s->st));
+  Bundle bv = bundle_view(s->b);
+  return with_grid(s->g, [&](auto acc) -> int {
+    using G = decltype(acc);
+    auto kfn = k_ray_server<G>;
+    int per_sm = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfn, kBlock, 0));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s->device));
+    if ((long long)per_sm * sms < s->segs)
+      return fail(RMPB_ERR_UNSUPPORTED, "server needs %d co-resident CTAs, device holds %d",
+                  s->segs, per_sm * sms);
+    GridGeom geom = s->g->geom;
+    PolicyParams pp = s->pp;
+    double mr = s->max_range, eps = s->eps, ss = s->step_scale;
+    int seg_rays = s->seg_rays;
+    ServerMail* dm = s->d_mail;
+    ServerDev* dd = s->d_dev;
+    double* parts = s->d_partials;
+    unsigned* tk = s->d_tickets;
+    unsigned long long idle = s->idle_ns, first = s->epoch;
+    void* args[] = {&acc, &geom, &bv, &pp, &mr, &eps, &ss, &seg_rays, &dm, &dd, &parts, &tk, &idle,
+                    &first};
+    CK(cudaLaunchCooperativeKernel((const void*)kfn, dim3((unsigned)s->segs), dim3(kBlock), args, 0,
+                                   s->st));
+    g_launches.fetch_add(1);
+    s->running = true;
+    return RMPB_OK;
+  });
+}
+
+extern "C" int rmpb_server_start(const rmpb_grid* g, const rmpb_bundle* b, const double params[7],
+                                 double max_range, double eps, double step_scale,
+                                 double idle_timeout_s, rmpb_server** out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = nullptr;
+  TRY(check_gb(g, b));
+  TRY(check_params(params));
+  if (!(idle_timeout_s > 0.0) || idle_timeout_s > 3600.0)
+    return fail(RMPB_ERR_INVALID, "idle_timeout_s must be in (0, 3600]");
+  DeviceGuard dg(g->device);
+  if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d", g->device);
+  std::unique_ptr<rmpb_server> s(new rmpb_server());
+  s->device = g->device; s->g = g; s->b = b;
+  s->pp = make_params(params, 0.0);
+  s->max_range = max_range; s->eps = eps; s->step_scale = step_scale;
+  s->idle_ns = (unsigned long long)(idle_timeout_s * 1e9);
+  choose_segments(1, b->n, &s->segs, &s->seg_rays);
+  CK(cudaStreamCreateWithFlags(&s->st, cudaStreamNonBlocking));
+  CK(cudaHostAlloc((void**)&s->mail, sizeof(ServerMail), cudaHostAllocMapped));
+  memset((void*)s->mail, 0, sizeof(ServerMail));
+  CK(cudaHostGetDevicePointer((void**)&s->d_mail, s->mail, 0));
+  CK(cudaMalloc((void**)&s->d_dev, sizeof(ServerDev)));
+  CK(cudaMalloc((void**)&s->d_partials, (size_t)s->segs * kAcc * sizeof(double)));
+  CK(cudaMalloc((void**)&s->d_tickets, sizeof(unsigned)));
+  CK(cudaMemset(s->d_tickets, 0, sizeof(unsigned)));
+  TRY(server_launch(s.get()));
+  *out = s.release();
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_server_eval(rmpb_server* s, const double x[3], const double v[3],
+                                double out_slot[13], double out_accel[3]) {
+  if (!s || !x || !v || !out_slot) return fail(RMPB_ERR_INVALID, "NULL argument");
+  volatile ServerMail* m = s->mail;
+  if (!s->running || m->exited) {  // idle timeout ended the loop: relaunch
+    DeviceGuard dg(s->device);
+    CK(cudaStreamSynchronize(s->st));
+    s->running = false;
+    TRY(server_launch(s));
+  }
+  for (int k = 0; k < 3; ++k) { m->x[k] = x[k]; m->v[k] = v[k]; }
+  const unsigned long long e = ++s->epoch;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  m->req = e;
+  // spin on the result epoch (the device writes it last, after the results)
+  auto t0 = std::chrono::steady_clock::now();
+  unsigned long long spins = 0;
+  while (m->done != e) {
+    if ((++spins & 0xffff) == 0) {
+      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
+        cudaError_t qe = cudaStreamQuery(s->st);
+        return fail(RMPB_ERR_CUDA, "server did not answer within 5 s (%s)",
+                    qe == cudaErrorNotReady ? "kernel still running" : cudaGetErrorString(qe));
+      }
+      if (m->exited) return fail(RMPB_ERR_CUDA, "server exited while a request was pending");
+    }
+  }
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  for (int k = 0; k < 13; ++k) out_slot[k] = m->slot[k];
+  if (out_accel)
+    for (int k = 0; k < 3; ++k) out_accel[k] = m->accel[k];
+  return RMPB_OK;
+}
+
+extern "C" int rmpb_server_stop(rmpb_server* s) {
+  if (!s) return RMPB_OK;
+  DeviceGuard dg(s->device);
+  s->mail->stop = 1;
+  std::atomic_thread_fence(std::memory_order_seq_cst);
+  cudaError_t e = cudaStreamSynchronize(s->st);
+  cudaStreamDestroy(s->st);
+  cudaFreeHost((void*)s->mail);
+  cudaFree(s->d_dev);
+  cudaFree(s->d_partials);
+  cudaFree(s->d_tickets);
+  delete s;
+  if (e != cudaSuccess) return fail(RMPB_ERR_CUDA, "server kernel: %s", cudaGetErrorString(e));
+  return RMPB_OK;
 }
 
 // ---------------------------------------------------------------------------

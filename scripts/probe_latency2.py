@@ -58,5 +58,8 @@ res["raw_ctypes_us_range10"] = med(raw)
 res["raw_ctypes_us_range0"] = med(lambda i: raw(i, 1e-6))
 res["fused_host_call_us"] = med(lambda i: b200.ray_policy_fused(grid.values, grid.origin, grid.resolution, states[i % 10].position, states[i % 10].velocity, bundle.directions, params.as_tuple(), 10.0, 0.05, 0.9))
 res["public_ray_policy_us"] = med(lambda i: P.ray_policy(states[i % 10], grid, bundle, params, 10.0))
+with P.LatencyServer(grid, bundle, params, 10.0) as srv:
+    res["server_policy_us"] = med(lambda i: srv.policy(states[i % 10]))
+    res["server_eval_us"] = med(lambda i: srv.evaluate(states[i % 10].position, states[i % 10].velocity))
 res["torch_sync_roundtrip_us"] = med(lambda i: (oslot.fill_(0.0), torch.cuda.synchronize()))
 print(json.dumps(res))
