@@ -126,8 +126,12 @@ def load(path: str | None = None):
                 "`python -c 'import __graft_entry__ as g; g.build()'` or "
                 "`make -C paper_2301_08068_b200/csrc` (there is no CPU fallback)")
         lib = ctypes.CDLL(p)
+        # experiment builds (RMPB_LIBRARY) may predate newer entry points
+        lenient = bool(os.environ.get("RMPB_LIBRARY"))
         for name, (res, args) in _SIGS.items():
-            fn = getattr(lib, name)
+            fn = getattr(lib, name, None) if lenient else getattr(lib, name)
+            if fn is None:
+                continue
             fn.restype = res
             fn.argtypes = args
         if lib.rmpb_api_version() != 1:

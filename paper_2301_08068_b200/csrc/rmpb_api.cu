@@ -832,13 +832,16 @@ static void apply_carveout(K* kern) {
 static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io, int64_t P,
                              const PolicyParams& pp, double max_range, double eps,
                              double step_scale, int segs, int seg_rays, RayOut ro,
-                             cudaStream_t st, int mode = RMPB_MODE_EXACT) {
+                             cudaStream_t st, int mode = RMPB_MODE_EXACT,
+                             const ExArgs* xa = nullptr) {
   Bundle bv = bundle_view(b);
   const long long units = (long long)P * segs;
   if (units >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many CTA units");
   // one ray per thread -> the lean kernel (nothing to refill); else lane refill
   const int64_t kopt = g_opt_kernel.load();
-  const bool v2 = kopt == 2 || (kopt == 0 && seg_rays > kBlock) || mode == RMPB_MODE_FAST;
+  // the K4 exchange epilogue lives in the lean kernel only
+  const bool v2 = !xa && (kopt == 2 || (kopt == 0 && seg_rays > kBlock) || mode == RMPB_MODE_FAST);
+  const ExArgs xv = xa ? *xa : ExArgs{nullptr, 0ull, 0};
   return with_grid(g, [&](auto acc) -> int {
     using G = decltype(acc);
     if (v2) {
@@ -847,9 +850,13 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
       apply_carveout(k_ray_policy2<G, true>);
       apply_carveout(k_ray_policy2<G, false>);
     }
-    if (!v2)
-      k_ray_policy<<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
-                                                       step_scale, segs, seg_rays, ro);
+    if (!v2 && xa)
+      k_ray_policy<G, true><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
+                                                                max_range, eps, step_scale, segs,
+                                                                seg_rays, ro, xv);
+    else if (!v2)
+      k_ray_policy<G><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
+                                                          step_scale, segs, seg_rays, ro, xv);
     else if (mode == RMPB_MODE_FAST && ro.step_total)
       k_ray_policy2<G, true, true><<<(unsigned)units, kBlock, 0, st>>>(
           acc, g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays, ro);
@@ -1347,12 +1354,10 @@ extern "C" int rmpb_ray_policy_range_exchange(const rmpb_grid* g, const rmpb_bun
   io.x = d_x; io.v = d_v; io.slot = d_slot; io.accel = d_accel;
   io.partials = (double*)ws->partials.p;
   io.tickets = (unsigned*)ws->tickets.p;
-  io.ex = peer->d_table;
-  io.ex_epoch = epoch;
-  io.ex_mode = mode;
+  const ExArgs xa{peer->d_table, (unsigned long long)epoch, mode};
   RayOut ro{};
   return launch_ray_policy(g, &sub, io, 1, make_params(params, 0.0), max_range, eps, step_scale,
-                           segs, seg_rays, ro, st);
+                           segs, seg_rays, ro, st, RMPB_MODE_EXACT, &xa);
 }
 
 extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double* d_slot,

@@ -62,11 +62,14 @@ __device__ __forceinline__ unsigned long long globaltimer_ns() {
 }
 
 // Fixed pairwise fold (rmpnav/_kernels/_pool.py:61-72: s[2k] + s[2k+1], odd
-// tail carried) of n <= 64 13-slots at `stride` doubles; one thread.
+// tail carried) of n <= MAXN 13-slots at `stride` doubles; one thread.
+// (The buffer is thread-local: keep MAXN small where it is inlined into the
+// trace kernels -- it sizes their stack frame.)
+template <int MAXN>
 __device__ inline void fold_slots(const double* slots, int n, int stride, bool bypass_l1,
                                   double out[13]) {
-  double buf[64 * 13];
-  int m = n < 64 ? n : 64;
+  double buf[MAXN * 13];
+  int m = n < MAXN ? n : MAXN;
   for (int i = 0; i < m; ++i)
     for (int j = 0; j < 13; ++j)
       buf[i * 13 + j] = bypass_l1 ? __ldcg(slots + (size_t)i * stride + j) : slots[(size_t)i * stride + j];
@@ -81,8 +84,36 @@ __device__ inline void fold_slots(const double* slots, int n, int stride, bool b
   for (int j = 0; j < 13; ++j) out[j] = buf[j];
 }
 
+// The same fold for n <= kMaxPeers (8) slots held in registers: every index
+// is a compile-time constant (no local-memory buffer in the trace kernels).
+__device__ __forceinline__ double fold8(const double* p, int n, int stride) {
+  double v[kMaxPeers];
+#pragma unroll
+  for (int i = 0; i < kMaxPeers; ++i) v[i] = i < n ? __ldcg(p + (size_t)i * stride) : 0.0;
+  int m = n;
+#pragma unroll
+  for (int level = 0; level < 3; ++level) {  // 8 -> 4 -> 2 -> 1
+    const int half = m >> 1, odd = m & 1;
+    double last = 0.0;
+#pragma unroll
+    for (int i = 0; i < kMaxPeers; ++i)
+      if (i == m - 1) last = v[i];
+#pragma unroll
+    for (int k = 0; k < kMaxPeers / 2; ++k)
+      v[k] = k < half ? v[2 * k] + v[2 * k + 1] : (k == half && odd ? last : v[k]);
+    m = half + odd;
+  }
+  return v[0];
+}
+
+struct ExArgs {  // per-call exchange arguments (kernel parameter of the lean kernel)
+  const PeerEx* ex;
+  unsigned long long epoch;
+  int mode;  // EX_POST | EX_WAIT (split only for one-GPU tests)
+};
+
 struct PoseIO;
-__device__ void exchange_emit(const Acc& s, const PoseIO& io);
+__device__ void exchange_emit(const Acc& s, const PoseIO& io, const ExArgs& xa);
 
 struct PoseIO {
   const double* __restrict__ x;   // [P][3] positions
@@ -94,9 +125,6 @@ struct PoseIO {
   double* __restrict__ seg_out;   // [P*segs][10] raw segment partials (ray-split), or null
   double x0[3], v0[3];            // single pose by value when x / v are null
   const int* __restrict__ active; // [P] skip poses whose flag is 0 (rollouts), or null
-  const PeerEx* ex;               // fused peer exchange (K4; single pose), or null
-  unsigned long long ex_epoch;
-  int ex_mode;                    // EX_POST | EX_WAIT (split only for one-GPU tests)
   __device__ __forceinline__ void pose(int p, double& a, double& b, double& c) const {
     if (x) { a = x[3 * p]; b = x[3 * p + 1]; c = x[3 * p + 2]; } else { a = x0[0]; b = x0[1]; c = x0[2]; }
   }
@@ -135,16 +163,19 @@ __device__ __forceinline__ void acc_to_arr(const Acc& a, double* o) {
 
 // Finish a unit: reduce the CTA, then either resolve the pose or publish a
 // partial and let the last CTA of the pose fold + resolve.
-// Returns true in the one thread that wrote the pose's final slot.
+// Returns true in the one thread that wrote the pose's final slot.  EX: the
+// K4 exchange epilogue is compiled in (only the lean kernel serves it; the
+// throughput kernel stays free of its code and registers).
+template <bool EX = false>
 __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose, int seg,
-                                            int segs) {
+                                            int segs, const ExArgs* xa = nullptr) {
   __shared__ double sm[kWarps * kAcc];
   __shared__ int s_last;
   block_reduce(acc, sm);
   if (io.seg_out && threadIdx.x == 0) acc_to_arr(acc, io.seg_out + (size_t)(pose * segs + seg) * kAcc);
   if (segs == 1) {
     if (threadIdx.x == 0 && io.slot) {
-      if (io.ex) exchange_emit(acc, io);
+      if (EX) exchange_emit(acc, io, *xa);
       else write_slot(acc, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
       return true;
     }
@@ -177,7 +208,7 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
   block_reduce(f, sm);
   if (threadIdx.x == 0) {
     io.tickets[pose] = 0u;  // self-reset: graph replays / next call start clean
-    if (io.ex) exchange_emit(f, io);
+    if (EX) exchange_emit(f, io, *xa);
     else write_slot(f, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
     return true;
   }
@@ -185,10 +216,10 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
 }
 
 // The K4 epilogue (one thread of the pose's final CTA); see PeerEx.
-__device__ void exchange_emit(const Acc& s, const PoseIO& io) {
-  const PeerEx& ex = *io.ex;
-  const int W = ex.world, par = (int)(io.ex_epoch & 1ull);
-  if (io.ex_mode & EX_POST) {
+__device__ void exchange_emit(const Acc& s, const PoseIO& io, const ExArgs& xa) {
+  const PeerEx& ex = *xa.ex;
+  const int W = ex.world, par = (int)(xa.epoch & 1ull);
+  if (xa.mode & EX_POST) {
     const double rec[13] = {s.a00, s.a01, s.a02, s.a01, s.a11, s.a12, s.a02, s.a12, s.a22,
                             s.b0,  s.b1,  s.b2,  (double)s.cnt};
     for (int r = 0; r < W; ++r) {
@@ -196,21 +227,21 @@ __device__ void exchange_emit(const Acc& s, const PoseIO& io) {
       for (int j = 0; j < 13; ++j) __stcg(dst + j, rec[j]);
     }
     __threadfence_system();
-    for (int r = 0; r < W; ++r) st_release_sys(ex.flags[r] + (size_t)par * W + ex.rank, io.ex_epoch);
+    for (int r = 0; r < W; ++r) st_release_sys(ex.flags[r] + (size_t)par * W + ex.rank, xa.epoch);
   }
-  if (!(io.ex_mode & EX_WAIT)) return;
+  if (!(xa.mode & EX_WAIT)) return;
   const unsigned long long* fl = ex.flags[ex.rank] + (size_t)par * W;
   const unsigned long long t0 = globaltimer_ns();
   bool ok = true;
   for (int r = 0; r < W && ok; ++r) {
-    while (ld_acquire_sys(fl + r) != io.ex_epoch) {
+    while (ld_acquire_sys(fl + r) != xa.epoch) {
       if (globaltimer_ns() - t0 > 10000000000ull) { ok = false; break; }  // 10 s: a peer is gone
       __nanosleep(32);
     }
   }
   double out[13];
   if (ok) {
-    fold_slots(ex.slots[ex.rank] + (size_t)par * W * kMbox, W, kMbox, true, out);
+    for (int j = 0; j < 13; ++j) out[j] = fold8(ex.slots[ex.rank] + (size_t)par * W * kMbox + j, W, kMbox);
   } else {
     atomicExch(ex.err, 1u);
     for (int j = 0; j < 13; ++j) out[j] = CUDART_NAN;
@@ -229,26 +260,30 @@ __device__ void exchange_emit(const Acc& s, const PoseIO& io) {
 // where the longest ray's dependent chain is the whole story.
 // grid: P * segs CTAs of kBlock threads; segment = seg_rays consecutive
 // stored rays of the bundle.
-template <class G>
+template <class G, bool EX = false>
 __device__ __forceinline__ bool lean_unit(const G& grid, const GridGeom& g, const Bundle& b,
                                           const PoseIO& io, const PolicyParams& p,
                                           double max_range, double eps, double step_scale,
-                                          int segs, int seg_rays, const RayOut& ro, int unit);
+                                          int segs, int seg_rays, const RayOut& ro, int unit,
+                                          const ExArgs* xa = nullptr);
 
-template <class G>
+// EX: with the K4 peer-exchange epilogue (config C5 ray split).
+template <class G, bool EX = false>
 __global__ void __launch_bounds__(kBlock)
 k_ray_policy(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
-             double eps, double step_scale, int segs, int seg_rays, RayOut ro) {
-  lean_unit(grid, g, b, io, p, max_range, eps, step_scale, segs, seg_rays, ro, (int)blockIdx.x);
+             double eps, double step_scale, int segs, int seg_rays, RayOut ro, ExArgs xa) {
+  lean_unit<G, EX>(grid, g, b, io, p, max_range, eps, step_scale, segs, seg_rays, ro,
+                   (int)blockIdx.x, &xa);
 }
 
 // One CTA's unit of the lean kernel; true in the thread that wrote the
 // pose's final slot.
-template <class G>
+template <class G, bool EX>
 __device__ __forceinline__ bool lean_unit(const G& grid, const GridGeom& g, const Bundle& b,
                                           const PoseIO& io, const PolicyParams& p,
                                           double max_range, double eps, double step_scale,
-                                          int segs, int seg_rays, const RayOut& ro, int unit) {
+                                          int segs, int seg_rays, const RayOut& ro, int unit,
+                                          const ExArgs* xa) {
   const int pose = unit / segs, seg = unit - pose * segs;
   double sx, sy, sz, vx, vy, vz;
   io.pose(pose, sx, sy, sz);
@@ -276,7 +311,7 @@ __device__ __forceinline__ bool lean_unit(const G& grid, const GridGeom& g, cons
     int s = warp_sum_i(my_steps);
     if ((threadIdx.x & 31) == 0) atomicAdd(ro.step_total, (unsigned long long)s);
   }
-  return finish_unit(acc, io, pose, seg, segs);
+  return finish_unit<EX>(acc, io, pose, seg, segs, xa);
 }
 
 // ---------------------------------------------------------------------------
@@ -1165,7 +1200,7 @@ __global__ void k_fold_resolve(const double* __restrict__ slots, int n, double* 
   if (threadIdx.x != 0 || blockIdx.x != 0) return;
   // n is small (number of GPUs): fold in a local buffer.
   double buf[13];
-  fold_slots(slots, n, 13, false, buf);
+  fold_slots<64>(slots, n, 13, false, buf);
   for (int j = 0; j < 13; ++j) out_slot[j] = buf[j];
   if (out_accel) {
     double m9[9], f[3];

@@ -29,10 +29,19 @@ from .rays import DEFAULT_MAX_RANGE, RayBundle
 
 class LatencyServer:
     def __init__(self, field: EsdfGrid, bundle: RayBundle, p: ObstacleParams,
-                 max_range: float = DEFAULT_MAX_RANGE, idle_timeout_s: float = 10.0):
+                 max_range: float = DEFAULT_MAX_RANGE, idle_timeout_s: float = 10.0,
+                 storage: int | None = None, layout: int | None = None):
+        """``storage`` / ``layout`` (librmpb STORE_* / LAYOUT_*) give the
+        server its own device copy of the map in that layout; default: the
+        map shared with ``ray_policy``."""
         if not isinstance(field, EsdfGrid):
             raise TypeError("LatencyServer needs an EsdfGrid")
-        self._grid = b200.device_grid(field.values, field.origin, field.resolution)
+        if storage is None and layout is None:
+            self._grid = b200.device_grid(field.values, field.origin, field.resolution)
+        else:
+            self._grid = b200.DeviceGrid(field.values, field.origin, field.resolution,
+                                         storage=L.STORE_AUTO if storage is None else storage,
+                                         layout=L.LAYOUT_AUTO if layout is None else layout)
         self._bundle = b200.device_bundle(getattr(bundle, "directions", bundle))
         self._params = np.ascontiguousarray(np.asarray(p.as_tuple(), dtype=np.float64))
         h = ctypes.c_void_p()
