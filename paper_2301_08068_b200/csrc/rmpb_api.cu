@@ -37,7 +37,8 @@ static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int64_t> g_opt_seg_rays{0};
 static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread per pass, 2 lane refill
 static std::atomic<int64_t> g_opt_carveout{-1};
-static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (v3 warp units), 1, 2, 3
+static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (= 3), 1, 2 (v1/v2), 3 (v3 warp units), 4/5 (v4 TMA-fed, 2 stage sizes)
+static std::atomic<int64_t> g_opt_lidar_tma_warps{48000};  // v4: target warp units per launch
 static std::atomic<int64_t> g_opt_lidar_warps{76000};  // v3: target warp units per launch  // shared-memory carveout % for the trace kernel
 
 static int fail(int code, const char* fmt, ...) {
@@ -296,8 +297,13 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
     g_opt_lidar_warps.store(value);
     return RMPB_OK;
   }
+  if (!strcmp(name, "lidar_tma_warps")) {
+    if (value < 1) return fail(RMPB_ERR_INVALID, "lidar_tma_warps must be >= 1");
+    g_opt_lidar_tma_warps.store(value);
+    return RMPB_OK;
+  }
   if (!strcmp(name, "lidar_kernel")) {
-    if (value < 0 || value > 3) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..3");
+    if (value < 0 || value > 5) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..5");
     g_opt_lidar_kernel.store(value);
     return RMPB_OK;
   }
@@ -1413,10 +1419,62 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
   return RMPB_OK;
 }
 
+// K2 v4 / K2b v2: the TMA-fed warp-unit kernel.  Longer warp units than v3
+// (the stages keep bytes in flight, so fewer, longer-lived warps suffice):
+// target g_opt_lidar_tma_warps units per launch.
+template <class Src, int NST, int GPS>
+static int launch_lidar_tma(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
+                            const PolicyParams& pp, double* d_slot, double* d_accel,
+                            Workspace* ws, cudaStream_t st) {
+  const int64_t target = g_opt_lidar_tma_warps.load();
+  int64_t wps = (target + S_ - 1) / S_;
+  wps = std::min<int64_t>(wps, 1024);
+  wps = std::min<int64_t>(wps, (n + 127) / 128);
+  wps = std::max<int64_t>(wps, 1);
+  const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
+  wps = (n + seg - 1) / seg;
+  const long long nunits = (long long)S_ * wps;
+  if (wps > 1) {
+    TRY(ws->partials.ensure((size_t)nunits * kAcc * sizeof(double)));
+    TRY(ws->ensure_tickets((size_t)S_));
+  }
+  PoseIO io{};
+  io.x = nullptr; io.v = d_v;
+  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
+  io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  const long long blocks = (nunits + kWarps - 1) / kWarps;
+  if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
+  const size_t smem = (size_t)kWarps * (NST * (Src::kStage + sizeof(unsigned long long)) +
+                                        sizeof(LidarTmaSmem));
+  static std::once_flag once[64];
+  int dev = 0;
+  CK(cudaGetDevice(&dev));
+  std::call_once(once[dev & 63], [&] {
+    cudaFuncSetAttribute(k_lidar_tma<Src, NST, GPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+  });
+  k_lidar_tma<Src, NST, GPS><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps,
+                                                                      (int)seg, nunits);
+  CKL();
+  return RMPB_OK;
+}
+
 static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
                         const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                         cudaStream_t st) {
   const int64_t kopt = g_opt_lidar_kernel.load();
+  if (kopt == 4 || kopt == 5) {
+    if (kopt == 5) {
+      LatticeTma<4> src{};
+      src.sc = sc;
+      return launch_lidar_tma<LatticeTma<4>, 2, 4>(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+    }
+    LatticeTma<2> src{};
+    src.sc = sc;
+    return launch_lidar_tma<LatticeTma<2>, 2, 2>(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+  }
   if (kopt == 0 || kopt == 3) {
     LatticeSrc src{};
     src.sc = sc;
@@ -1532,6 +1590,16 @@ static int points_launch(PointsIO pt, int64_t S_, const double* d_v, double v0[3
                          const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                          cudaStream_t st) {
   const int64_t kopt = g_opt_lidar_kernel.load();
+  if (kopt == 4 || kopt == 5) {
+    if (kopt == 5) {
+      PointTma<4> src{};
+      src.pt = pt;
+      return launch_lidar_tma<PointTma<4>, 2, 4>(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+    }
+    PointTma<2> src{};
+    src.pt = pt;
+    return launch_lidar_tma<PointTma<2>, 2, 2>(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+  }
   if (kopt == 0 || kopt == 3) {
     PointSrc src{};
     src.pt = pt;

@@ -1125,6 +1125,290 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
   }
 }
 
+// K2 v4 / K2b v2 (option lidar_kernel = 4 / 5; measured, NOT the default):
+// the warp-unit kernel fed by TMA bulk copies.  v3 keeps one 128-beam group
+// of loads in flight per warp and ncu attributes ~40 % of its stall samples
+// to that load; here lane 0 of each warp keeps NST stages of GPS groups in
+// flight with cp.async.bulk.shared::cluster.global (one bulk copy per array
+// per stage, completion counted on a per-stage mbarrier), so bytes in flight
+// no longer depend on warps or registers.  Lanes read their beams from
+// shared memory; stages 1 / 2 and the fold are those of k_lidar_warp, with
+// the per-lane running sums in registers (frees shared memory for stages).
+// Ragged tails and rows that are not 16-B aligned take the direct loads.
+// Measured on C3 (profiles/README.md): 0.54-0.57 ms vs v3's 0.50 ms -- with
+// the stream hidden, the warps stall on the stage-1 direction gather and the
+// fp64 policy chains instead, and the stages cost occupancy (24 vs 32 warps
+// per SM): the kernel is bound by per-warp dependent latency, not the stream.
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+  return (unsigned)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
+  asm volatile(
+      "{\n .reg .pred p;\n"
+      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      " @!p bra W;\n}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
+}
+// global -> shared bulk copy (16-B aligned, size a multiple of 16),
+// completion signalled on mbarrier `b`; streaming data: L2 evict-first.
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
+                                         unsigned long long* b) {
+  asm volatile(
+      "{\n .reg .b64 pol;\n"
+      " createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
+      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
+      " [%0], [%1], %2, [%3], pol;\n}" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
+      : "memory");
+}
+
+// Beam sources of the TMA kernel.  Stage layout per 128-beam group:
+// lattice: 1024 B ranges | 128 B validity; points: 1536 B xyz.
+template <int GPS>
+struct LatticeTma : LatticeSrc {
+  static constexpr unsigned kStage = 1152 * GPS;  // GPS x 1024 B ranges | GPS x 128 B validity
+  bool tma;  // rows 16-B aligned: bulk copies allowed
+  __device__ __forceinline__ void bind_tma(int scan) {
+    bind(scan);
+    tma = ((reinterpret_cast<uintptr_t>(rg) & 15) == 0) &&
+          (!vl || (reinterpret_cast<uintptr_t>(vl) & 15) == 0);
+  }
+  __device__ __forceinline__ void issue(unsigned char* st, int base, unsigned long long* b) const {
+    mbar_expect_tx(b, vl ? 1152u * GPS : 1024u * GPS);
+    bulk_g2s(st, rg + base, 1024u * GPS, b);
+    if (vl) bulk_g2s(st + 1024 * GPS, vl + base, 128u * GPS, b);
+  }
+  // group j of the stage; lane's beams {2l, 2l+1, 64+2l, 65+2l}
+  // (conflict-free 16-B reads); their in-group indices through `idx`
+  __device__ __forceinline__ void read4(const unsigned char* st, int j, int lane, double (&o)[4],
+                                        int (&idx)[4]) const {
+    const unsigned char* r = st + 1024 * j;
+    const double2 x0 = *reinterpret_cast<const double2*>(r + 16 * lane);
+    const double2 x1 = *reinterpret_cast<const double2*>(r + 512 + 16 * lane);
+    o[0] = x0.x; o[1] = x0.y; o[2] = x1.x; o[3] = x1.y;
+    idx[0] = 2 * lane; idx[1] = 2 * lane + 1; idx[2] = 64 + 2 * lane; idx[3] = 65 + 2 * lane;
+    if (vl) {
+      const unsigned char* m = st + 1024 * GPS + 128 * j;
+      const unsigned short m0 = *reinterpret_cast<const unsigned short*>(m + 2 * lane);
+      const unsigned short m1 = *reinterpret_cast<const unsigned short*>(m + 64 + 2 * lane);
+      if (!(m0 & 0xffu)) o[0] = CUDART_INF;
+      if (!(m0 >> 8)) o[1] = CUDART_INF;
+      if (!(m1 & 0xffu)) o[2] = CUDART_INF;
+      if (!(m1 >> 8)) o[3] = CUDART_INF;
+    }
+  }
+};
+
+template <int GPS>
+struct PointTma : PointSrc {
+  static constexpr unsigned kStage = 1536 * GPS;
+  bool tma;
+  __device__ __forceinline__ void bind_tma(int scan) {
+    bind(scan);
+    tma = vec;
+  }
+  __device__ __forceinline__ void issue(unsigned char* st, int base, unsigned long long* b) const {
+    mbar_expect_tx(b, 1536u * GPS);
+    bulk_g2s(st, P + 3 * (size_t)base, 1536u * GPS, b);
+  }
+  // group j of the stage; lane's points 4l..4l+3 (48-B stride: conflict-free
+  // 16-B reads)
+  __device__ __forceinline__ void read4(const unsigned char* st, int j, int lane, double (&o)[4],
+                                        int (&idx)[4]) const {
+    const float4* q = reinterpret_cast<const float4*>(st + 1536 * j + 48 * lane);
+    const float4 a = q[0], b = q[1], c = q[2];
+    o[0] = range(a.x, a.y, a.z); o[1] = range(a.w, b.x, b.y);
+    o[2] = range(b.z, b.w, c.x); o[3] = range(c.y, c.z, c.w);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) idx[k] = 4 * lane + k;
+  }
+};
+
+struct LidarTmaSmem {
+  double R[9], v[3];
+  double q1d[kRing1];
+  int q1i[kRing1];
+  double q2d[kRing2], q2x[kRing2], q2y[kRing2], q2z[kRing2];
+};
+
+template <class Src, int NST, int GPS>
+__global__ void __launch_bounds__(kBlock, 3)
+k_lidar_tma(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits) {
+  extern __shared__ __align__(128) unsigned char lidar_tsm[];
+  // [kWarps][NST][kStage] stages | [kWarps][NST] mbarriers | [kWarps] LidarTmaSmem
+  unsigned char* stages = lidar_tsm;
+  unsigned long long* bars =
+      reinterpret_cast<unsigned long long*>(lidar_tsm + (size_t)kWarps * NST * Src::kStage);
+  LidarTmaSmem* smw = reinterpret_cast<LidarTmaSmem*>(bars + kWarps * NST);
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
+  const long long unit = (long long)blockIdx.x * kWarps + warp;
+  if (unit >= nunits) return;
+  const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
+  LidarTmaSmem& w = smw[warp];
+  unsigned char* st0 = stages + (size_t)warp * NST * Src::kStage;
+  unsigned long long* bar = bars + warp * NST;
+  const double* Rall = src.rot();
+  const bool rot = Rall != nullptr;
+  if (rot && lane < 9) w.R[lane] = Rall[9 * scan + lane];
+  if (lane == 0) io.vel(scan, w.v[0], w.v[1], w.v[2]);
+  src.bind_tma(scan);
+  const int begin = wu * seg;
+  const int end = min(begin + seg, src.count());
+  // full stages (GPS groups of 128 beams) go through shared memory; the
+  // remaining groups are loaded directly
+  constexpr int SB = 128 * GPS;  // beams per stage
+  const int nstages = src.tma ? (end - begin) / SB : 0;
+  const int nbulk = nstages * GPS;  // groups served from the stages
+  if (lane == 0 && nstages > 0) {
+    for (int s = 0; s < NST; ++s) mbar_init(bar + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int s = 0; s < NST && s < nstages; ++s) src.issue(st0 + s * Src::kStage, begin + SB * s, bar + s);
+  }
+  double acc[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) acc[k] = 0.0;
+  int h1 = 0, q1n = 0, h2 = 0, q2n = 0, cnt = 0;
+  int base = begin, g = 0;
+  __syncwarp();
+  while (true) {
+    const bool draining = base >= end;
+    if (!draining) {
+      double cur[4];
+      int idx[4];
+      const int sg = g / GPS, j = g - sg * GPS;  // stage sequence number, group in stage
+      if (g < nbulk) {
+        if (j == 0) mbar_wait(bar + sg % NST, (unsigned)((sg / NST) & 1));
+        src.read4(st0 + (sg % NST) * Src::kStage, j, lane, cur, idx);
+      } else {
+        src.load4(base + 4 * lane, end, cur);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) idx[j] = 4 * lane + j;
+      }
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const double d = cur[j];
+        const bool counted = !(d != d || d == CUDART_INF || d < p.min_range);
+        cnt += counted;
+        const bool enq = counted && d < p.radius;
+        const unsigned em = __ballot_sync(FULL, enq);
+        if (enq) {
+          int pos = h1 + q1n + __popc(em & lt);
+          if (pos >= kRing1) pos -= kRing1;
+          w.q1d[pos] = d;
+          w.q1i[pos] = base + idx[j];
+        }
+        q1n += __popc(em);
+      }
+      // every lane consumed the stage (ballots above): refill it
+      if (j == GPS - 1 && g < nbulk) {
+        __syncwarp();
+        if (lane == 0 && sg + NST < nstages)
+          src.issue(st0 + (sg % NST) * Src::kStage, begin + SB * (sg + NST), bar + sg % NST);
+      }
+      base += 128;
+      ++g;
+    }
+    __syncwarp();
+    // ---- stage 1 (one call site): direction gather, rotation, closing test
+    while (q1n >= 32 || (draining && (q1n > 0 || q2n > 0))) {
+      const int take = min(q1n, 32);
+      bool keep = false;
+      double d = 0, wx = 0, wy = 0, wz = 0;
+      if (lane < take) {
+        int e = h1 + lane;
+        if (e >= kRing1) e -= kRing1;
+        const int i = w.q1i[e];
+        d = w.q1d[e];
+        double ex, ey, ez;
+        src.dir(i, d, ex, ey, ez);
+        wx = ex; wy = ey; wz = ez;
+        if (rot) {  // directions @ orientation.T  (rays.py:172-173)
+          wx = ex * w.R[0] + ey * w.R[1] + ez * w.R[2];
+          wy = ex * w.R[3] + ey * w.R[4] + ez * w.R[5];
+          wz = ex * w.R[6] + ey * w.R[7] + ez * w.R[8];
+        }
+        keep = wx * w.v[0] + wy * w.v[1] + wz * w.v[2] > 0.0;  // policy_accumulate's test
+      }
+      h1 += take;
+      if (h1 >= kRing1) h1 -= kRing1;
+      q1n -= take;
+      const unsigned km = __ballot_sync(FULL, keep);
+      if (keep) {
+        const int pos = (h2 + q2n + __popc(km & lt)) & (kRing2 - 1);
+        w.q2d[pos] = d; w.q2x[pos] = wx; w.q2y[pos] = wy; w.q2z[pos] = wz;
+      }
+      q2n += __popc(km);
+      __syncwarp();
+      // ---- stage 2 (one call site): transcendental policy, 32 at a time
+      const bool last = draining && q1n == 0;
+      if (q2n >= 32 || (last && q2n > 0)) {
+        const int t2 = min(q2n, 32);
+        Acc a;
+        a.zero();
+        if (lane < t2) {
+          const int e = (h2 + lane) & (kRing2 - 1);
+          policy_accumulate(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2], p);
+        }
+        h2 = (h2 + t2) & (kRing2 - 1);
+        q2n -= t2;
+        if (lane < t2) {  // lane-private running sums (registers)
+          acc[0] += a.a00; acc[1] += a.a01; acc[2] += a.a02;
+          acc[3] += a.a11; acc[4] += a.a12; acc[5] += a.a22;
+          acc[6] += a.b0; acc[7] += a.b1; acc[8] += a.b2;
+        }
+        __syncwarp();
+      }
+    }
+    if (draining) break;
+  }
+  __syncwarp();
+  cnt = warp_sum_i(cnt);
+  double ws[9];
+#pragma unroll
+  for (int k = 0; k < 9; ++k) ws[k] = warp_sum(acc[k]);
+  Acc a;
+  a.a00 = ws[0]; a.a01 = ws[1]; a.a02 = ws[2]; a.a11 = ws[3]; a.a12 = ws[4];
+  a.a22 = ws[5]; a.b0 = ws[6]; a.b1 = ws[7]; a.b2 = ws[8]; a.cnt = cnt;
+  if (wps == 1) {
+    if (lane == 0 && io.slot)
+      write_slot(a, io.slot + (size_t)scan * 13, io.accel ? io.accel + (size_t)scan * 3 : nullptr);
+    return;
+  }
+  unsigned prev = 0;
+  if (lane == 0) {
+    acc_to_arr(a, io.partials + ((size_t)scan * wps + wu) * kAcc);
+    __threadfence();
+    prev = atomicAdd(io.tickets + scan, 1u);
+  }
+  prev = __shfl_sync(FULL, prev, 0);
+  if (prev != (unsigned)(wps - 1)) return;
+  __threadfence();
+  double f[kAcc];
+#pragma unroll
+  for (int k = 0; k < kAcc; ++k) f[k] = 0.0;
+  const double* pb = io.partials + (size_t)scan * wps * kAcc;
+  for (int j = lane; j < wps; j += 32) {
+#pragma unroll
+    for (int k = 0; k < kAcc; ++k) f[k] += __ldcg(pb + (size_t)j * kAcc + k);
+  }
+#pragma unroll
+  for (int k = 0; k < kAcc; ++k) f[k] = warp_sum(f[k]);
+  if (lane == 0) {
+    Acc t;
+    t.a00 = f[0]; t.a01 = f[1]; t.a02 = f[2]; t.a11 = f[3]; t.a12 = f[4]; t.a22 = f[5];
+    t.b0 = f[6]; t.b1 = f[7]; t.b2 = f[8]; t.cnt = (int)f[9];
+    if (io.slot)
+      write_slot(t, io.slot + (size_t)scan * 13, io.accel ? io.accel + (size_t)scan * 3 : nullptr);
+    io.tickets[scan] = 0u;  // self-reset
+  }
+}
+
 // K2b v1: one point per thread per pass (kept as a measured alternative,
 // option lidar_kernel = 1 or 2).
 __global__ void __launch_bounds__(kBlock)

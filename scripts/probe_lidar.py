@@ -15,6 +15,9 @@ from paper_2301_08068_b200.rays import scan_pattern  # noqa: E402
 scene = synth.c1_scene()
 states = synth.bench_states(scene, count=10, seed=123, distance=synth.host_box_distance(scene))
 scans = synth.lidar_scans(scene, states, 128, 1024, 20.0)
+_r = np.stack([s_.ranges for s_ in scans]); _ok = np.stack([s_.valid for s_ in scans])
+print("valid frac", _ok.mean(), "in-radius frac", (_ok & (_r < 1.3) & (_r >= 0.3)).mean(),
+      file=sys.stderr)
 S = 1024
 dirs = torch.from_numpy(np.ascontiguousarray(scan_pattern(128, 1024)).copy()).cuda()
 rg = torch.from_numpy(np.stack([scans[i % 10].ranges for i in range(S)])).cuda()
@@ -29,7 +32,7 @@ for arg in sys.argv[1:] or ["2", "3"]:
     k = int(k)
     _lib.call("rmpb_set_option", b"lidar_kernel", k)
     if wt:
-        _lib.call("rmpb_set_option", b"lidar_warps", int(wt))
+        _lib.call("rmpb_set_option", b"lidar_tma_warps" if k >= 4 else b"lidar_warps", int(wt))
     k = arg
     s, a = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
     torch.cuda.synchronize()
@@ -55,7 +58,7 @@ from paper_2301_08068_b200.device import lidar_points_batch_device  # noqa: E402
 
 pts = torch.where(vl.bool()[:, :, None], dirs[None] * rg[:, :, None], 0.0).float().contiguous()
 pts = torch.nan_to_num(pts, nan=0.0, posinf=0.0, neginf=0.0)
-for k in (1, 3):
+for k in [int(a) for a in os.environ.get("POINT_KERNELS", "1,3,4,5").split(",")]:
     _lib.call("rmpb_set_option", b"lidar_kernel", k)
     lidar_points_batch_device(pts, R, v, LIDAR, 0.3)
     ts = []

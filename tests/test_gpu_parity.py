@@ -618,10 +618,16 @@ def test_lidar_points_batch_device(be, oracle, c1):
         assert rel_err(accs[k], acc_r) <= 1e-5
 
 
-@pytest.mark.parametrize("n,S", [(131072, 1), (1000, 5), (131, 3), (97, 2), (4096, 40)])
+# 1: per-thread, 2: CTA streaming, 3: warp units, 4 / 5: TMA-fed warp units
+# (two pipeline depths); 14: variant 4 with long warp units (3 per launch:
+# many groups per warp, so the stage ring wraps and the mbarrier parity flips)
+LIDAR_VARIANTS = (1, 2, 3, 4, 5, 14)
+LIDAR_VARIANTS_PTS = (1, 3, 4, 5, 14)
+
+
+@pytest.mark.parametrize("n,S", [(131072, 1), (1000, 5), (131, 3), (97, 2), (4096, 40), (8192, 3)])
 def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
-    """All LiDAR kernel variants (1: per-thread, 2: CTA streaming, 3: warp
-    units) vs the oracle on ragged beam counts, odd rows (16-B misaligned
+    """All LiDAR kernel variants (LIDAR_VARIANTS) vs the oracle on ragged beam counts, odd rows (16-B misaligned
     range rows / 4-B misaligned validity rows -> scalar path), with and
     without rotation / validity; variant 3 with the default warp targets
     also exercises the multi-warp fold (S = 1: 512 warp partials)."""
@@ -652,15 +658,16 @@ def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
                 d_R = torch.from_numpy(Rs.reshape(S, 9).copy()).cuda() if use_R else None
                 d_vl = torch.from_numpy(valid.astype(np.uint8)).cuda() if use_valid else None
                 outs = {}
-                for k in (1, 2, 3):
-                    _lib.call("rmpb_set_option", b"lidar_kernel", k)
+                for k in LIDAR_VARIANTS:
+                    _lib.call("rmpb_set_option", b"lidar_kernel", k % 10)
+                    _lib.call("rmpb_set_option", b"lidar_tma_warps", 3 if k >= 10 else 48000)
                     sl, ac = lidar_policy_batch_device(d_dirs, d_R, d_rg, d_vl, d_v, LIDAR, 0.3)
                     outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
                 for s in range(S):
                     wd = dirs @ Rs[s].T if use_R else dirs
                     vv = valid[s] if use_valid else np.ones(n, bool)
                     slot_r, acc_r = oracle.lidar_policy(wd, ranges[s], vv, v[s], LIDAR, 0.3)
-                    for k in (1, 2, 3):
+                    for k in LIDAR_VARIANTS:
                         sl, ac = outs[k]
                         assert sl[s][12] == slot_r[12], (k, s)
                         assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
@@ -668,9 +675,10 @@ def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
                             assert rel_err(ac[s], acc_r) <= ACC_TOL, (k, s)
     finally:
         _lib.call("rmpb_set_option", b"lidar_kernel", 0)
+        _lib.call("rmpb_set_option", b"lidar_tma_warps", 48000)
 
 
-@pytest.mark.parametrize("n,S", [(131072, 1), (1001, 4), (131, 3)])
+@pytest.mark.parametrize("n,S", [(131072, 1), (1001, 4), (131, 3), (4096, 6)])
 def test_lidar_points_kernels_ragged(be, oracle, n, S):
     """Raw-point kernels (1: per-thread, 3: warp units) vs the oracle on
     ragged / misaligned rows (12-B points: odd n -> scalar path), zero and
@@ -690,8 +698,9 @@ def test_lidar_points_kernels_ragged(be, oracle, n, S):
         for use_R in (True, False):
             d_R = torch.from_numpy(Rs.reshape(S, 9).copy()).cuda() if use_R else None
             outs = {}
-            for k in (1, 3):
-                _lib.call("rmpb_set_option", b"lidar_kernel", k)
+            for k in LIDAR_VARIANTS_PTS:
+                _lib.call("rmpb_set_option", b"lidar_kernel", k % 10)
+                _lib.call("rmpb_set_option", b"lidar_tma_warps", 3 if k >= 10 else 48000)
                 sl, ac = lidar_points_batch_device(torch.from_numpy(pts).cuda(), d_R,
                                                    torch.from_numpy(v).cuda(), LIDAR, 0.3)
                 outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
@@ -703,12 +712,13 @@ def test_lidar_points_kernels_ragged(be, oracle, n, S):
                     dd = np.where(ok[:, None], p64 / r[:, None], 0.0)
                 wd = dd @ Rs[s].T if use_R else dd
                 slot_r, acc_r = oracle.lidar_policy(wd, r, ok, v[s], LIDAR, 0.3)
-                for k in (1, 3):
+                for k in LIDAR_VARIANTS_PTS:
                     sl, ac = outs[k]
                     assert sl[s][12] == slot_r[12], (k, s)
                     assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
     finally:
         _lib.call("rmpb_set_option", b"lidar_kernel", 0)
+        _lib.call("rmpb_set_option", b"lidar_tma_warps", 48000)
 
 
 # --- host fast path: repeated calls with the same arrays -----------------------
