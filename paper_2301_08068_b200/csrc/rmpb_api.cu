@@ -37,6 +37,7 @@ static std::atomic<uint64_t> g_launches{0};
 static std::atomic<int64_t> g_opt_seg_rays{0};
 static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread per pass, 2 lane refill
 static std::atomic<int64_t> g_opt_carveout{-1};
+static std::atomic<int64_t> g_opt_l2_window{1};  // map access-policy window on trace launches
 static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (= 3), 1, 2 (v1/v2), 3 (v3 warp units), 4/5 (v4 TMA-fed, 2 stage sizes)
 static std::atomic<int64_t> g_opt_lidar_tma_warps{48000};  // v4: target warp units per launch
 static std::atomic<int64_t> g_opt_lidar_warps{76000};  // v3: target warp units per launch  // shared-memory carveout % for the trace kernel
@@ -295,6 +296,11 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
   if (!strcmp(name, "lidar_warps")) {
     if (value < 1) return fail(RMPB_ERR_INVALID, "lidar_warps must be >= 1");
     g_opt_lidar_warps.store(value);
+    return RMPB_OK;
+  }
+  if (!strcmp(name, "l2_window")) {
+    if (value < 0 || value > 1) return fail(RMPB_ERR_INVALID, "l2_window must be 0 or 1");
+    g_opt_l2_window.store(value);
     return RMPB_OK;
   }
   if (!strcmp(name, "lidar_tma_warps")) {
@@ -835,6 +841,66 @@ static void apply_carveout(K* kern) {
   done[key] = pct;
 }
 
+// L2 residency of the map (north_star: the grid "pinned in L2 with an
+// access-policy window"): every trace launch carries an access-policy window
+// over the map's device array, hit property persisting, so the map stays in
+// the persisting L2 carve-out while other traffic (LiDAR streams, the
+// caller's own kernels) streams past it.  The carve-out is sized once per
+// device to the largest map seen (<= cudaDevAttrMaxPersistingL2CacheSize);
+// a window larger than the carve-out gets hitRatio = carve-out / window.
+// Option "l2_window" = 0 turns it off (plain launches).
+static bool l2_window_attr(const rmpb_grid* g, cudaLaunchAttribute* a) {
+  if (!g_opt_l2_window.load() || !g->d_values || g->bytes <= 0) return false;
+  struct DevL2 { int max_win = 0, max_persist = 0; size_t limit = 0; bool init = false; };
+  static std::mutex mu;
+  static DevL2 devs[64];
+  std::lock_guard<std::mutex> lk(mu);
+  DevL2& d = devs[g->device & 63];
+  if (!d.init) {
+    d.init = true;
+    cudaDeviceGetAttribute(&d.max_win, cudaDevAttrMaxAccessPolicyWindowSize, g->device);
+    cudaDeviceGetAttribute(&d.max_persist, cudaDevAttrMaxPersistingL2CacheSize, g->device);
+    cudaGetLastError();
+  }
+  if (d.max_win <= 0 || d.max_persist <= 0) return false;
+  const size_t win = std::min<size_t>((size_t)g->bytes, (size_t)d.max_win);
+  const size_t want = std::min<size_t>(win, (size_t)d.max_persist);
+  if (want > d.limit) {
+    if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+      cudaGetLastError();
+      return false;
+    }
+    d.limit = want;
+  }
+  a->id = cudaLaunchAttributeAccessPolicyWindow;
+  a->val.accessPolicyWindow.base_ptr = g->d_values;
+  a->val.accessPolicyWindow.num_bytes = win;
+  a->val.accessPolicyWindow.hitRatio = std::min(1.0f, (float)((double)d.limit / (double)win));
+  a->val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a->val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  return true;
+}
+
+// Launch `kern` with the map's L2 window when enabled (cudaLaunchKernelEx),
+// else a plain launch.
+template <class... KArgs, class... Args>
+static cudaError_t launch_mapped(const rmpb_grid* g, void (*kern)(KArgs...), unsigned blocks,
+                                 unsigned threads, cudaStream_t st, Args&&... args) {
+  cudaLaunchAttribute attr[1];
+  if (l2_window_attr(g, &attr[0])) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(blocks);
+    cfg.blockDim = dim3(threads);
+    cfg.dynamicSmemBytes = 0;
+    cfg.stream = st;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+  }
+  kern<<<blocks, threads, 0, st>>>(std::forward<Args>(args)...);
+  return cudaSuccess;
+}
+
 static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io, int64_t P,
                              const PolicyParams& pp, double max_range, double eps,
                              double step_scale, int segs, int seg_rays, RayOut ro,
@@ -856,28 +922,27 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
       apply_carveout(k_ray_policy2<G, true>);
       apply_carveout(k_ray_policy2<G, false>);
     }
+    cudaError_t le;
+    const unsigned nb = (unsigned)units;
     if (!v2 && xa)
-      k_ray_policy<G, true><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
-                                                                max_range, eps, step_scale, segs,
-                                                                seg_rays, ro, xv);
+      le = launch_mapped(g, k_ray_policy<G, true>, nb, kBlock, st, acc, g->geom, bv, io, pp,
+                         max_range, eps, step_scale, segs, seg_rays, ro, xv);
     else if (!v2)
-      k_ray_policy<G><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp, max_range, eps,
-                                                          step_scale, segs, seg_rays, ro, xv);
+      le = launch_mapped(g, k_ray_policy<G>, nb, kBlock, st, acc, g->geom, bv, io, pp, max_range,
+                         eps, step_scale, segs, seg_rays, ro, xv);
     else if (mode == RMPB_MODE_FAST && ro.step_total)
-      k_ray_policy2<G, true, true><<<(unsigned)units, kBlock, 0, st>>>(
-          acc, g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays, ro);
+      le = launch_mapped(g, k_ray_policy2<G, true, true>, nb, kBlock, st, acc, g->geom, bv, io,
+                         pp, max_range, eps, step_scale, segs, seg_rays, ro);
     else if (mode == RMPB_MODE_FAST)
-      k_ray_policy2<G, false, true><<<(unsigned)units, kBlock, 0, st>>>(
-          acc, g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays, ro);
+      le = launch_mapped(g, k_ray_policy2<G, false, true>, nb, kBlock, st, acc, g->geom, bv, io,
+                         pp, max_range, eps, step_scale, segs, seg_rays, ro);
     else if (ro.t || ro.step_total)
-      k_ray_policy2<G, true><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
-                                                                 max_range, eps, step_scale, segs,
-                                                                 seg_rays, ro);
-
+      le = launch_mapped(g, k_ray_policy2<G, true>, nb, kBlock, st, acc, g->geom, bv, io, pp,
+                         max_range, eps, step_scale, segs, seg_rays, ro);
     else
-      k_ray_policy2<G, false><<<(unsigned)units, kBlock, 0, st>>>(acc, g->geom, bv, io, pp,
-                                                                  max_range, eps, step_scale, segs,
-                                                                  seg_rays, ro);
+      le = launch_mapped(g, k_ray_policy2<G, false>, nb, kBlock, st, acc, g->geom, bv, io, pp,
+                         max_range, eps, step_scale, segs, seg_rays, ro);
+    CK(le);
     CKL();
     return RMPB_OK;
   });
@@ -1128,8 +1193,18 @@ static int server_launch(rmpb_server* s) {
     unsigned long long idle = s->idle_ns, first = s->epoch;
     void* args[] = {&acc, &geom, &bv, &pp, &mr, &eps, &ss, &seg_rays, &dm, &dd, &parts, &tk, &idle,
                     &first};
-    CK(cudaLaunchCooperativeKernel((const void*)kfn, dim3((unsigned)s->segs), dim3(kBlock), args, 0,
-                                   s->st));
+    // cooperative (all CTAs co-resident) + the map's L2 window
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    const int na = l2_window_attr(s->g, &attr[1]) ? 2 : 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((unsigned)s->segs);
+    cfg.blockDim = dim3(kBlock);
+    cfg.stream = s->st;
+    cfg.attrs = attr;
+    cfg.numAttrs = na;
+    CK(cudaLaunchKernelExC(&cfg, (const void*)kfn, args));
     g_launches.fetch_add(1);
     s->running = true;
     return RMPB_OK;

@@ -8,6 +8,9 @@ from paper_2301_08068_b200.device import RayPolicyEngine
 import paper_2301_08068_b200 as P
 
 PB = int(os.environ.get("PROBE_P", "4096"))
+from paper_2301_08068_b200 import _lib
+if os.environ.get("L2_WINDOW"):
+    _lib.call("rmpb_set_option", b"l2_window", int(os.environ["L2_WINDOW"]))
 scene = synth.c1_scene(); grid = synth.c1_grid(scene)
 states = synth.bench_states(scene, count=PB, seed=123)
 x_h, v_h = synth.states_arrays(states)
@@ -24,6 +27,7 @@ for _ in range(int(os.environ.get("PROBE_REPS", "5"))):
     ts.append(e0.elapsed_time(e1))
 sl = s.cpu().numpy()
 print(json.dumps({"lib": os.path.basename(os.environ.get("RMPB_LIBRARY", "") or "librmpb.so"),
+                  "l2_window": os.environ.get("L2_WINDOW", "default"),
                   "ms_min": round(min(ts), 3), "ms_med": round(sorted(ts)[len(ts) // 2], 3),
                   "hits": int(sl[:, 12].sum()), "sum_a00": float(sl[:, 0].sum()),
                   "sum_b0": float(sl[:, 9].sum())}), flush=True)

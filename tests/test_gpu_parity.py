@@ -211,6 +211,27 @@ def test_determinism_bitwise(be, c1):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
 
 
+def test_l2_window_on_off_bitwise(be, c1):
+    """The map's L2 access-policy window (option l2_window, default on) only
+    changes cache residency: results are bitwise those of a plain launch."""
+    from paper_2301_08068_b200 import _lib as L
+
+    scene, grid, states, dirs = c1
+    st = states[2]
+    outs = []
+    try:
+        for w in (1, 0, 1):
+            L.call("rmpb_set_option", b"l2_window", w)
+            outs.append(be.ray_policy_fused(grid.values, grid.origin, grid.resolution, st.position,
+                                            st.velocity, dirs, STATIC_MAP, 10.0, 0.05, 0.9))
+    finally:
+        L.call("rmpb_set_option", b"l2_window", 1)
+    for o in outs[1:]:
+        assert np.array_equal(outs[0][0], o[0]) and np.array_equal(outs[0][1], o[1])
+    with pytest.raises(ValueError):
+        L.call("rmpb_set_option", b"l2_window", 2)
+
+
 def test_layouts_and_storage_identical(be, oracle, c1):
     from paper_2301_08068_b200 import _lib as L
 
