@@ -118,6 +118,10 @@ RMPB_EXPORT int rmpb_grid_destroy(rmpb_grid* g);
 RMPB_EXPORT int rmpb_bundle_create(const double* dirs, int64_t n, int order, int device, rmpb_bundle** out);
 /* Halton bundle generated on device: i = 1..n, polar = acos(1-2 h2), az = 2 pi h3. */
 RMPB_EXPORT int rmpb_bundle_halton(int64_t n, int order, int device, rmpb_bundle** out);
+/* Spherical-grid bundle generated on device: the LiDAR lattice of
+ * rmpnav/rays.py:176-199 (scan_pattern(rows, cols, vfov_deg)), row-major. */
+RMPB_EXPORT int rmpb_bundle_lattice(int64_t rows, int64_t cols, double vfov_deg, int order, int device,
+                        rmpb_bundle** out);
 RMPB_EXPORT int64_t rmpb_bundle_size(const rmpb_bundle* b);
 /* Directions back to host in ORIGINAL order (n x 3). */
 RMPB_EXPORT int rmpb_bundle_directions(const rmpb_bundle* b, double* out);

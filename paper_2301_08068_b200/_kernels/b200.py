@@ -180,12 +180,21 @@ class DeviceGrid:
 class DeviceBundle:
     """Ray directions on device, evaluated in Morton(polar, azimuth) order."""
 
-    def __init__(self, dirs=None, order=L.ORDER_MORTON, device=None, halton_n=None):
+    def __init__(self, dirs=None, order=L.ORDER_MORTON, device=None, halton_n=None,
+                 lattice=None):
+        """``halton_n``: the reference's Halton bundle of that size generated
+        on device (rays.py:78-86); ``lattice=(rows, cols, vfov_deg)``: the
+        spherical-grid scan pattern generated on device (rays.py:176-199)."""
         self.device = _device if device is None else int(device)
         h = ctypes.c_void_p()
         if halton_n is not None:
             L.call("rmpb_bundle_halton", int(halton_n), int(order), self.device, ctypes.byref(h))
             self.n = int(halton_n)
+        elif lattice is not None:
+            rows, cols, vfov = lattice
+            L.call("rmpb_bundle_lattice", int(rows), int(cols), float(vfov), int(order),
+                   self.device, ctypes.byref(h))
+            self.n = int(rows) * int(cols)
         else:
             d = _f64(dirs, (-1, 3))
             self.n = d.shape[0]

@@ -54,6 +54,7 @@ _SIGS = {
     "rmpb_grid_destroy": (_i, [_vp]),
     "rmpb_bundle_create": (_i, [_vp, _i64, _i, _i, _vp]),
     "rmpb_bundle_halton": (_i, [_i64, _i, _i, _vp]),
+    "rmpb_bundle_lattice": (_i, [_i64, _i64, _d, _i, _i, _vp]),
     "rmpb_bundle_size": (_i64, [_vp]),
     "rmpb_bundle_directions": (_i, [_vp, _vp]),
     "rmpb_bundle_destroy": (_i, [_vp]),

@@ -734,13 +734,15 @@ static int bundle_finish(rmpb_bundle* b, cudaStream_t st) {
   return RMPB_OK;
 }
 
+struct LatticeSpec { int rows = 0, cols = 0; double vfov = 0.0; };
+
 static int bundle_new(const double* dirs, int64_t n, int order, int device, bool halton,
-                      rmpb_bundle** out) {
+                      rmpb_bundle** out, const LatticeSpec* lat = nullptr) {
   if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
   *out = nullptr;
   if (n < 1) return fail(RMPB_ERR_INVALID, "need at least one direction");
   if (n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many directions");
-  if (!halton && !dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
+  if (!halton && !lat && !dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
   if (order != RMPB_ORDER_IDENTITY && order != RMPB_ORDER_MORTON)
     return fail(RMPB_ERR_INVALID, "bad order %d", order);
   DeviceGuard dg(device);
@@ -756,12 +758,15 @@ static int bundle_new(const double* dirs, int64_t n, int order, int device, bool
     cudaStreamDestroy(st);
     return fail(RMPB_ERR_NOMEM, "bundle alloc failed");
   }
-  if (halton) {
+  if (halton || lat) {
     double *x, *y, *z;
     cudaMalloc((void**)&x, n * sizeof(double));
     cudaMalloc((void**)&y, n * sizeof(double));
     cudaMalloc((void**)&z, n * sizeof(double));
-    k_halton<<<grid_blocks(n), 256, 0, st>>>((int)n, x, y, z);
+    if (lat)
+      k_lattice<<<grid_blocks(n), 256, 0, st>>>(lat->rows, lat->cols, lat->vfov, x, y, z);
+    else
+      k_halton<<<grid_blocks(n), 256, 0, st>>>((int)n, x, y, z);
     g_launches.fetch_add(1);
     k_soa_to_aos<<<grid_blocks(n), 256, 0, st>>>((int)n, x, y, z, b->d_aos);
     g_launches.fetch_add(1);
@@ -791,6 +796,16 @@ extern "C" int rmpb_bundle_create(const double* dirs, int64_t n, int order, int 
 
 extern "C" int rmpb_bundle_halton(int64_t n, int order, int device, rmpb_bundle** out) {
   return bundle_new(nullptr, n, order, device, true, out);
+}
+
+extern "C" int rmpb_bundle_lattice(int64_t rows, int64_t cols, double vfov_deg, int order,
+                                   int device, rmpb_bundle** out) {
+  if (rows < 1 || cols < 1) return fail(RMPB_ERR_INVALID, "scan pattern needs rows, cols >= 1");
+  if (rows * cols >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many directions");
+  if (!(vfov_deg == vfov_deg)) return fail(RMPB_ERR_INVALID, "vfov is NaN");
+  LatticeSpec L;
+  L.rows = (int)rows; L.cols = (int)cols; L.vfov = vfov_deg;
+  return bundle_new(nullptr, rows * cols, order, device, false, out, &L);
 }
 
 extern "C" int64_t rmpb_bundle_size(const rmpb_bundle* b) { return b ? b->n : -1; }

@@ -37,6 +37,30 @@ __global__ void k_halton(int n, double* __restrict__ dx, double* __restrict__ dy
   dz[i] = cos(polar);
 }
 
+// Spherical-grid (LiDAR lattice) bundle, rays.py:176-199 (_cached_pattern):
+// row r: elevation deg2rad(linspace(-vfov, vfov, rows)[r]) (0 for one row),
+// column c: azimuth 2*pi*c/cols; dir = (ce cos az, ce sin az, se), row-major.
+// numpy.linspace: start + r * step with step = (stop - start) / (rows - 1),
+// the last sample set to stop exactly; deg2rad multiplies by pi/180.
+__global__ void k_lattice(int rows, int cols, double vfov_deg, double* __restrict__ dx,
+                          double* __restrict__ dy, double* __restrict__ dz) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= (long long)rows * cols) return;
+  const int r = (int)(i / cols), c = (int)(i - (long long)r * cols);
+  double elev_deg = 0.0;
+  if (rows > 1) {
+    const double start = -vfov_deg, stop = vfov_deg;
+    const double step = (stop - start) / (double)(rows - 1);
+    elev_deg = (r == rows - 1) ? stop : start + (double)r * step;
+  }
+  const double elev = elev_deg * (CUDART_PI / 180.0);
+  const double az = 2.0 * CUDART_PI * (double)c / (double)cols;
+  const double ce = cos(elev), se = sin(elev);
+  dx[i] = ce * cos(az);
+  dy[i] = ce * sin(az);
+  dz[i] = se;
+}
+
 __device__ __forceinline__ unsigned part1by1(unsigned x) {
   x &= 0x0000ffffu;
   x = (x | (x << 8)) & 0x00ff00ffu;

@@ -414,6 +414,36 @@ def test_device_halton_close_to_reference(be, oracle):
     assert np.allclose(np.linalg.norm(d, axis=1), 1.0, atol=1e-12)
 
 
+@pytest.mark.parametrize("rows,cols,vfov", [(128, 1024, 45.0), (1, 360, 45.0), (7, 5, 30.0),
+                                             (64, 2048, 22.5)])
+def test_device_lattice_close_to_reference(be, oracle, rows, cols, vfov):
+    """Spherical-grid (LiDAR lattice) bundle generated on device vs the
+    reference's scan_pattern (rays.py:176-199, NumPy trig: a few ulp), and a
+    LiDAR policy on the device lattice vs the oracle on NumPy's lattice."""
+    from paper_2301_08068_b200 import _lib as L
+
+    b = be.DeviceBundle(lattice=(rows, cols, vfov), order=L.ORDER_IDENTITY)
+    d = b.directions()
+    r = oracle.scan_pattern(rows, cols, vfov)
+    assert d.shape == r.shape == (rows * cols, 3)
+    assert np.abs(d - r).max() <= 1e-15
+    rng = np.random.default_rng(rows * cols)
+    ranges = rng.uniform(0.0, 3.0, rows * cols)
+    valid = rng.random(rows * cols) < 0.7
+    v = np.array([0.4, -0.7, 0.2])
+    slot = np.empty(13)
+    acc = np.empty(3)
+    vl = valid.astype(np.uint8)  # keep the temporaries alive across the call
+    prm = np.asarray(LIDAR, dtype=np.float64)
+    L.call("rmpb_lidar_policy_bundle", b.handle, None, ranges.ctypes.data, vl.ctypes.data,
+           v.ctypes.data, prm.ctypes.data, 0.3, slot.ctypes.data, acc.ctypes.data, None)
+    slot_r, acc_r = oracle.lidar_policy(r, ranges, valid, v, LIDAR, 0.3)
+    assert slot[12] == slot_r[12]
+    assert rel_err(slot[:12], slot_r[:12]) <= 1e-9
+    with pytest.raises(ValueError):
+        be.DeviceBundle(lattice=(0, 5, 45.0))
+
+
 def test_tsdf_bake_bricks_and_readback(be, oracle):
     """Truncated (TSDF) GPU bake: brick-culled bake == clamp of the full
     oracle bake; BRICK / QUAD / LINEAR layouts read back the same nodes and
