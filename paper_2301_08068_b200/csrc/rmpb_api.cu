@@ -262,7 +262,10 @@ static int check_params(const double* p) {
 static void choose_segments(int64_t P, int64_t n, int* segs, int* seg_rays) {
   int64_t sr = g_opt_seg_rays.load();
   if (sr <= 0) {
-    const int64_t target_units = 148LL * 4 * 8;
+    // >= ~16 waves of 4 CTAs per SM: finer units shorten the tail of the
+    // last wave (4096 C1 poses: 4 segments of 16384 rays, 13.78 ms vs 14.02
+    // with 2 segments, vs 14.4 with 1)
+    const int64_t target_units = 148LL * 4 * 16;
     sr = kBlock;
     while (sr < n && P * ((n + sr * 2 - 1) / (sr * 2)) >= target_units) sr *= 2;
   }

@@ -9,6 +9,8 @@ import paper_2301_08068_b200 as P
 
 PB = int(os.environ.get("PROBE_P", "4096"))
 from paper_2301_08068_b200 import _lib
+if os.environ.get("SEG_RAYS"):
+    _lib.call("rmpb_set_option", b"seg_rays", int(os.environ["SEG_RAYS"]))
 if os.environ.get("L2_WINDOW"):
     _lib.call("rmpb_set_option", b"l2_window", int(os.environ["L2_WINDOW"]))
 scene = synth.c1_scene(); grid = synth.c1_grid(scene)
@@ -28,6 +30,7 @@ for _ in range(int(os.environ.get("PROBE_REPS", "5"))):
 sl = s.cpu().numpy()
 print(json.dumps({"lib": os.path.basename(os.environ.get("RMPB_LIBRARY", "") or "librmpb.so"),
                   "l2_window": os.environ.get("L2_WINDOW", "default"),
+                  "seg_rays": os.environ.get("SEG_RAYS", "auto"),
                   "ms_min": round(min(ts), 3), "ms_med": round(sorted(ts)[len(ts) // 2], 3),
                   "hits": int(sl[:, 12].sum()), "sum_a00": float(sl[:, 0].sum()),
                   "sum_b0": float(sl[:, 9].sum())}), flush=True)
