@@ -449,7 +449,8 @@ struct K2Smem {
 
 // Evaluates queue entry `lane` (when `valid`) and adds the warp's batch sum
 // to the warp accumulator (lane 0).
-__device__ __forceinline__ void policy_flush(K2Smem& sm, int warp, int lane, bool valid,
+template <class SM>
+__device__ __forceinline__ void policy_flush(SM& sm, int warp, int lane, bool valid,
                                              const Bundle& b, int ray, double d, double vx,
                                              double vy, double vz, const PolicyParams& p) {
   Acc a;
