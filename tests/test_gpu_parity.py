@@ -801,3 +801,28 @@ def test_public_ray_policy_repeated_and_in_place_edit(be, oracle):
     assert rel_err(pol2.metric, ref2[0][:9].reshape(3, 3)) <= SUM_TOL
     assert rel_err(pol2.accel, ref2[1]) <= ACC_TOL
     assert not np.allclose(pol2.metric, pol.metric)
+
+
+def test_concurrent_host_threads_bitwise(be, c1):
+    """The C ABI is thread-safe (per-(device, stream) workspaces, each behind
+    its own lock): host threads calling the public ray_policy / lidar_policy
+    concurrently get bitwise the results of sequential calls."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    import paper_2301_08068_b200 as P
+
+    scene, grid, states, dirs = c1
+    esdf = grid if isinstance(grid, P.EsdfGrid) else P.EsdfGrid(
+        grid.origin, grid.resolution, grid.values.shape, grid.values)
+    bundle = P.RayBundle(dirs)
+    params = P.preset("static_map").obstacle
+    seq = [P.ray_policy(st, esdf, bundle, params, 10.0) for st in states]
+
+    def one(k):
+        pol = P.ray_policy(states[k % len(states)], esdf, bundle, params, 10.0)
+        return k % len(states), pol
+
+    with ThreadPoolExecutor(max_workers=6) as ex:
+        for k, pol in ex.map(one, range(48)):
+            assert np.array_equal(pol.metric, seq[k].metric)
+            assert np.array_equal(pol.accel, seq[k].accel)
