@@ -38,7 +38,7 @@ static std::atomic<int64_t> g_opt_seg_rays{0};
 static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread per pass, 2 lane refill
 static std::atomic<int64_t> g_opt_carveout{-1};
 static std::atomic<int64_t> g_opt_l2_window{1};  // map access-policy window on trace launches
-static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (= 3), 1, 2 (v1/v2), 3 (v3 warp units), 4/5 (v4 TMA-fed, 2 stage sizes)
+static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (= 3), 1, 2 (v1/v2), 3 (v3 warp units), 4/5 (v4 TMA-fed, 2 stage sizes), 6 (v5 compact + list policy)
 static std::atomic<int64_t> g_opt_lidar_tma_warps{48000};  // v4: target warp units per launch
 static std::atomic<int64_t> g_opt_lidar_warps{76000};  // v3: target warp units per launch  // shared-memory carveout % for the trace kernel
 
@@ -135,6 +135,7 @@ struct HostBuf {  // pinned + mapped (device-visible under UVA)
 struct Workspace {
   std::mutex mu;
   DevBuf in, in2, in3, out, out2, out3, partials;
+  DevBuf lst;      // LiDAR v5 scratch list (compacted in-radius beams)
   DevBuf tickets;  // zeroed on growth
   size_t tickets_n = 0;
   HostBuf hres;    // pinned + mapped results (slots / accels)
@@ -312,7 +313,7 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
     return RMPB_OK;
   }
   if (!strcmp(name, "lidar_kernel")) {
-    if (value < 0 || value > 5) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..5");
+    if (value < 0 || value > 6) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..6");
     g_opt_lidar_kernel.store(value);
     return RMPB_OK;
   }
@@ -1554,6 +1555,47 @@ static int launch_lidar_tma(Src src, int64_t S_, int64_t n, const double* d_v, d
   return RMPB_OK;
 }
 
+// K2 v5 / K2b v3: stream-and-compact kernel + list-policy kernel (see
+// k_lidar_compact).  Same warp units as v3; the scratch list gives every unit
+// its own region of `seg` entries (range f64 + beam index i32).
+template <class Src>
+static int launch_lidar_two(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
+                            const PolicyParams& pp, double* d_slot, double* d_accel,
+                            Workspace* ws, cudaStream_t st) {
+  const int64_t target = g_opt_lidar_warps.load();
+  int64_t wps = (target + S_ - 1) / S_;
+  wps = std::min<int64_t>(wps, 1024);
+  wps = std::min<int64_t>(wps, (n + 127) / 128);
+  wps = std::max<int64_t>(wps, 1);
+  const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
+  wps = (n + seg - 1) / seg;
+  const long long nunits = (long long)S_ * wps;
+  if (wps > 1) {
+    TRY(ws->partials.ensure((size_t)nunits * kAcc * sizeof(double)));
+    TRY(ws->ensure_tickets((size_t)S_));
+  }
+  const size_t ent = (size_t)nunits * (size_t)seg;
+  TRY(ws->lst.ensure(ent * (sizeof(double) + sizeof(int)) + (size_t)nunits * sizeof(int2) + 16));
+  double* ld = (double*)ws->lst.p;
+  int* li = (int*)(ld + ent);
+  int2* uc = (int2*)(((uintptr_t)(li + ent) + 15) & ~(uintptr_t)15);
+  PoseIO io{};
+  io.x = nullptr; io.v = d_v;
+  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
+  io.slot = d_slot; io.accel = d_accel;
+  io.partials = (double*)ws->partials.p;
+  io.tickets = (unsigned*)ws->tickets.p;
+  const long long blocks = (nunits + kWarps - 1) / kWarps;
+  if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
+  k_lidar_compact<Src><<<(unsigned)blocks, kBlock, 0, st>>>(src, pp, (int)wps, (int)seg, nunits,
+                                                           ld, li, uc);
+  CKL();
+  k_lidar_listpolicy<Src><<<(unsigned)blocks, kBlock, 0, st>>>(src, io, pp, (int)wps, (int)seg,
+                                                              nunits, ld, li, uc);
+  CKL();
+  return RMPB_OK;
+}
+
 static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
                         const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                         cudaStream_t st) {
@@ -1567,6 +1609,11 @@ static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
     LatticeTma<2> src{};
     src.sc = sc;
     return launch_lidar_tma<LatticeTma<2>, 2, 2>(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+  }
+  if (kopt == 6) {
+    LatticeSrc src{};
+    src.sc = sc;
+    return launch_lidar_two(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
   }
   if (kopt == 0 || kopt == 3) {
     LatticeSrc src{};
@@ -1692,6 +1739,11 @@ static int points_launch(PointsIO pt, int64_t S_, const double* d_v, double v0[3
     PointTma<2> src{};
     src.pt = pt;
     return launch_lidar_tma<PointTma<2>, 2, 2>(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+  }
+  if (kopt == 6) {
+    PointSrc src{};
+    src.pt = pt;
+    return launch_lidar_two(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
   }
   if (kopt == 0 || kopt == 3) {
     PointSrc src{};

@@ -32,7 +32,7 @@ for arg in sys.argv[1:] or ["2", "3"]:
     k = int(k)
     _lib.call("rmpb_set_option", b"lidar_kernel", k)
     if wt:
-        _lib.call("rmpb_set_option", b"lidar_tma_warps" if k >= 4 else b"lidar_warps", int(wt))
+        _lib.call("rmpb_set_option", b"lidar_tma_warps" if k in (4, 5) else b"lidar_warps", int(wt))
     k = arg
     s, a = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
     torch.cuda.synchronize()

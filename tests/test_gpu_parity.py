@@ -670,10 +670,10 @@ def test_lidar_points_batch_device(be, oracle, c1):
 
 
 # 1: per-thread, 2: CTA streaming, 3: warp units, 4 / 5: TMA-fed warp units
-# (two pipeline depths); 14: variant 4 with long warp units (3 per launch:
+# (two stage sizes); 6: compact + list policy (two kernels); 14: variant 4 with long warp units (3 per launch:
 # many groups per warp, so the stage ring wraps and the mbarrier parity flips)
-LIDAR_VARIANTS = (1, 2, 3, 4, 5, 14)
-LIDAR_VARIANTS_PTS = (1, 3, 4, 5, 14)
+LIDAR_VARIANTS = (1, 2, 3, 4, 5, 6, 14)
+LIDAR_VARIANTS_PTS = (1, 3, 4, 5, 6, 14)
 
 
 @pytest.mark.parametrize("n,S", [(131072, 1), (1000, 5), (131, 3), (97, 2), (4096, 40), (8192, 3)])
