@@ -826,3 +826,47 @@ def test_concurrent_host_threads_bitwise(be, c1):
         for k, pol in ex.map(one, range(48)):
             assert np.array_equal(pol.metric, seq[k].metric)
             assert np.array_equal(pol.accel, seq[k].accel)
+
+
+def test_c5_full_size_properties(be, oracle):
+    """Config C5 at its full size (1000x1000x200 TSDF @0.05 m, 1 M rays per
+    pose): size-independent properties.  The block-hashed map evaluates
+    bitwise like the dense one; the 8-way ray split folds to the whole pose's
+    result (hit count exact, sums to 1e-12); a 2048-ray sample traces
+    bit-identically to the CPU oracle on the read-back node values."""
+    import torch
+
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200.device import RayPolicyEngine
+    from paper_2301_08068_b200.parallel import balanced_range
+
+    scene = synth.c5_scene()
+    dense, brick, info = synth.c5_grids(scene)
+    assert 0 < info["bricks_allocated"] < info["bricks_total"]
+    states = synth.bench_states(scene, count=2, seed=123, distance=synth.host_box_distance(scene))
+    n = 1 << 20
+    bundle = be.DeviceBundle(halton_n=n)
+    x = torch.tensor(np.stack([s.position for s in states]), dtype=torch.float64, device="cuda")
+    v = torch.tensor(np.stack([s.velocity for s in states]), dtype=torch.float64, device="cuda")
+    outs = []
+    for dg in (dense, brick):
+        eng = RayPolicyEngine(dg, bundle, STATIC_MAP, 10.0)
+        s, a = eng.evaluate(x, v)
+        outs.append((s.cpu().numpy(), a.cpu().numpy(), eng))
+    assert np.array_equal(outs[0][0], outs[1][0]) and np.array_equal(outs[0][1], outs[1][1])
+    eng = outs[1][2]
+    x1, v1 = x[0].contiguous(), v[0].contiguous()
+    parts = torch.stack([eng.partial(x1, v1, *balanced_range(n, 8, r)) for r in range(8)])
+    ss, sa = eng.resolve(parts)
+    ss, sa = ss.cpu().numpy(), sa.cpu().numpy()
+    whole = outs[1][0][0]
+    assert ss[12] == whole[12] > 0
+    assert rel_err(ss[:12], whole[:12]) <= 1e-12
+    vals = brick.values()
+    samp = np.ascontiguousarray(oracle.sample_directions(2048))
+    t, c, _ = be.grid_trace_ex(brick, synth.C5_ORIGIN, synth.C5_RES, states[0].position, samp,
+                               10.0, 0.5 * synth.C5_RES, 0.9, with_cells=True)
+    t_r, c_r = oracle.grid_trace(vals, synth.C5_ORIGIN, synth.C5_RES, states[0].position, samp,
+                                 10.0, 0.5 * synth.C5_RES, 0.9, with_cells=True, workers=8)
+    assert np.array_equal(t, t_r) and np.array_equal(c, c_r)
+    assert np.isfinite(t).mean() > 0.3
