@@ -47,6 +47,20 @@ __device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long
   asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// Fence-based flag protocol (PTX memory model: data stores; fence; relaxed
+// flag store || relaxed flag load; fence; data loads): one system-scope
+// fence per side instead of an implied fence per flag.
+__device__ __forceinline__ void fence_acq_rel_sys() {
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+}
+__device__ __forceinline__ void st_relaxed_sys(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long ld_relaxed_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void st_release_gpu(unsigned long long* p, unsigned long long v) {
   asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -226,19 +240,20 @@ __device__ void exchange_emit(const Acc& s, const PoseIO& io, const ExArgs& xa) 
       double* dst = ex.slots[r] + ((size_t)par * W + ex.rank) * kMbox;
       for (int j = 0; j < 13; ++j) __stcg(dst + j, rec[j]);
     }
-    __threadfence_system();
-    for (int r = 0; r < W; ++r) st_release_sys(ex.flags[r] + (size_t)par * W + ex.rank, xa.epoch);
+    fence_acq_rel_sys();  // slots before flags, once for all peers
+    for (int r = 0; r < W; ++r) st_relaxed_sys(ex.flags[r] + (size_t)par * W + ex.rank, xa.epoch);
   }
   if (!(xa.mode & EX_WAIT)) return;
   const unsigned long long* fl = ex.flags[ex.rank] + (size_t)par * W;
   const unsigned long long t0 = globaltimer_ns();
   bool ok = true;
   for (int r = 0; r < W && ok; ++r) {
-    while (ld_acquire_sys(fl + r) != xa.epoch) {
+    while (ld_relaxed_sys(fl + r) != xa.epoch) {
       if (globaltimer_ns() - t0 > 10000000000ull) { ok = false; break; }  // 10 s: a peer is gone
       __nanosleep(32);
     }
   }
+  fence_acq_rel_sys();  // every flag seen: the slots are visible
   double out[13];
   if (ok) {
     for (int j = 0; j < 13; ++j) out[j] = fold8(ex.slots[ex.rank] + (size_t)par * W * kMbox + j, W, kMbox);
@@ -406,10 +421,7 @@ k_ray_server(G grid, GridGeom g, Bundle b, PolicyParams p, double max_range, dou
     for (int k = 0; k < 3; ++k) { io.x0[k] = s_xv[k]; io.v0[k] = s_xv[3 + k]; }
     const bool wrote = lean_unit(grid, g, b, io, p, max_range, eps, step_scale, (int)gridDim.x,
                                  seg_rays, ro, (int)blockIdx.x);
-    if (wrote) {
-      __threadfence_system();
-      st_release_sys(&mail->done, e);
-    }
+    if (wrote) st_release_sys(&mail->done, e);  // orders this thread's slot / accel writes
     __syncthreads();
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
