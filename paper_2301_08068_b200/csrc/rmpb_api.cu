@@ -38,6 +38,7 @@ static std::atomic<int64_t> g_opt_seg_rays{0};
 static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread per pass, 2 lane refill
 static std::atomic<int64_t> g_opt_carveout{-1};
 static std::atomic<int64_t> g_opt_l2_window{1};  // map access-policy window on trace launches
+static std::atomic<int64_t> g_opt_graphs{1};     // CUDA-graph replay of rollout ticks
 static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (= 3), 1, 2 (v1/v2), 3 (v3 warp units), 4/5 (v4 TMA-fed, 2 stage sizes), 6 (v5 compact + list policy)
 static std::atomic<int64_t> g_opt_lidar_tma_warps{48000};  // v4: target warp units per launch
 static std::atomic<int64_t> g_opt_lidar_warps{76000};  // v3: target warp units per launch  // shared-memory carveout % for the trace kernel
@@ -269,6 +270,10 @@ static void choose_segments(int64_t P, int64_t n, int* segs, int* seg_rays) {
     const int64_t target_units = 148LL * 4 * 16;
     sr = kBlock;
     while (sr < n && P * ((n + sr * 2 - 1) / (sr * 2)) >= target_units) sr *= 2;
+    // one ray per thread (the lean kernel) only while every ray of the launch
+    // is in flight at once (~2 waves of 148 SMs x 2048 threads); beyond that
+    // lanes must refill, so segments of >= 2 rays per thread
+    if (sr == kBlock && n > kBlock && P * n > 2LL * 148 * 2048) sr = 2 * kBlock;
   }
   if (sr % kBlock) sr = (sr / kBlock + 1) * kBlock;
   if (sr > n) sr = ((n + kBlock - 1) / kBlock) * kBlock;
@@ -300,6 +305,11 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
   if (!strcmp(name, "lidar_warps")) {
     if (value < 1) return fail(RMPB_ERR_INVALID, "lidar_warps must be >= 1");
     g_opt_lidar_warps.store(value);
+    return RMPB_OK;
+  }
+  if (!strcmp(name, "graphs")) {
+    if (value < 0 || value > 1) return fail(RMPB_ERR_INVALID, "graphs must be 0 or 1");
+    g_opt_graphs.store(value);
     return RMPB_OK;
   }
   if (!strcmp(name, "l2_window")) {
@@ -2106,6 +2116,8 @@ struct rmpb_rollout {
   double* accels = nullptr;
   unsigned* h_active = nullptr;  // pinned mirror of the running count
   cudaStream_t st = nullptr;
+  cudaGraphExec_t graph = nullptr;  // 16 captured ticks (private stream only)
+  bool graph_failed = false;
 };
 
 extern "C" int rmpb_rollout_create(const rmpb_grid* g, const rmpb_bundle* b, const rmpb_scene* sc,
@@ -2168,6 +2180,50 @@ extern "C" int rmpb_rollout_create(const rmpb_grid* g, const rmpb_bundle* b, con
   return RMPB_OK;
 }
 
+// One closed-loop tick: checks, fused trace + policy + pinv, attractor /
+// combine / clamp / Euler.
+static int rollout_tick(rmpb_rollout* r, Workspace* ws, cudaStream_t st) {
+  const int P = (int)r->P;
+  const int nb = (P + 127) / 128;
+  CK(cudaMemsetAsync(r->s.n_active, 0, sizeof(unsigned), st));
+  k_rollout_check<<<(unsigned)(((int64_t)P * 32 + kCheckBlock - 1) / kCheckBlock), kCheckBlock, 0,
+                    st>>>(r->scene->pack, r->s, r->cfg, P);
+  CKL();
+  TRY(ray_policy_batch_impl(r->g, r->b, r->s.x, r->s.v, P, r->params, r->max_range,
+                            0.5 * r->g->geom.res, 0.9, r->slots, r->accels, nullptr, ws, st,
+                            r->s.active));
+  k_rollout_update<<<nb, 128, 0, st>>>(r->s, r->cfg, r->slots, r->accels, P);
+  CKL();
+  return RMPB_OK;
+}
+
+constexpr int kGraphTicks = 16;  // ticks per captured graph (= the polling period)
+
+// Captures kGraphTicks ticks into r->graph (CUDA graph: one launch per 16
+// ticks instead of 4 API calls per tick).  Only on the rollout's private
+// stream, whose workspace no other call can grow (the graph bakes in its
+// buffers).  Any capture failure falls back to eager ticks for good.
+static void rollout_capture(rmpb_rollout* r, Workspace* ws) {
+  cudaGraph_t graph = nullptr;
+  if (cudaStreamBeginCapture(r->st, cudaStreamCaptureModeThreadLocal) != cudaSuccess) {
+    cudaGetLastError();
+    r->graph_failed = true;
+    return;
+  }
+  const uint64_t n0 = g_launches.load();
+  int rc = RMPB_OK;
+  for (int k = 0; k < kGraphTicks && rc == RMPB_OK; ++k) rc = rollout_tick(r, ws, r->st);
+  g_launches.store(n0);  // captured, not launched
+  const cudaError_t e = cudaStreamEndCapture(r->st, &graph);
+  if (rc != RMPB_OK || e != cudaSuccess || !graph ||
+      cudaGraphInstantiate(&r->graph, graph, 0) != cudaSuccess) {
+    cudaGetLastError();
+    r->graph = nullptr;
+    r->graph_failed = true;
+  }
+  if (graph) cudaGraphDestroy(graph);
+}
+
 extern "C" int rmpb_rollout_run(rmpb_rollout* r, int64_t max_ticks, int64_t* active_left,
                                 void* stream) {
   if (!r) return fail(RMPB_ERR_INVALID, "rollout is NULL");
@@ -2175,29 +2231,34 @@ extern "C" int rmpb_rollout_run(rmpb_rollout* r, int64_t max_ticks, int64_t* act
   cudaStream_t st = stream ? S(stream) : r->st;
   Workspace* ws = workspace(r->g->device, stream ? stream : (void*)r->st);
   std::lock_guard<std::mutex> lk(ws->mu);
-  const int P = (int)r->P;
-  const int nb = (P + 127) / 128;
+  const bool graphs = !stream && g_opt_graphs.load() != 0;
   unsigned left = 1;
-  for (int64_t t = 0; t < max_ticks && left > 0; ++t) {
-    CK(cudaMemsetAsync(r->s.n_active, 0, sizeof(unsigned), st));
-    k_rollout_check<<<nb, 128, 0, st>>>(r->scene->pack, r->s, r->cfg, P);
-    CKL();
-    TRY(ray_policy_batch_impl(r->g, r->b, r->s.x, r->s.v, P, r->params, r->max_range,
-                              0.5 * r->g->geom.res, 0.9, r->slots, r->accels, nullptr, ws, st,
-                              r->s.active));
-    k_rollout_update<<<nb, 128, 0, st>>>(r->s, r->cfg, r->slots, r->accels, P);
-    CKL();
-    if ((t & 15) == 15 || t + 1 == max_ticks) {  // poll the running count now and then
-      CK(cudaMemcpyAsync(r->h_active, r->s.n_active, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
-      CK(cudaStreamSynchronize(st));
-      left = *r->h_active;
+  int64_t t = 0;
+  bool warm = false;
+  while (t < max_ticks && left > 0) {
+    const int64_t chunk = std::min<int64_t>(kGraphTicks, max_ticks - t);
+    if (graphs && chunk == kGraphTicks && warm && !r->graph && !r->graph_failed)
+      rollout_capture(r, ws);
+    if (graphs && chunk == kGraphTicks && r->graph) {
+      CK(cudaGraphLaunch(r->graph, st));
+      g_launches.fetch_add(3 * kGraphTicks, std::memory_order_relaxed);
+    } else {
+      // eager ticks (the first chunk also settles one-time setup: workspace
+      // growth, carve-outs, the L2 window limit -- none of it capturable)
+      for (int64_t k = 0; k < chunk; ++k) TRY(rollout_tick(r, ws, st));
+      warm = true;
     }
+    t += chunk;
+    // poll the running count once per chunk
+    CK(cudaMemcpyAsync(r->h_active, r->s.n_active, sizeof(unsigned), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    left = *r->h_active;
   }
   if (active_left) {
     // exact count after the last tick: run the checks once more without side effects
     CK(cudaStreamSynchronize(st));
-    std::vector<int> act((size_t)P);
-    CK(cudaMemcpy(act.data(), r->s.active, P * 4, cudaMemcpyDeviceToHost));
+    std::vector<int> act((size_t)r->P);
+    CK(cudaMemcpy(act.data(), r->s.active, r->P * 4, cudaMemcpyDeviceToHost));
     int64_t n = 0;
     for (int v : act) n += v;
     *active_left = n;
@@ -2239,6 +2300,7 @@ extern "C" int rmpb_rollout_destroy(rmpb_rollout* r) {
   if (!r) return RMPB_OK;
   DeviceGuard dg(r->g->device);
   if (r->st) cudaStreamSynchronize(r->st);
+  if (r->graph) cudaGraphExecDestroy(r->graph);
   cudaFree(r->mem);
   if (r->h_active) cudaFreeHost(r->h_active);
   if (r->st) cudaStreamDestroy(r->st);

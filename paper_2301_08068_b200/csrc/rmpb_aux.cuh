@@ -227,6 +227,47 @@ __device__ __forceinline__ double scene_sd(const ScenePack& s, double t, double 
   return d;
 }
 
+// scene_sd for one point evaluated by a whole warp: lanes compute the
+// per-primitive distances 32 at a time (the same expressions), then every
+// lane applies them in scene order through shuffles -- the same sequential
+// fold, so the result is bitwise scene_sd's; returned in every lane.
+__device__ __forceinline__ double scene_sd_warp(const ScenePack& s, double t, double px, double py,
+                                                double pz) {
+  const int lane = threadIdx.x & 31;
+  double d = s.empty;
+  for (int base = 0; base < s.n; base += 32) {
+    const int i = base + lane;
+    double dp = 0.0;
+    int op = 0;
+    if (i < s.n) {
+      double dx = px - (s.centers[3 * i] + s.vels[3 * i] * t);
+      double dy = py - (s.centers[3 * i + 1] + s.vels[3 * i + 1] * t);
+      double dz = pz - (s.centers[3 * i + 2] + s.vels[3 * i + 2] * t);
+      if (s.kinds[i] == 0) {
+        dp = sqrt(dx * dx + dy * dy + dz * dz) - s.sizes[3 * i];
+      } else {
+        double qx = fabs(dx) - s.sizes[3 * i];
+        double qy = fabs(dy) - s.sizes[3 * i + 1];
+        double qz = fabs(dz) - s.sizes[3 * i + 2];
+        double ex = qx > 0.0 ? qx : 0.0, ey = qy > 0.0 ? qy : 0.0, ez = qz > 0.0 ? qz : 0.0;
+        double mx = qx;
+        if (qy > mx) mx = qy;
+        if (qz > mx) mx = qz;
+        dp = sqrt(ex * ex + ey * ey + ez * ez) + (mx < 0.0 ? mx : 0.0);
+      }
+      op = s.ops[i];
+    }
+    const int cnt = min(32, s.n - base);
+    for (int j = 0; j < cnt; ++j) {
+      const double dj = __shfl_sync(0xffffffffu, dp, j);
+      const int oj = __shfl_sync(0xffffffffu, op, j);
+      if (oj == 0) { if (dj < d) d = dj; }
+      else { if (-dj > d) d = -dj; }
+    }
+  }
+  return d;
+}
+
 __global__ void k_scene_distance(ScenePack s, double t, const double* __restrict__ pts, int n,
                                   double* __restrict__ out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;

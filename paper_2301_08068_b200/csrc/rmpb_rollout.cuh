@@ -53,16 +53,23 @@ __device__ inline void record_sample(const RolloutState& s, const RolloutCfg& cf
   for (int i = 0; i < 3; ++i) { r[i] = x[i]; r[3 + i] = v[i]; r[6 + i] = a[i]; }
 }
 
-// Termination checks at the start of a tick (sim.py:236-250).
-__global__ void k_rollout_check(ScenePack scene, RolloutState s, RolloutCfg cfg, int P) {
-  const int p = blockIdx.x * blockDim.x + threadIdx.x;
-  if (p >= P || !s.active[p]) return;
+// Termination checks at the start of a tick (sim.py:236-250).  One warp per
+// robot: the analytic scene distance (a sequential fold over the scene's
+// primitives) is computed 32 primitives at a time (scene_sd_warp, bitwise
+// scene_sd); lane 0 does the rest.
+constexpr int kCheckBlock = 128;
+__global__ void __launch_bounds__(kCheckBlock)
+k_rollout_check(ScenePack scene, RolloutState s, RolloutCfg cfg, int P) {
+  const int p = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  if (p >= P || !s.active[p]) return;  // warp-uniform
   const int k = s.k[p];
   const double t = (double)k * cfg.dt;
   const double* x = s.x + 3 * p;
   const double* g = s.goal + 3 * p;
+  const double sd = scene_sd_warp(scene, t, x[0], x[1], x[2]);
+  if ((threadIdx.x & 31) != 0) return;
   int out = OUT_RUNNING;
-  if (scene_sd(scene, t, x[0], x[1], x[2]) <= cfg.robot_radius) {
+  if (sd <= cfg.robot_radius) {
     out = OUT_COLLISION;
   } else if (!cfg.hold && norm3(x[0] - g[0], x[1] - g[1], x[2] - g[2]) <= cfg.goal_tol) {
     out = OUT_SUCCESS;

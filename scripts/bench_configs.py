@@ -329,6 +329,23 @@ def c4loop(args, out):
            "still_running": left,
            "outcomes": {k: res.outcome.count(k) for k in set(res.outcome)},
            "note": "wall clock around rmpb_rollout_run (3 launches per tick, polled every 16)"}
+    # small batches are launch-bound: ticks replayed from a captured CUDA graph
+    # (16 per graph launch) vs eager launches
+    from paper_2301_08068_b200 import _lib as L
+    small = {}
+    for nr in (1, 64):
+        for gr in (0, 1):
+            L.call("rmpb_set_option", b"graphs", gr)
+            rb2 = RolloutBatch(scene, grid, bundle, starts[:nr], goals[:nr], cfg)
+            rb2.run(32)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rb2.run(96)
+            torch.cuda.synchronize()
+            small[f"robots{nr}_{'graph' if gr else 'eager'}_us_per_tick"] = round(
+                (time.perf_counter() - t0) / 96 * 1e6, 1)
+    L.call("rmpb_set_option", b"graphs", 1)
+    rec["small_batches"] = small
     print(json.dumps(rec), flush=True)
     out.append(rec)
 

@@ -528,6 +528,36 @@ def test_batched_rollout_vs_reference_golden(be, gworld, golden):
                 1.0, np.abs(g[f"roll{k}_acc"]).max())
 
 
+def test_rollout_graph_replay_bitwise(be, c1):
+    """Closed-loop ticks replayed from a captured CUDA graph (16 ticks per
+    graph launch, option "graphs") give bitwise the eager ticks' states."""
+    import paper_2301_08068_b200 as P
+    from paper_2301_08068_b200 import _lib as L
+    from paper_2301_08068_b200.rollout import BatchRolloutConfig, RolloutBatch
+
+    scene, grid, states, dirs = c1
+    starts = np.stack([s.position for s in states[:6]])
+    goals = starts[::-1].copy()
+    cfg = BatchRolloutConfig(params=P.preset("static_map"), dt=0.02, max_time=2.0,
+                             max_accel=20.0, max_range=10.0)
+    outs = []
+    try:
+        for gr in (0, 1):
+            L.call("rmpb_set_option", b"graphs", gr)
+            rb = RolloutBatch(scene, grid, P.RayBundle(dirs[:8192]), starts, goals, cfg)
+            for _ in range(3):  # partial runs: eager head, graph chunks, eager tail
+                rb.run(37)
+            outs.append(rb.result())
+    finally:
+        L.call("rmpb_set_option", b"graphs", 1)
+    a, b = outs
+    assert list(a.outcome) == list(b.outcome)
+    assert np.array_equal(a.steps, b.steps) and np.array_equal(a.n_clamped, b.n_clamped)
+    assert np.array_equal(a.positions, b.positions)
+    assert np.array_equal(a.velocities, b.velocities)
+    assert a.steps.max() > 32
+
+
 def test_k5_dda_bit_exact_vs_cpu_definition(be, oracle, c1):
     """K5 (north_star's DDA over occupancy; not reference parity): occupancy
     bits, entry distances (float32 bits) and hit voxel indices equal the CPU
