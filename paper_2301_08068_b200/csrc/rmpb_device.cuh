@@ -543,14 +543,20 @@ __device__ __forceinline__ void block_reduce(Acc& acc, double* sm) {
 // pinv_psd (rmpnav/core.py:103-115): eigen-decomposition of the symmetric 3x3
 // metric by cyclic Jacobi in fp64; eigenvalues <= 1e-8 * max(lambda_max, 0)
 // are dropped; accel = V diag(1/lambda) V^T Af.
-__device__ inline void jacobi3(double a[3][3], double V[3][3]) {
+__device__ __forceinline__ void jacobi3(double a[3][3], double V[3][3]) {
+#pragma unroll
   for (int i = 0; i < 3; ++i)
+#pragma unroll
     for (int j = 0; j < 3; ++j) V[i][j] = (i == j) ? 1.0 : 0.0;
   for (int sweep = 0; sweep < 32; ++sweep) {
     double off = fabs(a[0][1]) + fabs(a[0][2]) + fabs(a[1][2]);
     double diag = fabs(a[0][0]) + fabs(a[1][1]) + fabs(a[2][2]);
     if (off == 0.0 || off <= 1e-300 || off < 1e-18 * diag) break;
+    // fully unrolled rotations (0,1), (0,2), (1,2): every index is a
+    // compile-time constant, so a and V stay in registers
+#pragma unroll
     for (int p = 0; p < 2; ++p) {
+#pragma unroll
       for (int q = p + 1; q < 3; ++q) {
         double apq = a[p][q];
         if (apq == 0.0) continue;
@@ -558,17 +564,20 @@ __device__ inline void jacobi3(double a[3][3], double V[3][3]) {
         double t = (theta >= 0.0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
         if (!isfinite(theta)) t = 0.5 / theta;  // |theta| huge: t ~ 1/(2 theta)
         double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+#pragma unroll
         for (int k = 0; k < 3; ++k) {  // A <- A J
           double akp = a[k][p], akq = a[k][q];
           a[k][p] = c * akp - s * akq;
           a[k][q] = s * akp + c * akq;
         }
+#pragma unroll
         for (int k = 0; k < 3; ++k) {  // A <- J^T A
           double apk = a[p][k], aqk = a[q][k];
           a[p][k] = c * apk - s * aqk;
           a[q][k] = s * apk + c * aqk;
         }
         a[p][q] = a[q][p] = 0.0;
+#pragma unroll
         for (int k = 0; k < 3; ++k) {  // V <- V J
           double vkp = V[k][p], vkq = V[k][q];
           V[k][p] = c * vkp - s * vkq;
@@ -612,7 +621,9 @@ __device__ inline bool chol_solve3(const double m[9], const double f[3], double 
 __device__ inline void pinv_apply(const double m[9], const double f[3], double out[3]) {
   if (chol_solve3(m, f, out)) return;
   double a[3][3], V[3][3];
+#pragma unroll
   for (int i = 0; i < 3; ++i)
+#pragma unroll
     for (int j = 0; j < 3; ++j) a[i][j] = 0.5 * (m[3 * i + j] + m[3 * j + i]);
   jacobi3(a, V);
   double lam[3] = {a[0][0], a[1][1], a[2][2]};

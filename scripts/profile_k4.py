@@ -28,5 +28,18 @@ for i in range(5):  # post only (no wait / fold / pinv)
 parts = torch.stack([eng.partial(x, v, *balanced_range(n, 8, r)) for r in range(8)])
 for i in range(3):  # fold + pinv kernel of the all-gather path
     eng.resolve(parts)
+# well-conditioned metric (the whole sphere of one 65536-ray bundle, world 1):
+# the fused epilogue's pinv takes the Cholesky path, as after a real C5 fold
+b2 = b200.DeviceBundle(halton_n=65536)
+eng2 = RayPolicyEngine(b200.DeviceGrid(grid.values, grid.origin, grid.resolution), b2,
+                       (88.0, 1.4, 140.0, 1.2, 1e-6, 2.4, 0.2), 10.0)
+for i in range(3):
+    eng2.partial(x, v, 0, 65536)
+for i in range(3):
+    eng2.exchange(x, v, mb, 1000 + i, 0, 65536)
+# split the epilogue: post only, then wait + fold + pinv only (same epoch)
+for i in range(3):
+    eng2.exchange(x, v, mb, 2000 + i, 0, 65536, mode=1)
+    eng2.exchange(x, v, mb, 2000 + i, 0, 65536, mode=2)
 torch.cuda.synchronize()
 print("ok")
