@@ -19,13 +19,14 @@ namespace rmpb {
 // K4 fused: ray-split partial -> peer-memory exchange -> fold -> solve, in the
 // epilogue of the trace kernel (config C5).  Every rank owns
 // one mailbox in its device memory: flags [2][world] (u64 epochs) then slots
-// [2][world][16] doubles, double-buffered on the epoch parity.  The pose's
-// final CTA stores its 13-slot into mailbox[rank] of EVERY rank (NVLink P2P
-// stores through IPC-mapped pointers), fences at system scope, publishes the
-// epoch with a release store, then waits (acquire) for all `world` epochs in
-// its own mailbox and folds the slots in rank order with the reference's
-// pairwise shape (_pool.py:61-72) -- the same result as the all-gather path,
-// identical on every rank.  Parity double-buffering makes reuse safe: a rank
+// [2][world][16] doubles, double-buffered on the epoch parity.  Warp 0 of
+// the pose's final CTA stores the 13-slot into mailbox[rank] of EVERY rank
+// (lane r -> rank r: NVLink P2P stores through IPC-mapped pointers), fences
+// at system scope and publishes the epoch flag (relaxed store after the
+// fence), then polls all `world` flags of its own mailbox (lane r -> flag r),
+// fences, and folds the slots in rank order with the reference's pairwise
+// shape (_pool.py:61-72; lane j -> component j) -- the same result as the
+// all-gather path, identical on every rank.  Parity double-buffering makes reuse safe: a rank
 // can only start epoch e+2 (same parity) after every rank published e+1,
 // i.e. finished reading epoch e.
 constexpr int kMaxPeers = 8;
@@ -127,7 +128,7 @@ struct ExArgs {  // per-call exchange arguments (kernel parameter of the lean ke
 };
 
 struct PoseIO;
-__device__ void exchange_emit(const Acc& s, const PoseIO& io, const ExArgs& xa);
+__device__ void exchange_emit_warp(const Acc& s, const PoseIO& io, const ExArgs& xa);
 
 struct PoseIO {
   const double* __restrict__ x;   // [P][3] positions
@@ -188,9 +189,15 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
   block_reduce(acc, sm);
   if (io.seg_out && threadIdx.x == 0) acc_to_arr(acc, io.seg_out + (size_t)(pose * segs + seg) * kAcc);
   if (segs == 1) {
+    if (EX) {  // warp 0 runs the exchange (lane 0 holds the total)
+      if (threadIdx.x < 32 && io.slot) {
+        exchange_emit_warp(acc, io, *xa);
+        return threadIdx.x == 0;
+      }
+      return false;
+    }
     if (threadIdx.x == 0 && io.slot) {
-      if (EX) exchange_emit(acc, io, *xa);
-      else write_slot(acc, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
+      write_slot(acc, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
       return true;
     }
     return false;
@@ -220,47 +227,66 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
   }
   f.cnt = (int)cnt;
   block_reduce(f, sm);
+  if (EX) {
+    if (threadIdx.x < 32) {
+      if (threadIdx.x == 0) io.tickets[pose] = 0u;  // self-reset
+      exchange_emit_warp(f, io, *xa);
+      return threadIdx.x == 0;
+    }
+    return false;
+  }
   if (threadIdx.x == 0) {
     io.tickets[pose] = 0u;  // self-reset: graph replays / next call start clean
-    if (EX) exchange_emit(f, io, *xa);
-    else write_slot(f, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
+    write_slot(f, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
     return true;
   }
   return false;
 }
 
-// The K4 epilogue (one thread of the pose's final CTA); see PeerEx.
-__device__ void exchange_emit(const Acc& s, const PoseIO& io, const ExArgs& xa) {
+// The K4 epilogue run by warp 0 of the pose's final CTA (lane 0 holds the
+// slot): lane r posts to rank r and polls rank r's flag, lane j < 13 folds
+// component j over the ranks (fixed pairwise order, _pool.py:61-72), lane 0
+// writes the slot and runs the pinv.  The single-thread form serialised ~13
+// us of dependent memory operations per call (scripts/profile_k4.py).
+__device__ void exchange_emit_warp(const Acc& s, const PoseIO& io, const ExArgs& xa) {
+  const unsigned FULL = 0xffffffffu;
+  const int lane = threadIdx.x & 31;
   const PeerEx& ex = *xa.ex;
   const int W = ex.world, par = (int)(xa.epoch & 1ull);
   if (xa.mode & EX_POST) {
-    const double rec[13] = {s.a00, s.a01, s.a02, s.a01, s.a11, s.a12, s.a02, s.a12, s.a22,
-                            s.b0,  s.b1,  s.b2,  (double)s.cnt};
-    for (int r = 0; r < W; ++r) {
-      double* dst = ex.slots[r] + ((size_t)par * W + ex.rank) * kMbox;
+    const double r0[13] = {s.a00, s.a01, s.a02, s.a01, s.a11, s.a12, s.a02, s.a12, s.a22,
+                           s.b0,  s.b1,  s.b2,  (double)s.cnt};
+    double rec[13];
+#pragma unroll
+    for (int j = 0; j < 13; ++j) rec[j] = __shfl_sync(FULL, r0[j], 0);
+    if (lane < W) {
+      double* dst = ex.slots[lane] + ((size_t)par * W + ex.rank) * kMbox;
+#pragma unroll
       for (int j = 0; j < 13; ++j) __stcg(dst + j, rec[j]);
+      fence_acq_rel_sys();  // this slot before its flag
+      st_relaxed_sys(ex.flags[lane] + (size_t)par * W + ex.rank, xa.epoch);
     }
-    fence_acq_rel_sys();  // slots before flags, once for all peers
-    for (int r = 0; r < W; ++r) st_relaxed_sys(ex.flags[r] + (size_t)par * W + ex.rank, xa.epoch);
   }
   if (!(xa.mode & EX_WAIT)) return;
-  const unsigned long long* fl = ex.flags[ex.rank] + (size_t)par * W;
-  const unsigned long long t0 = globaltimer_ns();
   bool ok = true;
-  for (int r = 0; r < W && ok; ++r) {
-    while (ld_relaxed_sys(fl + r) != xa.epoch) {
+  if (lane < W) {
+    const unsigned long long* fl = ex.flags[ex.rank] + (size_t)par * W + lane;
+    const unsigned long long t0 = globaltimer_ns();
+    while (ld_relaxed_sys(fl) != xa.epoch) {
       if (globaltimer_ns() - t0 > 10000000000ull) { ok = false; break; }  // 10 s: a peer is gone
       __nanosleep(32);
     }
+    fence_acq_rel_sys();  // rank `lane`'s slot is visible
   }
-  fence_acq_rel_sys();  // every flag seen: the slots are visible
+  ok = __all_sync(FULL, ok);
+  __syncwarp();  // memory ordering: every lane's loads after every lane's acquire fence
+  double outj = CUDART_NAN;
+  if (ok && lane < 13) outj = fold8(ex.slots[ex.rank] + (size_t)par * W * kMbox + lane, W, kMbox);
   double out[13];
-  if (ok) {
-    for (int j = 0; j < 13; ++j) out[j] = fold8(ex.slots[ex.rank] + (size_t)par * W * kMbox + j, W, kMbox);
-  } else {
-    atomicExch(ex.err, 1u);
-    for (int j = 0; j < 13; ++j) out[j] = CUDART_NAN;
-  }
+#pragma unroll
+  for (int j = 0; j < 13; ++j) out[j] = __shfl_sync(FULL, outj, j);
+  if (lane != 0) return;
+  if (!ok) atomicExch(ex.err, 1u);
   for (int j = 0; j < 13; ++j) io.slot[j] = out[j];
   if (io.accel) {
     double m9[9] = {out[0], out[1], out[2], out[3], out[4], out[5], out[6], out[7], out[8]};
