@@ -181,6 +181,21 @@ struct BrickGrid {
   }
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
     Corners c;
+    if (((ix & 7) < 7) & ((iy & 7) < 7) & ((iz & 7) < 7)) {
+      // all 8 corners in one brick (343 of 512 cells): one table lookup
+      const int sl = __ldg(table + ((ix >> 3) * bny + (iy >> 3)) * bnz + (iz >> 3));
+      if (sl < 0) {
+        const double f = (double)fill;
+        c.v000 = c.v001 = c.v010 = c.v011 = c.v100 = c.v101 = c.v110 = c.v111 = f;
+        return c;
+      }
+      const T* q = pool + (int64_t)sl * 512 + (((ix & 7) << 6) | ((iy & 7) << 3) | (iz & 7));
+      c.v000 = (double)__ldg(q);      c.v001 = (double)__ldg(q + 1);
+      c.v010 = (double)__ldg(q + 8);  c.v011 = (double)__ldg(q + 9);
+      c.v100 = (double)__ldg(q + 64); c.v101 = (double)__ldg(q + 65);
+      c.v110 = (double)__ldg(q + 72); c.v111 = (double)__ldg(q + 73);
+      return c;
+    }
     c.v000 = at(ix, iy, iz);         c.v001 = at(ix, iy, iz + 1);
     c.v010 = at(ix, iy + 1, iz);     c.v011 = at(ix, iy + 1, iz + 1);
     c.v100 = at(ix + 1, iy, iz);     c.v101 = at(ix + 1, iy, iz + 1);
