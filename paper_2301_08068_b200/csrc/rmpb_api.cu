@@ -876,7 +876,7 @@ static void apply_carveout(K* kern) {
 // the persisting L2 carve-out while other traffic (LiDAR streams, the
 // caller's own kernels) streams past it.  The carve-out is sized once per
 // device to the largest map seen (<= cudaDevAttrMaxPersistingL2CacheSize);
-// a window larger than the carve-out gets hitRatio = carve-out / window.
+// maps larger than the carve-out get no window.
 // Option "l2_window" = 0 turns it off (plain launches).
 static bool l2_window_attr(const rmpb_grid* g, cudaLaunchAttribute* a) {
   if (!g_opt_l2_window.load() || !g->d_values || g->bytes <= 0) return false;
@@ -892,8 +892,11 @@ static bool l2_window_attr(const rmpb_grid* g, cudaLaunchAttribute* a) {
     cudaGetLastError();
   }
   if (d.max_win <= 0 || d.max_persist <= 0) return false;
-  const size_t win = std::min<size_t>((size_t)g->bytes, (size_t)d.max_win);
-  const size_t want = std::min<size_t>(win, (size_t)d.max_persist);
+  // a map larger than the carve-out streams anyway: pinning a fraction of it
+  // would only take L2 away from the normal lines (C5's 0.4-3.2 GB maps)
+  if ((size_t)g->bytes > (size_t)d.max_persist || (size_t)g->bytes > (size_t)d.max_win) return false;
+  const size_t win = (size_t)g->bytes;
+  const size_t want = win;
   if (want > d.limit) {
     if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
       cudaGetLastError();
