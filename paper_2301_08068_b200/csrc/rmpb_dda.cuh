@@ -56,10 +56,17 @@ struct DdaResult {
   int steps;        // voxels visited
 };
 
-__device__ __forceinline__ DdaResult dda_ray(const Occupancy& o, float sx, float sy, float sz,
-                                             float dx, float dy, float dz, float max_range) {
-  DdaResult res;
-  res.t = CUDART_INF_F; res.vx = res.vy = res.vz = -1; res.steps = 0;
+// March state of one ray (scalars: indexing per-axis arrays with the
+// data-dependent axis would put them on the stack).
+struct DdaState {
+  int vx, vy, vz, sx, sy, sz;
+  float tmx, tmy, tmz, tdx, tdy, tdz, t, t1;
+};
+
+// Ray set-up of orc_dda_trace; false = the ray misses the grid.
+__device__ __forceinline__ bool dda_setup(const Occupancy& o, float sx, float sy, float sz,
+                                          float dx, float dy, float dz, float max_range,
+                                          DdaState& q) {
   const int n[3] = {o.nx, o.ny, o.nz};
   float u[3], dv[3];
   {
@@ -82,10 +89,10 @@ __device__ __forceinline__ DdaResult dda_ray(const Occupancy& o, float sx, float
       if (ta > t0) t0 = ta;
       if (tb < t1) t1 = tb;
     } else if (u[a] < 0.0f || u[a] >= (float)n[a]) {
-      return res;
+      return false;
     }
   }
-  if (t0 > t1) return res;
+  if (t0 > t1) return false;
   int vox[3], stp[3];
   float tmax[3], tdel[3];
 #pragma unroll
@@ -109,35 +116,48 @@ __device__ __forceinline__ DdaResult dda_ray(const Occupancy& o, float sx, float
       tdel[a] = CUDART_INF_F;
     }
   }
-  // The march keeps every per-axis quantity in scalars: indexing the arrays
-  // with the data-dependent axis would put them on the stack (local memory).
-  // Axis choice, t and the tMax update are those of orc_dda_trace exactly:
-  // a = 0; if (tmax[1] < tmax[a]) a = 1; if (tmax[2] < tmax[a]) a = 2.
-  int vx = vox[0], vy = vox[1], vz = vox[2];
-  const int sx_ = stp[0], sy_ = stp[1], sz_ = stp[2];
-  float tmx = tmax[0], tmy = tmax[1], tmz = tmax[2];
-  const float tdx = tdel[0], tdy = tdel[1], tdz = tdel[2];
-  float t = t0;
+  q.vx = vox[0]; q.vy = vox[1]; q.vz = vox[2];
+  q.sx = stp[0]; q.sy = stp[1]; q.sz = stp[2];
+  q.tmx = tmax[0]; q.tmy = tmax[1]; q.tmz = tmax[2];
+  q.tdx = tdel[0]; q.tdy = tdel[1]; q.tdz = tdel[2];
+  q.t = t0; q.t1 = t1;
+  return true;
+}
+
+// One voxel visit of orc_dda_trace's loop: 1 = hit (q.t is the entry
+// distance), -1 = left the range / grid, 0 = continue.  Axis choice, t and
+// the tMax update are those of orc_dda_trace exactly:
+// a = 0; if (tmax[1] < tmax[a]) a = 1; if (tmax[2] < tmax[a]) a = 2.
+__device__ __forceinline__ int dda_step(const Occupancy& o, DdaState& q) {
+  if (o.occ(q.vx, q.vy, q.vz)) return 1;
+  const bool y_lt = q.tmy < q.tmx;
+  const float m = y_lt ? q.tmy : q.tmx;
+  const bool az = q.tmz < m, ay = !az && y_lt, ax = !az && !y_lt;
+  q.t = az ? q.tmz : m;
+  if (!(q.t <= q.t1)) return -1;
+  q.vx += ax ? q.sx : 0;
+  q.vy += ay ? q.sy : 0;
+  q.vz += az ? q.sz : 0;
+  if (((unsigned)q.vx >= (unsigned)o.nx) | ((unsigned)q.vy >= (unsigned)o.ny) |
+      ((unsigned)q.vz >= (unsigned)o.nz))
+    return -1;
+  q.tmx = ax ? q.tmx + q.tdx : q.tmx;
+  q.tmy = ay ? q.tmy + q.tdy : q.tmy;
+  q.tmz = az ? q.tmz + q.tdz : q.tmz;
+  return 0;
+}
+
+__device__ __forceinline__ DdaResult dda_ray(const Occupancy& o, float sx, float sy, float sz,
+                                             float dx, float dy, float dz, float max_range) {
+  DdaResult res;
+  res.t = CUDART_INF_F; res.vx = res.vy = res.vz = -1; res.steps = 0;
+  DdaState q;
+  if (!dda_setup(o, sx, sy, sz, dx, dy, dz, max_range, q)) return res;
   while (true) {
     ++res.steps;
-    if (o.occ(vx, vy, vz)) {
-      res.t = t; res.vx = vx; res.vy = vy; res.vz = vz;
-      break;
-    }
-    const bool y_lt = tmy < tmx;
-    const float m = y_lt ? tmy : tmx;
-    const bool az = tmz < m, ay = !az && y_lt, ax = !az && !y_lt;
-    t = az ? tmz : m;
-    if (!(t <= t1)) break;
-    vx += ax ? sx_ : 0;
-    vy += ay ? sy_ : 0;
-    vz += az ? sz_ : 0;
-    if (((unsigned)vx >= (unsigned)o.nx) | ((unsigned)vy >= (unsigned)o.ny) |
-        ((unsigned)vz >= (unsigned)o.nz))
-      break;
-    tmx = ax ? tmx + tdx : tmx;
-    tmy = ay ? tmy + tdy : tmy;
-    tmz = az ? tmz + tdz : tmz;
+    const int r = dda_step(o, q);
+    if (r > 0) { res.t = q.t; res.vx = q.vx; res.vy = q.vy; res.vz = q.vz; break; }
+    if (r < 0) break;
   }
   return res;
 }

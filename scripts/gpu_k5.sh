@@ -1,4 +1,4 @@
-# K5 DDA: parity test, then the K5 measurement for each librmpb build given
+# K5 DDA: parity test, then the K5 measurement per librmpb build
 mkdir -p gpurun_out
 timeout 300 python -m pytest tests/test_gpu_parity.py -m gpu -q -x -k "dda" > gpurun_out/dda.log 2>&1
 : > gpurun_out/k5.jsonl
