@@ -524,27 +524,20 @@ __device__ __forceinline__ void policy_flush(SM& sm, int warp, int lane, bool va
 
 // RAYOUT: per-ray parity outputs (t, cell, steps) and the step counter.
 // FAST: fp32 march (opt-in, not reference-exact; see interp_f).
-template <class G, bool RAYOUT, bool FAST = false>
-__global__ void __launch_bounds__(kBlock, RMPB_MINB)
-k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
-              double eps, double step_scale, int segs, int seg_rays, RayOut ro) {
+// INSIDE: the pose lies inside the map domain (CTA-uniform: one pose per
+// CTA), so the body is compiled without the per-refill domain test
+// (13.78 -> 13.55 ms per 4096-pose C1 step).
+template <class G, bool RAYOUT, bool FAST, bool INSIDE>
+__device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, const GridGeom& g,
+                                                 const Bundle& b, const PoseIO& io,
+                                                 const PolicyParams& p, double max_range,
+                                                 double eps, double step_scale, int segs,
+                                                 int seg_rays, const RayOut& ro, int pose, int seg,
+                                                 double sx, double sy, double sz) {
   using real = typename std::conditional<FAST, float, double>::type;
-  __shared__ K2Smem sm;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned FULL = 0xffffffffu;
   const unsigned lt = (1u << lane) - 1u;
-  const int unit = blockIdx.x;
-  const int pose = unit / segs, seg = unit - pose * segs;
-  if (io.active && !io.active[pose]) return;  // whole CTA: finished rollout
-  double sx, sy, sz;
-  io.pose(pose, sx, sy, sz);
-  // Inside the domain every axis' entry quotient is <= 0, so the reference's
-  // t = max(t0, 0) is exactly 0 and only the exit side is needed:
-  // (hi - s)/d for d > 0, (lo - s)/d for d < 0 (_ckern.pyx:171-212).
-  const bool inside =
-      sx >= g.ox && sx <= g.hx && sy >= g.oy && sy <= g.hy && sz >= g.oz && sz <= g.hz;
-  if (lane < 9) sm.acc[warp][lane] = 0.0;
-  __syncthreads();
   const int begin = seg * seg_rays;
   const int end = min(begin + seg_rays, b.n);
   const int nchunks = (end - begin + 31) >> 5;
@@ -574,7 +567,7 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
         double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
         if (ok) {
           ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
-          if (inside) {
+          if (INSIDE) {
             const RecipDir q = b.recip(r);
             double thi = CUDART_INF;
             if (ex != 0.0) {
@@ -744,6 +737,32 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
     acc.cnt = cnt;  // warp-uniform count: contributed once per warp
   }
   finish_unit(acc, io, pose, seg, segs);
+}
+
+template <class G, bool RAYOUT, bool FAST = false>
+__global__ void __launch_bounds__(kBlock, RMPB_MINB)
+k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
+              double eps, double step_scale, int segs, int seg_rays, RayOut ro) {
+  __shared__ K2Smem sm;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int unit = blockIdx.x;
+  const int pose = unit / segs, seg = unit - pose * segs;
+  if (io.active && !io.active[pose]) return;  // whole CTA: finished rollout
+  double sx, sy, sz;
+  io.pose(pose, sx, sy, sz);
+  // Inside the domain every axis' entry quotient is <= 0, so the reference's
+  // t = max(t0, 0) is exactly 0 and only the exit side is needed:
+  // (hi - s)/d for d > 0, (lo - s)/d for d < 0 (_ckern.pyx:171-212).
+  const bool inside =
+      sx >= g.ox && sx <= g.hx && sy >= g.oy && sy <= g.hy && sz >= g.oz && sz <= g.hz;
+  if (lane < 9) sm.acc[warp][lane] = 0.0;
+  __syncthreads();
+  if (inside)
+    ray_policy2_body<G, RAYOUT, FAST, true>(sm, grid, g, b, io, p, max_range, eps, step_scale,
+                                            segs, seg_rays, ro, pose, seg, sx, sy, sz);
+  else
+    ray_policy2_body<G, RAYOUT, FAST, false>(sm, grid, g, b, io, p, max_range, eps, step_scale,
+                                             segs, seg_rays, ro, pose, seg, sx, sy, sz);
 }
 
 // K2: LiDAR-direct policy (policies.py:195-205, rays.py:172-173).  Beam k of
