@@ -48,6 +48,7 @@ struct GridGeom {
   double hx, hy, hz;     // origin + (n-1)*res (the slab bounds)
   double rhi, rlo;       // double-double 1/res for the exact division (exdiv)
   double dx2, dy2, dz2;  // (double)(n - 2): the clamped cell's base
+  int nxm2, nym2, nzm2;  // n - 2: the last cell index (per-step boundary test)
 };
 
 // Exact a / b for a divisor with precomputed yhi = RN(1/b),
@@ -85,6 +86,7 @@ __host__ inline GridGeom make_geom(int64_t nx, int64_t ny, int64_t nz, double ox
   g.hz = oz + (double)(nz - 1) * res;
   recip_dd(res, g.rhi, g.rlo);
   g.dx2 = (double)(nx - 2); g.dy2 = (double)(ny - 2); g.dz2 = (double)(nz - 2);
+  g.nxm2 = (int)nx - 2; g.nym2 = (int)ny - 2; g.nzm2 = (int)nz - 2;
   return g;
 }
 
@@ -262,11 +264,11 @@ __device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, 
   cell_floor(exdiv(py - g.oy, g.res, g.rhi, g.rlo), iy, fy);
   cell_floor(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), iz, fz);
   // one (rarely taken) branch for all three boundary clamps
-  if (((unsigned)ix > (unsigned)(g.nx - 2)) | ((unsigned)iy > (unsigned)(g.ny - 2)) |
-      ((unsigned)iz > (unsigned)(g.nz - 2))) {
-    cell_fix(g.nx - 2, ix, fx);
-    cell_fix(g.ny - 2, iy, fy);
-    cell_fix(g.nz - 2, iz, fz);
+  if (((unsigned)ix > (unsigned)g.nxm2) | ((unsigned)iy > (unsigned)g.nym2) |
+      ((unsigned)iz > (unsigned)g.nzm2)) {
+    cell_fix(g.nxm2, ix, fx);
+    cell_fix(g.nym2, iy, fy);
+    cell_fix(g.nzm2, iz, fz);
   }
   Corners c = grid.load(ix, iy, iz);
   double c00 = c.v000 + fz * (c.v001 - c.v000);
