@@ -39,6 +39,7 @@ static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread pe
 static std::atomic<int64_t> g_opt_carveout{-1};
 static std::atomic<int64_t> g_opt_l2_window{1};  // map access-policy window on trace launches
 static std::atomic<int64_t> g_opt_graphs{1};     // CUDA-graph replay of rollout ticks
+static std::atomic<int64_t> g_opt_lidar_chunks{4};  // v5 pipelined (lidar_kernel = 7): scan chunks
 static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (= 3), 1, 2 (v1/v2), 3 (v3 warp units), 4/5 (v4 TMA-fed, 2 stage sizes), 6 (v5 compact + list policy)
 static std::atomic<int64_t> g_opt_lidar_tma_warps{48000};  // v4: target warp units per launch
 static std::atomic<int64_t> g_opt_lidar_warps{76000};  // v3: target warp units per launch  // shared-memory carveout % for the trace kernel
@@ -141,6 +142,18 @@ struct Workspace {
   size_t tickets_n = 0;
   HostBuf hres;    // pinned + mapped results (slots / accels)
   HostBuf hin;     // pinned staging of host inputs
+  cudaStream_t side = nullptr;  // LiDAR v5 pipeline: list-policy stream (high priority)
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int ensure_side(cudaStream_t st) {
+    if (side) return RMPB_OK;
+    int lo = 0, hi = 0;
+    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
+    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
+    (void)st;
+    return RMPB_OK;
+  }
   int ensure_tickets(size_t n) {
     if (n <= tickets_n) return RMPB_OK;
     TRY(tickets.ensure(n * sizeof(unsigned)));
@@ -322,8 +335,13 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
     g_opt_lidar_tma_warps.store(value);
     return RMPB_OK;
   }
+  if (!strcmp(name, "lidar_chunks")) {
+    if (value < 1 || value > 4096) return fail(RMPB_ERR_INVALID, "lidar_chunks must be 1..4096");
+    g_opt_lidar_chunks.store(value);
+    return RMPB_OK;
+  }
   if (!strcmp(name, "lidar_kernel")) {
-    if (value < 0 || value > 6) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..6");
+    if (value < 0 || value > 7) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..7");
     g_opt_lidar_kernel.store(value);
     return RMPB_OK;
   }
@@ -1491,7 +1509,7 @@ extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double
 template <class Src>
 static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
                              const PolicyParams& pp, double* d_slot, double* d_accel,
-                             Workspace* ws, cudaStream_t st) {
+                             Workspace* ws, cudaStream_t st, bool pipe = false) {
   const int64_t target = g_opt_lidar_warps.load();
   int64_t wps = (target + S_ - 1) / S_;
   wps = std::min<int64_t>(wps, 1024);
@@ -1574,7 +1592,7 @@ static int launch_lidar_tma(Src src, int64_t S_, int64_t n, const double* d_v, d
 template <class Src>
 static int launch_lidar_two(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
                             const PolicyParams& pp, double* d_slot, double* d_accel,
-                            Workspace* ws, cudaStream_t st) {
+                            Workspace* ws, cudaStream_t st, bool pipe = false) {
   const int64_t target = g_opt_lidar_warps.load();
   int64_t wps = (target + S_ - 1) / S_;
   wps = std::min<int64_t>(wps, 1024);
@@ -1600,6 +1618,32 @@ static int launch_lidar_two(Src src, int64_t S_, int64_t n, const double* d_v, d
   io.tickets = (unsigned*)ws->tickets.p;
   const long long blocks = (nunits + kWarps - 1) / kWarps;
   if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
+  // lidar_kernel = 7: pipeline the two phases over scan chunks.  Compact of
+  // chunk c+1 (HBM stream) runs on `st` while the list policy of chunk c
+  // (fp64 chains) runs on a high-priority side stream forked / joined by
+  // events, so the byte stream hides under the policy.  Chunks are whole
+  // scans and every unit still owns its list region: the per-unit work and
+  // the per-scan fold order are those of the one-shot launch (bitwise equal).
+  const int64_t chunks = pipe ? std::min<int64_t>(g_opt_lidar_chunks.load(), S_) : 1;
+  if (chunks > 1) {
+    TRY(ws->ensure_side(st));
+    const int64_t spc = (S_ + chunks - 1) / chunks;
+    for (int64_t s0 = 0; s0 < S_; s0 += spc) {
+      const long long a0 = (long long)s0 * wps;
+      const long long a1 = (long long)std::min<int64_t>(s0 + spc, S_) * wps;
+      const unsigned cb = (unsigned)((a1 - a0 + kWarps - 1) / kWarps);
+      k_lidar_compact<Src><<<cb, kBlock, 0, st>>>(src, pp, (int)wps, (int)seg, a1, ld, li, uc, a0);
+      CKL();
+      CK(cudaEventRecord(ws->ev_fork, st));
+      CK(cudaStreamWaitEvent(ws->side, ws->ev_fork, 0));
+      k_lidar_listpolicy<Src><<<cb, kBlock, 0, ws->side>>>(src, io, pp, (int)wps, (int)seg, a1,
+                                                          ld, li, uc, a0);
+      CKL();
+    }
+    CK(cudaEventRecord(ws->ev_join, ws->side));
+    CK(cudaStreamWaitEvent(st, ws->ev_join, 0));
+    return RMPB_OK;
+  }
   k_lidar_compact<Src><<<(unsigned)blocks, kBlock, 0, st>>>(src, pp, (int)wps, (int)seg, nunits,
                                                            ld, li, uc);
   CKL();
@@ -1623,10 +1667,10 @@ static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
     src.sc = sc;
     return launch_lidar_tma<LatticeTma<2>, 2, 2>(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
   }
-  if (kopt == 6) {
+  if (kopt == 6 || kopt == 7) {
     LatticeSrc src{};
     src.sc = sc;
-    return launch_lidar_two(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+    return launch_lidar_two(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st, kopt == 7);
   }
   if (kopt == 0 || kopt == 3) {
     LatticeSrc src{};
@@ -1753,10 +1797,10 @@ static int points_launch(PointsIO pt, int64_t S_, const double* d_v, double v0[3
     src.pt = pt;
     return launch_lidar_tma<PointTma<2>, 2, 2>(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
   }
-  if (kopt == 6) {
+  if (kopt == 6 || kopt == 7) {
     PointSrc src{};
     src.pt = pt;
-    return launch_lidar_two(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+    return launch_lidar_two(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st, kopt == 7);
   }
   if (kopt == 0 || kopt == 3) {
     PointSrc src{};

@@ -1513,10 +1513,11 @@ __device__ __forceinline__ void compact_group(const double (&cur)[4], int base, 
 template <class Src>
 __global__ void __launch_bounds__(kBlock, RMPB_COMPACT_MINB)
 k_lidar_compact(Src src, PolicyParams p, int wps, int seg, long long nunits,
-                double* __restrict__ ld, int* __restrict__ li, int2* __restrict__ ucnt) {
+                double* __restrict__ ld, int* __restrict__ li, int2* __restrict__ ucnt,
+                long long u0 = 0) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned lt = (1u << lane) - 1u;
-  const long long unit = (long long)blockIdx.x * kWarps + warp;
+  const long long unit = u0 + (long long)blockIdx.x * kWarps + warp;  // units [u0, nunits)
   if (unit >= nunits) return;
   const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
   src.bind(scan);
@@ -1551,11 +1552,11 @@ template <class Src>
 __global__ void __launch_bounds__(kBlock, 4)
 k_lidar_listpolicy(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits,
                    const double* __restrict__ ld, const int* __restrict__ li,
-                   const int2* __restrict__ ucnt) {
+                   const int2* __restrict__ ucnt, long long u0 = 0) {
   __shared__ ListSmem smw[kWarps];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const long long unit = (long long)blockIdx.x * kWarps + warp;
+  const long long unit = u0 + (long long)blockIdx.x * kWarps + warp;  // units [u0, nunits)
   if (unit >= nunits) return;
   const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
   ListSmem& w = smw[warp];

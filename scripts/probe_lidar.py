@@ -28,8 +28,11 @@ LIDAR = (1.2, 1.5, 3.0, 1.0, 1e-6, 1.3, 1.0)
 out, ref = {}, None
 # args: "2" (kernel 2) or "3:19000" (kernel 3, target warp units)
 for arg in sys.argv[1:] or ["2", "3"]:
-    k, _, wt = arg.partition(":")
+    arg0, _, ch = arg.partition("/")  # "7/8": kernel 7 with 8 scan chunks
+    k, _, wt = arg0.partition(":")
     k = int(k)
+    if ch:
+        _lib.call("rmpb_set_option", b"lidar_chunks", int(ch))
     _lib.call("rmpb_set_option", b"lidar_kernel", k)
     if wt:
         _lib.call("rmpb_set_option", b"lidar_tma_warps" if k in (4, 5) else b"lidar_warps", int(wt))

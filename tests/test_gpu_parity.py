@@ -700,10 +700,11 @@ def test_lidar_points_batch_device(be, oracle, c1):
 
 
 # 1: per-thread, 2: CTA streaming, 3: warp units, 4 / 5: TMA-fed warp units
-# (two stage sizes); 6: compact + list policy (two kernels); 14: variant 4 with long warp units (3 per launch:
+# (two stage sizes); 6: compact + list policy (two kernels); 7: variant 6
+# pipelined over scan chunks on two streams (bitwise variant 6); 14: variant 4 with long warp units (3 per launch:
 # many groups per warp, so the stage ring wraps and the mbarrier parity flips)
-LIDAR_VARIANTS = (1, 2, 3, 4, 5, 6, 14)
-LIDAR_VARIANTS_PTS = (1, 3, 4, 5, 6, 14)
+LIDAR_VARIANTS = (1, 2, 3, 4, 5, 6, 7, 14)
+LIDAR_VARIANTS_PTS = (1, 3, 4, 5, 6, 7, 14)
 
 
 @pytest.mark.parametrize("n,S", [(131072, 1), (1000, 5), (131, 3), (97, 2), (4096, 40), (8192, 3)])
@@ -744,6 +745,7 @@ def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
                     _lib.call("rmpb_set_option", b"lidar_tma_warps", 3 if k >= 10 else 48000)
                     sl, ac = lidar_policy_batch_device(d_dirs, d_R, d_rg, d_vl, d_v, LIDAR, 0.3)
                     outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
+                assert np.array_equal(outs[6][0], outs[7][0], equal_nan=True)
                 for s in range(S):
                     wd = dirs @ Rs[s].T if use_R else dirs
                     vv = valid[s] if use_valid else np.ones(n, bool)
@@ -785,6 +787,7 @@ def test_lidar_points_kernels_ragged(be, oracle, n, S):
                 sl, ac = lidar_points_batch_device(torch.from_numpy(pts).cuda(), d_R,
                                                    torch.from_numpy(v).cuda(), LIDAR, 0.3)
                 outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
+            assert np.array_equal(outs[6][0], outs[7][0], equal_nan=True)
             for s in range(S):
                 p64 = pts[s].astype(np.float64)
                 r = np.sqrt((p64 * p64).sum(1))
