@@ -1038,8 +1038,11 @@ struct PointSrc {
   }
 };
 
+#ifndef RMPB_LIDAR_MINB
+#define RMPB_LIDAR_MINB 4
+#endif
 template <class Src>
-__global__ void __launch_bounds__(kBlock, 4)
+__global__ void __launch_bounds__(kBlock, RMPB_LIDAR_MINB)
 k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits) {
   extern __shared__ __align__(16) unsigned char lidar_dsm[];  // kWarps x LidarWarpSmem
   LidarWarpSmem* smw = reinterpret_cast<LidarWarpSmem*>(lidar_dsm);
@@ -1549,7 +1552,7 @@ struct ListSmem {
 };
 
 template <class Src>
-__global__ void __launch_bounds__(kBlock, 4)
+__global__ void __launch_bounds__(kBlock, RMPB_LIDAR_MINB)
 k_lidar_listpolicy(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits,
                    const double* __restrict__ ld, const int* __restrict__ li,
                    const int2* __restrict__ ucnt, long long u0 = 0) {
