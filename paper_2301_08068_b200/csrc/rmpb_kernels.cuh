@@ -962,6 +962,16 @@ struct PointsIO {
 };
 
 
+// Bulk L2 prefetch (cp.async.bulk.prefetch.L2): 16-B aligned address, size a
+// multiple of 16.  Non-binding; the data are read later by ordinary loads.
+__device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+#ifndef RMPB_LIDAR_PF
+#define RMPB_LIDAR_PF 0  // groups of 128 beams prefetched ahead into L2 (0 = off)
+#endif
+
 // Beam sources of the warp-unit kernel: a lattice scan (sensor directions +
 // ranges + validity, policies.py:195-205) or raw sensor-frame points (K2b).
 struct LatticeSrc {
@@ -1001,6 +1011,13 @@ struct LatticeSrc {
   __device__ __forceinline__ void dir(int i, double, double& ex, double& ey, double& ez) const {
     ex = sc.dirs[3 * i]; ey = sc.dirs[3 * i + 1]; ez = sc.dirs[3 * i + 2];
   }
+  // L2 prefetch of the 128-beam group at i0 (one bulk prefetch per array;
+  // issued by one lane, no registers held): aligned full groups only
+  __device__ __forceinline__ void prefetch(int i0, int end) const {
+    if (!vec || i0 + 128 > end) return;
+    l2_prefetch(rg + i0, 128 * sizeof(double));
+    if (vl && ((reinterpret_cast<uintptr_t>(vl + i0) & 15) == 0)) l2_prefetch(vl + i0, 128);
+  }
 };
 
 struct PointSrc {
@@ -1036,6 +1053,10 @@ struct PointSrc {
   __device__ __forceinline__ void dir(int i, double d, double& ex, double& ey, double& ez) const {
     ex = (double)P[3 * i] / d; ey = (double)P[3 * i + 1] / d; ez = (double)P[3 * i + 2] / d;
   }
+  __device__ __forceinline__ void prefetch(int i0, int end) const {
+    if (!vec || i0 + 128 > end) return;
+    l2_prefetch(P + 3 * (size_t)i0, 128 * 12);
+  }
 };
 
 #ifndef RMPB_LIDAR_MINB
@@ -1063,6 +1084,8 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
   const int end = min(begin + seg, src.count());
   int h1 = 0, q1n = 0, h2 = 0, q2n = 0, cnt = 0;
   int base = begin;
+  if (RMPB_LIDAR_PF > 1 && lane > 0 && lane < RMPB_LIDAR_PF)  // the first groups
+    src.prefetch(base + lane * 128, end);
   __syncwarp();
   while (true) {
     const bool draining = base >= end;
@@ -1070,6 +1093,7 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
       // ---- stream one group, then count + push the in-radius beams to
       // ring 1 (no flush here).  (Prefetching the next group into registers
       // measured slower: 0.58 vs 0.50 ms on C3 -- more spills.)
+      if (RMPB_LIDAR_PF > 0 && lane == 0) src.prefetch(base + RMPB_LIDAR_PF * 128, end);
       double cur[4];
       src.load4(base + 4 * lane, end, cur);
 #pragma unroll
