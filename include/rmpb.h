@@ -70,7 +70,7 @@ enum {
 enum { RMPB_F32 = 0, RMPB_F64 = 1 };                              /* value dtypes */
 enum { RMPB_STORE_AUTO = 0, RMPB_STORE_F32 = 1, RMPB_STORE_F64 = 2 }; /* grid storage */
 enum { RMPB_LAYOUT_LINEAR = 0, RMPB_LAYOUT_QUAD = 1, RMPB_LAYOUT_BRICK = 2,
-       RMPB_LAYOUT_QUADB = 3, RMPB_LAYOUT_PAIR64 = 4, RMPB_LAYOUT_AUTO = -1 };
+       RMPB_LAYOUT_PAIR64 = 4, RMPB_LAYOUT_AUTO = -1 };
 enum { RMPB_ORDER_IDENTITY = 0, RMPB_ORDER_MORTON = 1 };          /* bundle evaluation order */
 /* EXACT: bit-identical to the reference (fp64, its operation order).  FAST:
  * fp32 march with FMA, opt-in, NOT reference-exact (grazing rays may differ;
@@ -110,6 +110,16 @@ RMPB_EXPORT int rmpb_grid_create_brick(const void* values, int dtype, int64_t nx
                            int storage, int device, rmpb_grid** out);
 /* Re-upload values into an existing grid (same shape); invalidates caches. */
 RMPB_EXPORT int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype);
+/* Overwrite the node sub-box [i0, i0+ni) x [j0, j0+nj) x [k0, k0+nk) of an
+ * existing LINEAR / QUAD / PAIR64 grid with `values` (f64, C-order, ni*nj*nk)
+ * in place: only those nodes cross PCIe.  RMPB_ERR_UNSUPPORTED (grid left
+ * unchanged) for a BRICK grid or an f32 grid and values that are not
+ * f32-exact: recreate the grid then.  Synchronous; the caller orders it
+ * after in-flight launches that read the grid.  Replaces the reference's
+ * in-place edit of EsdfGrid.values (rmpnav/geometry.py:215-240, re-read by
+ * every grid_trace call, rmpnav/_kernels/ckern.py:49-62). */
+RMPB_EXPORT int rmpb_grid_update_region(rmpb_grid* g, const void* values, int dtype, int64_t i0,
+                                        int64_t j0, int64_t k0, int64_t ni, int64_t nj, int64_t nk);
 RMPB_EXPORT int rmpb_grid_info(const rmpb_grid* g, int* storage, int* layout, int64_t* device_bytes,
                    int64_t* allocated_bricks);
 RMPB_EXPORT int rmpb_grid_destroy(rmpb_grid* g);
@@ -245,6 +255,10 @@ RMPB_EXPORT int rmpb_policy_reduce(const double* dirs, const double* dists, int6
                        void* stream);
 /* n symmetric 3x3 matrices (row-major) -> their PSD pseudo-inverses. */
 RMPB_EXPORT int rmpb_pinv_psd(const double* a, int64_t n, double* out, void* stream);
+/* Same with the reference's rcond argument (core.py:103-115: eigenvalues at
+ * or below rcond * max(lambda_max, 0) are dropped); rmpb_pinv_psd = 1e-8. */
+RMPB_EXPORT int rmpb_pinv_psd_rcond(const double* a, int64_t n, double rcond, double* out,
+                                    void* stream);
 
 /* ---- analytic scene + map construction (rows f2-f4) --------------------- */
 /* Scene pack as rmpnav/geometry.py:177-197: kinds (0 sphere, 1 box), ops

@@ -20,9 +20,12 @@ guarantees results independent of it (_pool.py:1-7) and so does this
 backend (fixed reduction order on device).
 
 The reference passes the grid / directions on every call and retains
-nothing.  This backend keeps device copies in small caches
-keyed by buffer address, shape and a strided content fingerprint; call
-``invalidate_caches()`` after mutating a cached array in place.
+nothing.  This backend keeps device copies in small caches:
+deeply read-only arrays (``EsdfGrid.values``, ``RayBundle.directions``) by
+identity -- their content cannot change, and ``EsdfGrid.update`` patches the
+device copies itself; writable arrays by address, re-validated bit for bit
+against a private snapshot on every hit, so an in-place edit is always
+seen.
 """
 
 from __future__ import annotations
@@ -30,7 +33,6 @@ from __future__ import annotations
 import ctypes
 import os
 import threading
-import zlib
 from collections import OrderedDict
 
 import numpy as np
@@ -70,8 +72,14 @@ def _ptr(a) -> int | None:
 
 
 def _f64(a, shape=None):
+    """C-contiguous f64 view / copy; the SAME object when ``a`` already is
+    that with the wanted shape (the device caches compare identities)."""
     a = np.ascontiguousarray(a, dtype=np.float64)
-    return a if shape is None else a.reshape(shape)
+    if shape is None:
+        return a
+    if a.ndim == len(shape) and all(w in (-1, n) for w, n in zip(shape, a.shape)):
+        return a
+    return a.reshape(shape)
 
 
 def _vec3(v):
@@ -123,8 +131,7 @@ class DeviceGrid:
                ctypes.byref(nb), ctypes.byref(nbr))
         self.storage = {L.STORE_F32: "f32", L.STORE_F64: "f64"}[st.value]
         self.layout = {L.LAYOUT_LINEAR: "linear", L.LAYOUT_QUAD: "quad",
-                       L.LAYOUT_BRICK: "brick", L.LAYOUT_QUADB: "quadb",
-                       L.LAYOUT_PAIR64: "pair64"}[lay.value]
+                       L.LAYOUT_BRICK: "brick", L.LAYOUT_PAIR64: "pair64"}[lay.value]
         self.device_bytes = int(nb.value)
         self.bricks = int(nbr.value)
 
@@ -243,7 +250,8 @@ class DeviceOccupancy:
         t = np.empty(n, np.float32)
         vox = np.empty((n, 3), np.int32)
         steps = np.empty(n, np.int32)
-        L.call("rmpb_dda_trace", self.handle, d.ctypes.data, n, _vec3(start).ctypes.data,
+        s = _vec3(start)  # named: a temporary's buffer would be freed before the call
+        L.call("rmpb_dda_trace", self.handle, d.ctypes.data, n, s.ctypes.data,
                float(max_range), t.ctypes.data, vox.ctypes.data, steps.ctypes.data, None)
         return t, vox, steps
 
@@ -295,31 +303,32 @@ _bundles: "OrderedDict[tuple, tuple]" = OrderedDict()
 _scenes: "OrderedDict[int, tuple]" = OrderedDict()
 
 
-def _fingerprint(a: np.ndarray) -> int:
-    """Cheap content check for cache hits: crc32 of 8 cache lines spread over
-    the array plus both ends (a few cache misses, not a scan).  An in-place
-    edit that touches none of them is not seen -- call invalidate_caches()
-    after mutating a cached array."""
-    flat = a.reshape(-1)
-    n = flat.shape[0]
-    if n <= 512:
-        return zlib.crc32(flat)
-    step = n // 8
-    h = zlib.crc32(flat[-8:])
-    for k in range(8):
-        h = zlib.crc32(flat[k * step:k * step + 8], h)
-    return h
-
-
 def _frozen(a: np.ndarray) -> bool:
     """True when neither the array nor any base it views is writable (e.g.
-    RayBundle.directions from sample_directions): its content cannot change
-    through NumPy, so the cache needs no content check."""
+    EsdfGrid.values, RayBundle.directions): its content cannot change through
+    NumPy, so a cache hit needs no content check."""
     while isinstance(a, np.ndarray):
         if a.flags.writeable:
             return False
         a = a.base
-    return a is None or isinstance(a, (bytes,))
+    return True
+
+
+def _bits(a: np.ndarray) -> np.ndarray:
+    """Unsigned-integer view of a contiguous array (bitwise compare, NaN-safe)."""
+    return a.reshape(-1).view({8: np.uint64, 4: np.uint32, 2: np.uint16, 1: np.uint8}[a.itemsize])
+
+
+def _same_content(a: np.ndarray, snap) -> bool:
+    """Writable arrays are re-validated on every cache hit against a private
+    snapshot, bit for bit (one pass over the array: ~3 ms for the 32 MB C1
+    map -- the reference re-reads the whole map on every call too,
+    ckern.py:49-62).  Frozen arrays carry no snapshot."""
+    return snap is None or (a.shape == snap.shape and np.array_equal(_bits(a), _bits(snap)))
+
+
+def _snapshot(a: np.ndarray, frozen: bool):
+    return None if frozen else a.copy()
 
 
 def invalidate_caches() -> None:
@@ -329,49 +338,31 @@ def invalidate_caches() -> None:
         _bundles.clear()
         _scenes.clear()
         _fast.clear()
+        _patterns.clear()
 
 
 # Identity fast path for the control-loop pattern (the same EsdfGrid.values /
 # RayBundle.directions objects passed on every call): id(array) -> entry,
-# valid while the entry holds the array (so the id cannot be reused) and the
-# array still samples the same 72 values the fingerprint hashes.  ~2 us
-# instead of ~12 us for the keyed lookup (ndarray.ctypes alone is ~2 us).
+# valid while the entry holds the array (so the id cannot be reused).  Only
+# deeply frozen arrays take it (their content cannot change behind the cache;
+# EsdfGrid.update patches the device copies itself): ~2 us instead of the
+# keyed lookup.
 _fast: "OrderedDict[int, tuple]" = OrderedDict()
 _FAST_MAX = 16
-_sample_idx_cache: dict = {}
-
-
-def _sample_idx(n: int) -> np.ndarray:
-    idx = _sample_idx_cache.get(n)
-    if idx is None:
-        if n <= 512:
-            idx = np.arange(n, dtype=np.intp)
-        else:
-            step = n // 8
-            idx = np.concatenate([np.arange(k * step, k * step + 8) for k in range(8)] +
-                                 [np.arange(n - 8, n)]).astype(np.intp)
-        _sample_idx_cache[n] = idx
-    return idx
-
-
-def _sample(a: np.ndarray) -> bytes:
-    return a.reshape(-1).take(_sample_idx(a.size)).tobytes()
 
 
 def _fast_get(obj, extra):
     e = _fast.get(id(obj))
     if e is None or e[0] is not obj or e[1] != extra:
         return None
-    if e[2] is not None and _sample(obj) != e[2]:
-        return None
-    return e[3]
+    return e[2]
 
 
-def _fast_put(obj, extra, frozen: bool, dev_obj) -> None:
+def _fast_put(obj, extra, dev_obj) -> None:
     with _lock:
         if len(_fast) >= _FAST_MAX:
             _fast.popitem(last=False)
-        _fast[id(obj)] = (obj, extra, None if frozen else _sample(obj), dev_obj)
+        _fast[id(obj)] = (obj, extra, dev_obj)
 
 
 def device_grid(values, origin, res) -> DeviceGrid:
@@ -385,8 +376,8 @@ def device_grid(values, origin, res) -> DeviceGrid:
         return hit
     g = _device_grid_keyed(values, origin, res)
     if (type(values) is np.ndarray and values.flags.c_contiguous and values.dtype in
-            (np.float64, np.float32)):
-        _fast_put(values, extra, _frozen(values), g)
+            (np.float64, np.float32) and _frozen(values)):
+        _fast_put(values, extra, g)
     return g
 
 
@@ -397,17 +388,47 @@ def _device_grid_keyed(values, origin, res) -> DeviceGrid:
     else:
         v = np.ascontiguousarray(v)
     o = tuple(float(x) for x in np.asarray(origin, dtype=np.float64).reshape(3))
-    key = (v.ctypes.data, v.shape, v.dtype.str, o, float(res), _device, _fingerprint(v))
+    key = (v.ctypes.data, v.shape, v.dtype.str, o, float(res), _device)
     with _lock:
         hit = _grids.get(key)
-        if hit is not None:
+        if hit is not None and hit[1] is v and _same_content(v, hit[2]):
             _grids.move_to_end(key)
             return hit[0]
+        frozen = _frozen(v)
         g = DeviceGrid(v, o, res)
-        _grids[key] = (g, v)  # keep `v` alive so the address stays unique
+        _grids[key] = (g, v, _snapshot(v, frozen))  # `v` alive: the address stays unique
         while len(_grids) > _MAX_GRIDS:
             _grids.popitem(last=False)
         return g
+
+
+def grid_updated(values: np.ndarray, corner, sub: np.ndarray) -> None:
+    """EsdfGrid.update hook: ``values[corner : corner + sub.shape] = sub`` has
+    just been written on the host.  Every cached device copy of ``values`` is
+    patched in place (only the touched nodes cross PCIe; QUAD / LINEAR /
+    PAIR64 layouts); a copy that cannot take the patch (a BRICK map, or f32
+    storage and values that are not f32-exact) is dropped and re-uploaded on
+    its next use."""
+    sub = np.ascontiguousarray(sub, dtype=np.float64)
+    i0, j0, k0 = (int(c) for c in corner)
+    ni, nj, nk = sub.shape
+    with _lock:
+        targets = []
+        for k, e in list(_fast.items()):
+            if e[0] is values:
+                targets.append(("fast", k, e[2]))
+        for k, e in list(_grids.items()):
+            if e[1] is values:
+                targets.append(("keyed", k, e[0]))
+        done = {}
+        for kind, k, g in targets:
+            ok = done.get(id(g))
+            if ok is None:
+                st = L.load().rmpb_grid_update_region(g.handle, sub.ctypes.data, L.RMPB_F64,
+                                                      i0, j0, k0, ni, nj, nk)
+                ok = done[id(g)] = st == 0
+            if not ok:
+                (_fast if kind == "fast" else _grids).pop(k, None)
 
 
 def device_bundle(dirs) -> DeviceBundle:
@@ -418,21 +439,21 @@ def device_bundle(dirs) -> DeviceBundle:
         return hit
     b = _device_bundle_keyed(dirs)
     if (type(dirs) is np.ndarray and dirs.flags.c_contiguous and dirs.dtype == np.float64 and
-            dirs.ndim == 2 and dirs.shape[1] == 3):
-        _fast_put(dirs, _device, _frozen(dirs), b)
+            dirs.ndim == 2 and dirs.shape[1] == 3 and _frozen(dirs)):
+        _fast_put(dirs, _device, b)
     return b
 
 
 def _device_bundle_keyed(dirs) -> DeviceBundle:
     d = _f64(dirs, (-1, 3))
-    key = (d.ctypes.data, d.shape[0], _device, 0 if _frozen(d) else _fingerprint(d))
+    key = (d.ctypes.data, d.shape[0], _device)
     with _lock:
         hit = _bundles.get(key)
-        if hit is not None:
+        if hit is not None and hit[1] is d and _same_content(d, hit[2]):
             _bundles.move_to_end(key)
             return hit[0]
         b = DeviceBundle(d)
-        _bundles[key] = (b, d)
+        _bundles[key] = (b, d, _snapshot(d, _frozen(d)))
         while len(_bundles) > _MAX_BUNDLES:
             _bundles.popitem(last=False)
         return b
@@ -442,9 +463,9 @@ def register_bundle(dirs: np.ndarray, dev: DeviceBundle) -> None:
     """Associate a host direction array with an existing device bundle (e.g.
     one generated on device) so later calls do not re-upload it."""
     d = _f64(dirs, (-1, 3))
-    key = (d.ctypes.data, d.shape[0], dev.device, 0 if _frozen(d) else _fingerprint(d))
+    key = (d.ctypes.data, d.shape[0], dev.device)
     with _lock:
-        _bundles[key] = (dev, d)
+        _bundles[key] = (dev, d, _snapshot(d, _frozen(d)))
         while len(_bundles) > _MAX_BUNDLES:
             _bundles.popitem(last=False)
 
@@ -532,27 +553,32 @@ def policy_reduce(dirs: np.ndarray, dists: np.ndarray, v, params: tuple, min_ran
     if r.shape[0] != d.shape[0]:
         raise ValueError(f"dirs ({d.shape[0]}) and dists ({r.shape[0]}) lengths differ")
     slot = np.empty(13)
-    L.call("rmpb_policy_reduce", d.ctypes.data, r.ctypes.data, d.shape[0], _vec3(v).ctypes.data,
-           _params(params).ctypes.data, float(min_range), slot.ctypes.data, None)
+    va, pa = _vec3(v), _params(params)  # named: kept alive across the call
+    L.call("rmpb_policy_reduce", d.ctypes.data, r.ctypes.data, d.shape[0], va.ctypes.data,
+           pa.ctypes.data, float(min_range), slot.ctypes.data, None)
     return slot[0:9].reshape(3, 3).copy(), slot[9:12].copy(), int(slot[12])
 
 
 # --------------------------------------------------------------------------
 # fused / batched entries (beyond the reference protocol)
 
-_param_cache: dict = {}
+_param_cache: "OrderedDict[tuple, tuple]" = OrderedDict()
 
 
 def _params_cached(params):
-    """(array, pointer) of the 7 params; cached for hashable params."""
+    """(array, pointer) of the 7 params; LRU-cached for hashable params.
+    The CALLER must keep the returned array alive until the C call returns
+    (the pointer alone does not own the buffer)."""
     key = tuple(params) if not isinstance(params, np.ndarray) else None
     if key is not None:
-        hit = _param_cache.get(key)
-        if hit is None:
-            a = _params(params)
-            hit = (a, a.ctypes.data)
-            if len(_param_cache) < 64:
+        with _lock:
+            hit = _param_cache.get(key)
+            if hit is None:
+                a = _params(params)
+                hit = (a, a.ctypes.data)
                 _param_cache[key] = hit
+                while len(_param_cache) > 64:
+                    _param_cache.popitem(last=False)
         return hit
     a = _params(params)
     return a, a.ctypes.data
@@ -587,10 +613,12 @@ def ray_policy_fused(values, origin, res, start, velocity, dirs, params, max_ran
         t = np.empty(b.n)
         cells = np.empty((b.n, 3), np.int32)
         steps = np.empty(b.n, np.int32)
+    pa, pptr = _params_cached(params)  # `pa` keeps the buffer alive across the call
     L.check(L.load().rmpb_ray_policy(
-        g.handle, b.handle, base, base + 24, _params_cached(params)[1],
+        g.handle, b.handle, base, base + 24, pptr,
         float(max_range), float(eps), float(step_scale), optr, optr + 104,
         _ptr(t), _ptr(cells), _ptr(steps), None), "rmpb_ray_policy")
+    del pa
     out = out.copy()
     slot, acc = out[:13], out[13:]
     if with_rays:
@@ -612,8 +640,9 @@ def ray_policy_batch(values, origin, res, positions, velocities, dirs, params, m
     acc = np.empty((P, 3))
     if P == 0:
         return slots, acc
+    pa = _params(params)
     L.call("rmpb_ray_policy_batch", g.handle, b.handle, x.ctypes.data, v.ctypes.data, P,
-           _params(params).ctypes.data, float(max_range), float(eps), float(step_scale),
+           pa.ctypes.data, float(max_range), float(eps), float(step_scale),
            slots.ctypes.data, acc.ctypes.data, None)
     return slots, acc
 
@@ -635,14 +664,15 @@ def lidar_policy_fused(dirs, R, ranges, valid, velocity, params, min_range):
     Rm = None if R is None else _f64(R, (3, 3))
     slot = np.empty(13)
     acc = np.empty(3)
-    if not d.flags.writeable and n >= 4096:
+    va, pa = _vec3(velocity), _params(params)
+    if _frozen(d) and n >= 4096:
         pat = device_bundle_identity(d)
         L.call("rmpb_lidar_policy_bundle", pat.handle, _ptr(Rm), r.ctypes.data, _ptr(vl),
-               _vec3(velocity).ctypes.data, _params(params).ctypes.data, float(min_range),
+               va.ctypes.data, pa.ctypes.data, float(min_range),
                slot.ctypes.data, acc.ctypes.data, None)
     else:
         L.call("rmpb_lidar_policy", d.ctypes.data, _ptr(Rm), r.ctypes.data, _ptr(vl), n,
-               _vec3(velocity).ctypes.data, _params(params).ctypes.data, float(min_range),
+               va.ctypes.data, pa.ctypes.data, float(min_range),
                slot.ctypes.data, acc.ctypes.data, None)
     return slot, acc
 
@@ -653,13 +683,13 @@ _patterns: "OrderedDict[tuple, tuple]" = OrderedDict()
 def device_bundle_identity(d: np.ndarray) -> DeviceBundle:
     """Read-only sensor lattices (rays.py:176-191 caches them read-only) are
     kept on device so a scan call only moves ranges + validity."""
-    key = (d.ctypes.data, d.shape[0], _device, _fingerprint(d))
+    key = (d.ctypes.data, d.shape[0], _device)
     with _lock:
         hit = _patterns.get(key)
-        if hit is not None:
+        if hit is not None and hit[1] is d and _same_content(d, hit[2]):
             return hit[0]
         b = DeviceBundle(d, order=L.ORDER_IDENTITY)
-        _patterns[key] = (b, d)
+        _patterns[key] = (b, d, _snapshot(d, _frozen(d)))
         while len(_patterns) > 8:
             _patterns.popitem(last=False)
         return b
@@ -675,16 +705,17 @@ def lidar_points_fused(xyz, R, velocity, params, min_range):
         slot[:] = 0.0
         acc[:] = 0.0
         return slot, acc
-    L.call("rmpb_lidar_points", p.ctypes.data, _ptr(Rm), p.shape[0], _vec3(velocity).ctypes.data,
-           _params(params).ctypes.data, float(min_range), slot.ctypes.data, acc.ctypes.data, None)
+    va, pa = _vec3(velocity), _params(params)
+    L.call("rmpb_lidar_points", p.ctypes.data, _ptr(Rm), p.shape[0], va.ctypes.data,
+           pa.ctypes.data, float(min_range), slot.ctypes.data, acc.ctypes.data, None)
     return slot, acc
 
 
-def pinv_psd(a) -> np.ndarray:
+def pinv_psd(a, rcond: float = 1e-8) -> np.ndarray:
     """Batch of symmetric 3x3 -> PSD pseudo-inverse on device (core.py:103-115)."""
     m = _f64(a)
     single = m.shape == (3, 3)
     m = m.reshape(-1, 9)
     out = np.empty_like(m)
-    L.call("rmpb_pinv_psd", m.ctypes.data, m.shape[0], out.ctypes.data, None)
+    L.call("rmpb_pinv_psd_rcond", m.ctypes.data, m.shape[0], float(rcond), out.ctypes.data, None)
     return out.reshape(3, 3) if single else out.reshape(-1, 3, 3)

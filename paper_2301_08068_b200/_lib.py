@@ -29,8 +29,7 @@ RMPB_ERR_UNSUPPORTED = -4
 
 RMPB_F32, RMPB_F64 = 0, 1
 STORE_AUTO, STORE_F32, STORE_F64 = 0, 1, 2
-LAYOUT_LINEAR, LAYOUT_QUAD, LAYOUT_BRICK, LAYOUT_QUADB, LAYOUT_PAIR64, LAYOUT_AUTO = \
-    0, 1, 2, 3, 4, -1
+LAYOUT_LINEAR, LAYOUT_QUAD, LAYOUT_BRICK, LAYOUT_PAIR64, LAYOUT_AUTO = 0, 1, 2, 4, -1
 ORDER_IDENTITY, ORDER_MORTON = 0, 1
 MODE_EXACT, MODE_FAST = 0, 1
 
@@ -50,6 +49,7 @@ _SIGS = {
     "rmpb_grid_create_device": (_i, [_vp, _i, _i64, _i64, _i64, _d, _d, _d, _d, _i, _i, _i, _vp]),
     "rmpb_grid_create_brick": (_i, [_vp, _i, _i64, _i64, _i64, _d, _d, _d, _d, _d, _i, _i, _vp]),
     "rmpb_grid_update": (_i, [_vp, _vp, _i]),
+    "rmpb_grid_update_region": (_i, [_vp, _vp, _i, _i64, _i64, _i64, _i64, _i64, _i64]),
     "rmpb_grid_info": (_i, [_vp, _vp, _vp, _vp, _vp]),
     "rmpb_grid_destroy": (_i, [_vp]),
     "rmpb_bundle_create": (_i, [_vp, _i64, _i, _i, _vp]),
@@ -86,6 +86,7 @@ _SIGS = {
     "rmpb_grid_trace": (_i, [_vp, _vp, _i64, _vp, _d, _d, _d, _vp, _vp, _vp, _vp]),
     "rmpb_policy_reduce": (_i, [_vp, _vp, _i64, _vp, _vp, _d, _vp, _vp]),
     "rmpb_pinv_psd": (_i, [_vp, _i64, _vp, _vp]),
+    "rmpb_pinv_psd_rcond": (_i, [_vp, _i64, _d, _vp, _vp]),
     "rmpb_scene_create": (_i, [_vp, _vp, _vp, _vp, _vp, _i64, _d, _i, _vp]),
     "rmpb_scene_destroy": (_i, [_vp]),
     "rmpb_scene_distance": (_i, [_vp, _vp, _i64, _d, _vp, _vp]),

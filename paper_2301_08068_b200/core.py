@@ -83,8 +83,6 @@ class RobotState:
 
 def pinv_psd(a, rcond: float = PINV_RCOND) -> np.ndarray:
     """PSD pseudo-inverse of a symmetric 3x3 (or a stack of them), on device."""
-    if rcond != PINV_RCOND:
-        raise ValueError("the device solver implements rcond = 1e-8 (core.py:26)")
     from ._kernels import get_backend
 
-    return get_backend().pinv_psd(np.asarray(a, dtype=float))
+    return get_backend().pinv_psd(np.asarray(a, dtype=float), float(rcond))

@@ -18,6 +18,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <type_traits>
 #include <utility>
 #include <vector>
 
@@ -39,10 +40,7 @@ static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread pe
 static std::atomic<int64_t> g_opt_carveout{-1};
 static std::atomic<int64_t> g_opt_l2_window{1};  // map access-policy window on trace launches
 static std::atomic<int64_t> g_opt_graphs{1};     // CUDA-graph replay of rollout ticks
-static std::atomic<int64_t> g_opt_lidar_chunks{4};  // v5 pipelined (lidar_kernel = 7): scan chunks
-static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0 auto (= 3), 1, 2 (v1/v2), 3 (v3 warp units), 4/5 (v4 TMA-fed, 2 stage sizes), 6 (v5 compact + list policy)
-static std::atomic<int64_t> g_opt_lidar_tma_warps{48000};  // v4: target warp units per launch
-static std::atomic<int64_t> g_opt_lidar_warps{76000};  // v3: target warp units per launch  // shared-memory carveout % for the trace kernel
+static std::atomic<int64_t> g_opt_lidar_warps{76000};  // LiDAR: target warp units per launch
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -102,6 +100,28 @@ static int current_device(int* dev) {
 }
 
 // ---------------------------------------------------------------------------
+// Device-synchronising calls (cudaFree / cudaFreeHost / cudaDeviceSynchronize)
+// block while a latency server's resident kernel spins on its device.  Every
+// such call in this library goes through these wrappers, which first park
+// the running servers of the current device (stop + wait; the next
+// rmpb_server_eval relaunches them transparently).
+static void park_servers();
+static cudaError_t rfree(void* p) {
+  if (!p) return cudaSuccess;
+  park_servers();
+  return cudaFree(p);
+}
+static cudaError_t rfree_host(void* p) {
+  if (!p) return cudaSuccess;
+  park_servers();
+  return cudaFreeHost(p);
+}
+static cudaError_t rdevsync() {
+  park_servers();
+  return cudaDeviceSynchronize();
+}
+
+// ---------------------------------------------------------------------------
 // workspaces: one per (device, stream), grown on demand, never shrunk.
 
 struct DevBuf {
@@ -109,7 +129,7 @@ struct DevBuf {
   size_t cap = 0;
   int ensure(size_t bytes) {
     if (bytes <= cap) return RMPB_OK;
-    if (p) cudaFree(p);
+    if (p) rfree(p);
     p = nullptr;
     cap = 0;
     size_t want = bytes < 256 ? 256 : bytes + bytes / 4;
@@ -124,7 +144,7 @@ struct HostBuf {  // pinned + mapped (device-visible under UVA)
   size_t cap = 0;
   int ensure(size_t bytes) {
     if (bytes <= cap) return RMPB_OK;
-    if (p) cudaFreeHost(p);
+    if (p) rfree_host(p);
     p = nullptr;
     cap = 0;
     size_t want = bytes < 4096 ? 4096 : bytes + bytes / 4;
@@ -137,23 +157,10 @@ struct HostBuf {  // pinned + mapped (device-visible under UVA)
 struct Workspace {
   std::mutex mu;
   DevBuf in, in2, in3, out, out2, out3, partials;
-  DevBuf lst;      // LiDAR v5 scratch list (compacted in-radius beams)
   DevBuf tickets;  // zeroed on growth
   size_t tickets_n = 0;
   HostBuf hres;    // pinned + mapped results (slots / accels)
   HostBuf hin;     // pinned staging of host inputs
-  cudaStream_t side = nullptr;  // LiDAR v5 pipeline: list-policy stream (high priority)
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-  int ensure_side(cudaStream_t st) {
-    if (side) return RMPB_OK;
-    int lo = 0, hi = 0;
-    CK(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    CK(cudaStreamCreateWithPriority(&side, cudaStreamNonBlocking, hi));
-    CK(cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming));
-    CK(cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming));
-    (void)st;
-    return RMPB_OK;
-  }
   int ensure_tickets(size_t n) {
     if (n <= tickets_n) return RMPB_OK;
     TRY(tickets.ensure(n * sizeof(unsigned)));
@@ -226,16 +233,8 @@ static int with_grid(const rmpb_grid* g, F&& f) {
     PairGridF64 a{(const double2*)g->d_values, G.nz - 1, G.ny * (G.nz - 1)};
     return f(a);
   }
-  if (g->layout == LAYOUT_QUADB) {
-    QuadGridF32B a{(const float4*)g->d_values, (G.ny - 1 + 1) / 2, (G.nz - 1 + 1) / 2};
-    return f(a);
-  }
-  if (g->layout == LAYOUT_QUAD) {
-    if (g->storage == RMPB_STORE_F32) {
-      QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1)};
-      return f(a);
-    }
-    QuadGridF64 a{(const double2*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1)};
+  if (g->layout == LAYOUT_QUAD) {  // f32 storage only (grid_build)
+    QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1)};
     return f(a);
   }
   if (g->storage == RMPB_STORE_F32) {
@@ -330,21 +329,6 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
     g_opt_l2_window.store(value);
     return RMPB_OK;
   }
-  if (!strcmp(name, "lidar_tma_warps")) {
-    if (value < 1) return fail(RMPB_ERR_INVALID, "lidar_tma_warps must be >= 1");
-    g_opt_lidar_tma_warps.store(value);
-    return RMPB_OK;
-  }
-  if (!strcmp(name, "lidar_chunks")) {
-    if (value < 1 || value > 4096) return fail(RMPB_ERR_INVALID, "lidar_chunks must be 1..4096");
-    g_opt_lidar_chunks.store(value);
-    return RMPB_OK;
-  }
-  if (!strcmp(name, "lidar_kernel")) {
-    if (value < 0 || value > 7) return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0..7");
-    g_opt_lidar_kernel.store(value);
-    return RMPB_OK;
-  }
   if (!strcmp(name, "carveout")) {
     if (value < -1 || value > 100) return fail(RMPB_ERR_INVALID, "carveout must be -1..100");
     g_opt_carveout.store(value);
@@ -413,18 +397,18 @@ static int grid_build(rmpb_grid* g, const void* d_src, int dtype, int storage, i
     g->d_values = lin;
     g->bytes = n * esz;
   } else if (layout == LAYOUT_QUAD) {
+    if (store != RMPB_STORE_F32) {  // f64 values: the PAIR64 layout (AUTO picks it)
+      rfree(lin);
+      return fail(RMPB_ERR_UNSUPPORTED, "QUAD layout needs f32-exact values (use PAIR64 / AUTO)");
+    }
     long long nq = g->nx * (g->ny - 1) * (g->nz - 1);
     void* q = nullptr;
     CK(cudaMalloc(&q, nq * 4 * esz));
-    if (store == RMPB_STORE_F32)
-      k_build_quad<float, float4><<<grid_blocks(nq), 256, 0, st>>>(
-          (int)g->nx, (int)g->ny, (int)g->nz, (const float*)lin, (float4*)q);
-    else
-      k_build_quad<double, double2><<<grid_blocks(nq), 256, 0, st>>>(
-          (int)g->nx, (int)g->ny, (int)g->nz, (const double*)lin, (double2*)q);
+    k_build_quad<float, float4><<<grid_blocks(nq), 256, 0, st>>>(
+        (int)g->nx, (int)g->ny, (int)g->nz, (const float*)lin, (float4*)q);
     CKL();
     CK(cudaStreamSynchronize(st));
-    cudaFree(lin);
+    rfree(lin);
     g->d_values = q;
     g->bytes = nq * 4 * esz;
   } else if (layout == LAYOUT_PAIR64) {
@@ -439,26 +423,9 @@ static int grid_build(rmpb_grid* g, const void* d_src, int dtype, int storage, i
                                                             (const double*)lin, (double2*)q);
     CKL();
     CK(cudaStreamSynchronize(st));
-    cudaFree(lin);
+    rfree(lin);
     g->d_values = q;
     g->bytes = np * 16;
-  } else if (layout == LAYOUT_QUADB) {
-    if (store != RMPB_STORE_F32) {
-      cudaFree(lin);
-      return fail(RMPB_ERR_UNSUPPORTED, "QUADB layout needs f32-exact values");
-    }
-    const long long bnx = (g->nx + 1) / 2, bny = (g->ny - 1 + 1) / 2, bnz = (g->nz - 1 + 1) / 2;
-    const long long nq = bnx * bny * bnz * 8;
-    void* q = nullptr;
-    CK(cudaMalloc(&q, nq * 16));
-    CK(cudaMemsetAsync(q, 0, nq * 16, st));
-    k_build_quadb<<<grid_blocks(g->nx * (g->ny - 1) * (g->nz - 1)), 256, 0, st>>>(
-        (int)g->nx, (int)g->ny, (int)g->nz, (int)bny, (int)bnz, (const float*)lin, (float4*)q);
-    CKL();
-    CK(cudaStreamSynchronize(st));
-    cudaFree(lin);
-    g->d_values = q;
-    g->bytes = nq * 16;
   } else {
     return fail(RMPB_ERR_INVALID, "unknown layout %d", layout);
   }
@@ -488,15 +455,15 @@ static int brick_build_t(rmpb_grid* g, const T* d_lin, T fill, cudaStream_t st) 
   int count = 0;
   CK(cudaMemcpyAsync(&count, slot + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
   CK(cudaStreamSynchronize(st));
-  cudaFree(tmp);
+  rfree(tmp);
   const size_t pool_b = (size_t)(count > 0 ? count : 1) * 512 * sizeof(T);
   CK(cudaMalloc(&g->d_values, pool_b));
   CK(cudaMalloc((void**)&g->d_table, (size_t)nb * sizeof(int32_t)));
   k_brick_fill<T><<<nb, 512, 0, st>>>(d_lin, nx, ny, nz, fill, flag, slot, g->d_table, (T*)g->d_values);
   CKL();
   CK(cudaStreamSynchronize(st));
-  cudaFree(flag);
-  cudaFree(slot);
+  rfree(flag);
+  rfree(slot);
   g->layout = LAYOUT_BRICK;
   g->bnx = bnx; g->bny = bny; g->bnz = bnz;
   g->bricks = count;
@@ -538,7 +505,7 @@ static int brick_build(rmpb_grid* g, const void* d_src, int dtype, double fill, 
   k_to_f32<<<grid_blocks(n), 256, 0, st>>>(n, (const double*)d_src, lin);
   CKL();
   int rc = brick_build_t<float>(g, lin, (float)fill, st);
-  cudaFree(lin);
+  rfree(lin);
   return rc;
 }
 
@@ -550,8 +517,8 @@ static int grid_new(const void* values, bool on_device, int dtype, int64_t nx, i
   if (!values) return fail(RMPB_ERR_INVALID, "values is NULL");
   if (dtype != RMPB_F32 && dtype != RMPB_F64) return fail(RMPB_ERR_INVALID, "bad dtype %d", dtype);
   TRY(grid_check_dims(nx, ny, nz, res));
-  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD && layout != LAYOUT_QUADB &&
-      layout != LAYOUT_PAIR64 && layout != RMPB_LAYOUT_AUTO)
+  if (layout != LAYOUT_LINEAR && layout != LAYOUT_QUAD && layout != LAYOUT_PAIR64 &&
+      layout != RMPB_LAYOUT_AUTO)
     return fail(RMPB_ERR_INVALID, "layout %d not valid here (use rmpb_grid_create_brick)", layout);
   DeviceGuard dg(device);
   if (!dg.ok) return fail(RMPB_ERR_CUDA, "cannot select CUDA device %d: %s", device, cudaGetErrorString(dg.err));
@@ -575,7 +542,7 @@ static int grid_new(const void* values, bool on_device, int dtype, int64_t nx, i
   }
   rc = grid_build(g.get(), src, dtype, storage, layout, st);
   cudaStreamSynchronize(st);
-  if (tmp) cudaFree(tmp);
+  if (tmp) rfree(tmp);
   cudaStreamDestroy(st);
   if (rc != RMPB_OK) return rc;
   *out = g.release();
@@ -619,7 +586,7 @@ extern "C" int rmpb_grid_create_brick(const void* values, int dtype, int64_t nx,
     rc = brick_build(g.get(), tmp, dtype, fill, storage, st);
   }
   cudaStreamSynchronize(st);
-  if (tmp) cudaFree(tmp);
+  if (tmp) rfree(tmp);
   cudaStreamDestroy(st);
   if (rc != RMPB_OK) return rc;
   *out = g.release();
@@ -667,7 +634,7 @@ extern "C" int rmpb_bake_grid_tsdf(const rmpb_scene* s, double ox, double oy, do
       rc = grid_build(g.get(), tmp, f32 ? RMPB_F32 : RMPB_F64, storage, layout, st);
   }
   cudaStreamSynchronize(st);
-  if (tmp) cudaFree(tmp);
+  if (tmp) rfree(tmp);
   cudaStreamDestroy(st);
   if (rc != RMPB_OK) return rc;
   *out = g.release();
@@ -690,7 +657,7 @@ extern "C" int rmpb_grid_values(const rmpb_grid* g, double* out) {
     cudaError_t e = cudaMemcpy(out, d, n * sizeof(double), cudaMemcpyDeviceToHost);
     if (e != cudaSuccess) rc = fail(RMPB_ERR_CUDA, "grid values copy: %s", cudaGetErrorString(e));
   }
-  cudaFree(d);
+  rfree(d);
   return rc;
 }
 
@@ -702,13 +669,68 @@ extern "C" int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype) {
   TRY(grid_new(values, false, dtype, g->nx, g->ny, g->nz, g->geom.ox, g->geom.oy, g->geom.oz,
                g->geom.res, RMPB_STORE_AUTO, g->layout, g->device, &fresh));
   DeviceGuard dg(g->device);
-  cudaFree(g->d_values);
+  rfree(g->d_values);
   g->d_values = fresh->d_values;
   g->storage = fresh->storage;
   g->bytes = fresh->bytes;
   fresh->d_values = nullptr;
   delete fresh;
   return RMPB_OK;
+}
+
+extern "C" int rmpb_grid_update_region(rmpb_grid* g, const void* values, int dtype, int64_t i0,
+                                       int64_t j0, int64_t k0, int64_t ni, int64_t nj,
+                                       int64_t nk) {
+  if (!g || !values) return fail(RMPB_ERR_INVALID, "NULL argument");
+  if (dtype != RMPB_F64) return fail(RMPB_ERR_INVALID, "region values must be f64");
+  if (i0 < 0 || j0 < 0 || k0 < 0 || ni < 0 || nj < 0 || nk < 0 || i0 + ni > g->nx ||
+      j0 + nj > g->ny || k0 + nk > g->nz)
+    return fail(RMPB_ERR_INVALID, "region [%lld+%lld, %lld+%lld, %lld+%lld] outside the %lldx%lldx%lld map",
+                (long long)i0, (long long)ni, (long long)j0, (long long)nj, (long long)k0,
+                (long long)nk, (long long)g->nx, (long long)g->ny, (long long)g->nz);
+  int lay;
+  if (g->layout == LAYOUT_LINEAR) lay = 0;
+  else if (g->layout == LAYOUT_QUAD) lay = 1;
+  else if (g->layout == LAYOUT_PAIR64) lay = 2;
+  else return fail(RMPB_ERR_UNSUPPORTED, "region update of layout %d: recreate the grid", g->layout);
+  const long long n = ni * nj * nk;
+  if (n == 0) return RMPB_OK;
+  DeviceGuard dg(g->device);
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  double* d_sub = nullptr;
+  int* d_bad = nullptr;
+  int rc = RMPB_OK, bad = 0;
+  if (cudaMalloc((void**)&d_sub, n * sizeof(double) + 16) != cudaSuccess) {
+    cudaStreamDestroy(st);
+    return fail(RMPB_ERR_NOMEM, "region update alloc");
+  }
+  d_bad = (int*)((char*)d_sub + n * sizeof(double));
+  cudaMemcpyAsync(d_sub, values, n * sizeof(double), cudaMemcpyHostToDevice, st);
+  cudaMemsetAsync(d_bad, 0, sizeof(int), st);
+  if (g->storage == RMPB_STORE_F32 && lay != 2) {  // the new values must stay f32-exact
+    k_check_f32<<<grid_blocks(n), 256, 0, st>>>(n, d_sub, d_bad);
+    g_launches.fetch_add(1);
+    cudaMemcpyAsync(&bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaStreamSynchronize(st);
+    if (bad) rc = fail(RMPB_ERR_UNSUPPORTED, "new values are not f32-exact: recreate the grid");
+  }
+  if (rc == RMPB_OK) {
+    if (g->storage == RMPB_STORE_F32 && lay != 2)
+      k_patch_nodes<float><<<grid_blocks(n), 256, 0, st>>>(lay, (int)g->nx, (int)g->ny, (int)g->nz,
+          (int)i0, (int)j0, (int)k0, (int)ni, (int)nj, (int)nk, d_sub, g->d_values);
+    else
+      k_patch_nodes<double><<<grid_blocks(n), 256, 0, st>>>(lay, (int)g->nx, (int)g->ny, (int)g->nz,
+          (int)i0, (int)j0, (int)k0, (int)ni, (int)nj, (int)nk, d_sub, g->d_values);
+    g_launches.fetch_add(1);
+    cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) rc = fail(RMPB_ERR_CUDA, "k_patch_nodes: %s", cudaGetErrorString(e));
+  }
+  cudaStreamSynchronize(st);
+  rfree(d_sub);
+  cudaStreamDestroy(st);
+  return rc;
 }
 
 extern "C" int rmpb_grid_info(const rmpb_grid* g, int* storage, int* layout, int64_t* bytes,
@@ -724,8 +746,8 @@ extern "C" int rmpb_grid_info(const rmpb_grid* g, int* storage, int* layout, int
 extern "C" int rmpb_grid_destroy(rmpb_grid* g) {
   if (!g) return RMPB_OK;
   DeviceGuard dg(g->device);
-  if (g->d_values) cudaFree(g->d_values);
-  if (g->d_table) cudaFree(g->d_table);
+  if (g->d_values) rfree(g->d_values);
+  if (g->d_table) rfree(g->d_table);
   delete g;
   return RMPB_OK;
 }
@@ -757,7 +779,7 @@ static int bundle_finish(rmpb_bundle* b, cudaStream_t st) {
     CK(cub::DeviceRadixSort::SortPairs(tmp, tmp_bytes, k_in, k_out, i_in, b->d_perm, n, 0, 32, st));
     g_launches.fetch_add(1);
     CK(cudaStreamSynchronize(st));
-    cudaFree(tmp); cudaFree(k_in); cudaFree(k_out); cudaFree(i_in);
+    rfree(tmp); rfree(k_in); rfree(k_out); rfree(i_in);
   }
   k_gather_dirs<<<grid_blocks(n), 256, 0, st>>>(n, b->d_aos, b->d_perm, b->d_dx, b->d_dy, b->d_dz,
                                                 b->d_rcp);
@@ -773,7 +795,7 @@ static int bundle_new(const double* dirs, int64_t n, int order, int device, bool
   if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
   *out = nullptr;
   if (n < 1) return fail(RMPB_ERR_INVALID, "need at least one direction");
-  if (n >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many directions");
+  if (n >= (1LL << 30)) return fail(RMPB_ERR_INVALID, "too many directions (max 2^30)");
   if (!halton && !lat && !dirs) return fail(RMPB_ERR_INVALID, "dirs is NULL");
   if (order != RMPB_ORDER_IDENTITY && order != RMPB_ORDER_MORTON)
     return fail(RMPB_ERR_INVALID, "bad order %d", order);
@@ -803,7 +825,7 @@ static int bundle_new(const double* dirs, int64_t n, int order, int device, bool
     k_soa_to_aos<<<grid_blocks(n), 256, 0, st>>>((int)n, x, y, z, b->d_aos);
     g_launches.fetch_add(1);
     cudaStreamSynchronize(st);
-    cudaFree(x); cudaFree(y); cudaFree(z);
+    rfree(x); rfree(y); rfree(z);
   } else {
     cudaMemcpyAsync(b->d_aos, dirs, n * 3 * sizeof(double), cudaMemcpyHostToDevice, st);
   }
@@ -813,7 +835,7 @@ static int bundle_new(const double* dirs, int64_t n, int order, int device, bool
   cudaStreamDestroy(st);
   if (rc != RMPB_OK) {
     rmpb_bundle* p = b.release();
-    cudaFree(p->d_aos); cudaFree(p->d_dx); cudaFree(p->d_dy); cudaFree(p->d_dz); cudaFree(p->d_perm); cudaFree(p->d_rcp);
+    rfree(p->d_aos); rfree(p->d_dx); rfree(p->d_dy); rfree(p->d_dz); rfree(p->d_perm); rfree(p->d_rcp);
     delete p;
     return rc;
   }
@@ -833,7 +855,7 @@ extern "C" int rmpb_bundle_halton(int64_t n, int order, int device, rmpb_bundle*
 extern "C" int rmpb_bundle_lattice(int64_t rows, int64_t cols, double vfov_deg, int order,
                                    int device, rmpb_bundle** out) {
   if (rows < 1 || cols < 1) return fail(RMPB_ERR_INVALID, "scan pattern needs rows, cols >= 1");
-  if (rows * cols >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many directions");
+  if (rows * cols >= (1LL << 30)) return fail(RMPB_ERR_INVALID, "too many directions (max 2^30)");
   if (!(vfov_deg == vfov_deg)) return fail(RMPB_ERR_INVALID, "vfov is NaN");
   LatticeSpec L;
   L.rows = (int)rows; L.cols = (int)cols; L.vfov = vfov_deg;
@@ -852,9 +874,9 @@ extern "C" int rmpb_bundle_directions(const rmpb_bundle* b, double* out) {
 extern "C" int rmpb_bundle_destroy(rmpb_bundle* b) {
   if (!b) return RMPB_OK;
   DeviceGuard dg(b->device);
-  cudaFree(b->d_aos); cudaFree(b->d_dx); cudaFree(b->d_dy); cudaFree(b->d_dz);
-  cudaFree(b->d_rcp);
-  if (b->d_perm) cudaFree(b->d_perm);
+  rfree(b->d_aos); rfree(b->d_dx); rfree(b->d_dy); rfree(b->d_dz);
+  rfree(b->d_rcp);
+  if (b->d_perm) rfree(b->d_perm);
   delete b;
   return RMPB_OK;
 }
@@ -934,21 +956,42 @@ static bool l2_window_attr(const rmpb_grid* g, cudaLaunchAttribute* a) {
 // Launch `kern` with the map's L2 window when enabled (cudaLaunchKernelEx),
 // else a plain launch.
 template <class... KArgs, class... Args>
-static cudaError_t launch_mapped(const rmpb_grid* g, void (*kern)(KArgs...), unsigned blocks,
-                                 unsigned threads, cudaStream_t st, Args&&... args) {
+static cudaError_t launch_mapped_smem(const rmpb_grid* g, void (*kern)(KArgs...), unsigned blocks,
+                                      unsigned threads, size_t smem, cudaStream_t st,
+                                      Args&&... args) {
+  if (smem > 48 * 1024) {  // opt in once per (kernel, device)
+    static std::mutex mu;
+    static std::map<std::pair<const void*, int>, size_t> done;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    std::lock_guard<std::mutex> lk(mu);
+    size_t& have = done[{(const void*)kern, dev}];
+    if (have < smem) {
+      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           (int)smem);
+      if (e != cudaSuccess) return e;
+      have = smem;
+    }
+  }
   cudaLaunchAttribute attr[1];
   if (l2_window_attr(g, &attr[0])) {
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(blocks);
     cfg.blockDim = dim3(threads);
-    cfg.dynamicSmemBytes = 0;
+    cfg.dynamicSmemBytes = smem;
     cfg.stream = st;
     cfg.attrs = attr;
     cfg.numAttrs = 1;
     return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
   }
-  kern<<<blocks, threads, 0, st>>>(std::forward<Args>(args)...);
+  kern<<<blocks, threads, smem, st>>>(std::forward<Args>(args)...);
   return cudaSuccess;
+}
+
+template <class... KArgs, class... Args>
+static cudaError_t launch_mapped(const rmpb_grid* g, void (*kern)(KArgs...), unsigned blocks,
+                                 unsigned threads, cudaStream_t st, Args&&... args) {
+  return launch_mapped_smem(g, kern, blocks, threads, 0, st, std::forward<Args>(args)...);
 }
 
 static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io, int64_t P,
@@ -966,32 +1009,45 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
   const ExArgs xv = xa ? *xa : ExArgs{nullptr, 0ull, 0};
   return with_grid(g, [&](auto acc) -> int {
     using G = decltype(acc);
+    constexpr bool kFastOk = std::is_same<G, QuadGridF32>::value;  // FAST: f32 QUAD maps only
+    if (mode == RMPB_MODE_FAST && !kFastOk)
+      return fail(RMPB_ERR_UNSUPPORTED, "FAST mode needs an f32 QUAD map");
     if (v2) {
-      apply_carveout(k_ray_policy2<G, true, true>);
-      apply_carveout(k_ray_policy2<G, false, true>);
+      if constexpr (kFastOk) {
+        apply_carveout(k_ray_policy2<G, true, true>);
+        apply_carveout(k_ray_policy2<G, false, true>);
+      }
       apply_carveout(k_ray_policy2<G, true>);
       apply_carveout(k_ray_policy2<G, false>);
     }
-    cudaError_t le;
+    cudaError_t le = cudaSuccess;
     const unsigned nb = (unsigned)units;
-    if (!v2 && xa)
+    const size_t sm8 = sizeof(K2Smem<kTraceWarps>);
+    if (!v2 && xa) {
       le = launch_mapped(g, k_ray_policy<G, true>, nb, kBlock, st, acc, g->geom, bv, io, pp,
                          max_range, eps, step_scale, segs, seg_rays, ro, xv);
-    else if (!v2)
+    } else if (!v2) {
       le = launch_mapped(g, k_ray_policy<G>, nb, kBlock, st, acc, g->geom, bv, io, pp, max_range,
                          eps, step_scale, segs, seg_rays, ro, xv);
-    else if (mode == RMPB_MODE_FAST && ro.step_total)
-      le = launch_mapped(g, k_ray_policy2<G, true, true>, nb, kBlock, st, acc, g->geom, bv, io,
-                         pp, max_range, eps, step_scale, segs, seg_rays, ro);
-    else if (mode == RMPB_MODE_FAST)
-      le = launch_mapped(g, k_ray_policy2<G, false, true>, nb, kBlock, st, acc, g->geom, bv, io,
-                         pp, max_range, eps, step_scale, segs, seg_rays, ro);
-    else if (ro.t || ro.step_total)
-      le = launch_mapped(g, k_ray_policy2<G, true>, nb, kBlock, st, acc, g->geom, bv, io, pp,
-                         max_range, eps, step_scale, segs, seg_rays, ro);
-    else
-      le = launch_mapped(g, k_ray_policy2<G, false>, nb, kBlock, st, acc, g->geom, bv, io, pp,
-                         max_range, eps, step_scale, segs, seg_rays, ro);
+    } else if (mode == RMPB_MODE_FAST) {
+      if constexpr (kFastOk) {
+        if (ro.step_total)
+          le = launch_mapped_smem(g, k_ray_policy2<G, true, true>, nb, kTraceWarps * 32, sm8, st, acc,
+                                  g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays,
+                                  ro);
+        else
+          le = launch_mapped_smem(g, k_ray_policy2<G, false, true>, nb, kTraceWarps * 32, sm8, st, acc,
+                                  g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays,
+                                  ro);
+      }
+    } else if (ro.t || ro.step_total) {
+      le = launch_mapped_smem(g, k_ray_policy2<G, true>, nb, kTraceWarps * 32, sm8, st, acc, g->geom, bv,
+                              io, pp, max_range, eps, step_scale, segs, seg_rays, ro);
+    } else {
+      le = launch_mapped_smem(g, k_ray_policy2<G, false>, nb, kTraceWarps * 32, sm8, st, acc,
+                              g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays,
+                              ro);
+    }
     CK(le);
     CKL();
     return RMPB_OK;
@@ -1213,7 +1269,30 @@ struct rmpb_server {
   unsigned* d_tickets = nullptr;
   unsigned long long epoch = 0;
   bool running = false;
+  std::mutex mu;  // one request at a time; parking waits for it
 };
+
+// Running servers, so device-synchronising calls can park them (rfree).
+static std::mutex g_srv_mu;
+static std::vector<rmpb_server*> g_servers;
+
+// Stop the resident kernels of the servers on the current device (the next
+// rmpb_server_eval relaunches them).  Holds g_srv_mu throughout, so a server
+// cannot be destroyed meanwhile; waits for an in-flight request (s->mu).
+static void park_servers() {
+  int dev = -1;
+  if (cudaGetDevice(&dev) != cudaSuccess) return;
+  std::lock_guard<std::mutex> lk(g_srv_mu);
+  for (rmpb_server* s : g_servers) {
+    if (s->device != dev) continue;
+    std::lock_guard<std::mutex> ls(s->mu);
+    if (!s->running) continue;
+    s->mail->stop = 1;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    cudaStreamSynchronize(s->st);
+    s->running = false;
+  }
+}
 
 static int server_launch(rmpb_server* s) {
   volatile ServerMail* m = s->mail;
@@ -1287,6 +1366,10 @@ extern "C" int rmpb_server_start(const rmpb_grid* g, const rmpb_bundle* b, const
   CK(cudaMalloc((void**)&s->d_tickets, sizeof(unsigned)));
   CK(cudaMemset(s->d_tickets, 0, sizeof(unsigned)));
   TRY(server_launch(s.get()));
+  {
+    std::lock_guard<std::mutex> lk(g_srv_mu);
+    g_servers.push_back(s.get());
+  }
   *out = s.release();
   return RMPB_OK;
 }
@@ -1294,39 +1377,61 @@ extern "C" int rmpb_server_start(const rmpb_grid* g, const rmpb_bundle* b, const
 extern "C" int rmpb_server_eval(rmpb_server* s, const double x[3], const double v[3],
                                 double out_slot[13], double out_accel[3]) {
   if (!s || !x || !v || !out_slot) return fail(RMPB_ERR_INVALID, "NULL argument");
+  std::lock_guard<std::mutex> lk(s->mu);
   volatile ServerMail* m = s->mail;
-  if (!s->running || m->exited) {  // idle timeout ended the loop: relaunch
-    DeviceGuard dg(s->device);
-    CK(cudaStreamSynchronize(s->st));
-    s->running = false;
-    TRY(server_launch(s));
-  }
-  for (int k = 0; k < 3; ++k) { m->x[k] = x[k]; m->v[k] = v[k]; }
-  const unsigned long long e = ++s->epoch;
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  m->req = e;
-  // spin on the result epoch (the device writes it last, after the results)
-  auto t0 = std::chrono::steady_clock::now();
-  unsigned long long spins = 0;
-  while (m->done != e) {
-    if ((++spins & 0xffff) == 0) {
-      if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
-        cudaError_t qe = cudaStreamQuery(s->st);
-        return fail(RMPB_ERR_CUDA, "server did not answer within 5 s (%s)",
-                    qe == cudaErrorNotReady ? "kernel still running" : cudaGetErrorString(qe));
-      }
-      if (m->exited) return fail(RMPB_ERR_CUDA, "server exited while a request was pending");
+  // Two attempts: a request posted just as the idle timeout ended the loop
+  // finds the kernel exited with the request unserved -> relaunch, re-post.
+  for (int attempt = 0; attempt < 2; ++attempt) {
+    if (!s->running || m->exited) {  // idle timeout / parked: relaunch
+      DeviceGuard dg(s->device);
+      CK(cudaStreamSynchronize(s->st));
+      s->running = false;
+      TRY(server_launch(s));
     }
+    for (int k = 0; k < 3; ++k) { m->x[k] = x[k]; m->v[k] = v[k]; }
+    const unsigned long long e = ++s->epoch;
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    m->req = e;
+    // spin on the result epoch (the device writes it last, after the results)
+    auto t0 = std::chrono::steady_clock::now();
+    unsigned long long spins = 0;
+    bool lost = false;
+    while (m->done != e) {
+      if ((++spins & 0xffff) == 0) {
+        if (std::chrono::steady_clock::now() - t0 > std::chrono::seconds(5)) {
+          cudaError_t qe = cudaStreamQuery(s->st);
+          return fail(RMPB_ERR_CUDA, "server did not answer within 5 s (%s)",
+                      qe == cudaErrorNotReady ? "kernel still running" : cudaGetErrorString(qe));
+        }
+        if (m->exited) {
+          std::atomic_thread_fence(std::memory_order_seq_cst);
+          if (m->done == e) break;
+          lost = true;  // exited without serving e
+          break;
+        }
+      }
+    }
+    if (lost) {
+      s->epoch = e - 1;
+      s->running = false;
+      continue;
+    }
+    std::atomic_thread_fence(std::memory_order_seq_cst);
+    for (int k = 0; k < 13; ++k) out_slot[k] = m->slot[k];
+    if (out_accel)
+      for (int k = 0; k < 3; ++k) out_accel[k] = m->accel[k];
+    return RMPB_OK;
   }
-  std::atomic_thread_fence(std::memory_order_seq_cst);
-  for (int k = 0; k < 13; ++k) out_slot[k] = m->slot[k];
-  if (out_accel)
-    for (int k = 0; k < 3; ++k) out_accel[k] = m->accel[k];
-  return RMPB_OK;
+  return fail(RMPB_ERR_CUDA, "server exited twice while a request was pending");
 }
 
 extern "C" int rmpb_server_stop(rmpb_server* s) {
   if (!s) return RMPB_OK;
+  {
+    std::lock_guard<std::mutex> lk(g_srv_mu);
+    g_servers.erase(std::remove(g_servers.begin(), g_servers.end(), s), g_servers.end());
+  }
+  std::unique_lock<std::mutex> ls(s->mu);
   DeviceGuard dg(s->device);
   s->mail->stop = 1;
   std::atomic_thread_fence(std::memory_order_seq_cst);
@@ -1336,6 +1441,7 @@ extern "C" int rmpb_server_stop(rmpb_server* s) {
   cudaFree(s->d_dev);
   cudaFree(s->d_partials);
   cudaFree(s->d_tickets);
+  ls.unlock();
   delete s;
   if (e != cudaSuccess) return fail(RMPB_ERR_CUDA, "server kernel: %s", cudaGetErrorString(e));
   return RMPB_OK;
@@ -1386,7 +1492,7 @@ extern "C" int rmpb_peer_create(int world, int rank, int device, void* ipc_out, 
     static_assert(sizeof(h) == RMPB_IPC_HANDLE_BYTES, "IPC handle size");
     memcpy(ipc_out, &h, sizeof(h));
   }
-  CK(cudaDeviceSynchronize());
+  CK(rdevsync());
   *out = p.release();
   return RMPB_OK;
 }
@@ -1435,11 +1541,11 @@ extern "C" int rmpb_peer_error(rmpb_peer* p, int* timed_out) {
 extern "C" int rmpb_peer_destroy(rmpb_peer* p) {
   if (!p) return RMPB_OK;
   DeviceGuard dg(p->device);
-  cudaDeviceSynchronize();
+  rdevsync();
   for (void* m : p->ipc_mapped) cudaIpcCloseMemHandle(m);
-  cudaFree(p->d_block);
-  cudaFree(p->d_table);
-  cudaFree(p->d_err);
+  rfree(p->d_block);
+  rfree(p->d_table);
+  rfree(p->d_err);
   delete p;
   return RMPB_OK;
 }
@@ -1509,7 +1615,7 @@ extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double
 template <class Src>
 static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
                              const PolicyParams& pp, double* d_slot, double* d_accel,
-                             Workspace* ws, cudaStream_t st, bool pipe = false) {
+                             Workspace* ws, cudaStream_t st) {
   const int64_t target = g_opt_lidar_warps.load();
   int64_t wps = (target + S_ - 1) / S_;
   wps = std::min<int64_t>(wps, 1024);
@@ -1544,158 +1650,12 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
   return RMPB_OK;
 }
 
-// K2 v4 / K2b v2: the TMA-fed warp-unit kernel.  Longer warp units than v3
-// (the stages keep bytes in flight, so fewer, longer-lived warps suffice):
-// target g_opt_lidar_tma_warps units per launch.
-template <class Src, int NST, int GPS>
-static int launch_lidar_tma(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
-                            const PolicyParams& pp, double* d_slot, double* d_accel,
-                            Workspace* ws, cudaStream_t st) {
-  const int64_t target = g_opt_lidar_tma_warps.load();
-  int64_t wps = (target + S_ - 1) / S_;
-  wps = std::min<int64_t>(wps, 1024);
-  wps = std::min<int64_t>(wps, (n + 127) / 128);
-  wps = std::max<int64_t>(wps, 1);
-  const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
-  wps = (n + seg - 1) / seg;
-  const long long nunits = (long long)S_ * wps;
-  if (wps > 1) {
-    TRY(ws->partials.ensure((size_t)nunits * kAcc * sizeof(double)));
-    TRY(ws->ensure_tickets((size_t)S_));
-  }
-  PoseIO io{};
-  io.x = nullptr; io.v = d_v;
-  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
-  io.slot = d_slot; io.accel = d_accel;
-  io.partials = (double*)ws->partials.p;
-  io.tickets = (unsigned*)ws->tickets.p;
-  const long long blocks = (nunits + kWarps - 1) / kWarps;
-  if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
-  const size_t smem = (size_t)kWarps * (NST * (Src::kStage + sizeof(unsigned long long)) +
-                                        sizeof(LidarTmaSmem));
-  static std::once_flag once[64];
-  int dev = 0;
-  CK(cudaGetDevice(&dev));
-  std::call_once(once[dev & 63], [&] {
-    cudaFuncSetAttribute(k_lidar_tma<Src, NST, GPS>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-  });
-  k_lidar_tma<Src, NST, GPS><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps,
-                                                                      (int)seg, nunits);
-  CKL();
-  return RMPB_OK;
-}
-
-// K2 v5 / K2b v3: stream-and-compact kernel + list-policy kernel (see
-// k_lidar_compact).  Same warp units as v3; the scratch list gives every unit
-// its own region of `seg` entries (range f64 + beam index i32).
-template <class Src>
-static int launch_lidar_two(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
-                            const PolicyParams& pp, double* d_slot, double* d_accel,
-                            Workspace* ws, cudaStream_t st, bool pipe = false) {
-  const int64_t target = g_opt_lidar_warps.load();
-  int64_t wps = (target + S_ - 1) / S_;
-  wps = std::min<int64_t>(wps, 1024);
-  wps = std::min<int64_t>(wps, (n + 127) / 128);
-  wps = std::max<int64_t>(wps, 1);
-  const int64_t seg = ((n + wps - 1) / wps + 127) / 128 * 128;
-  wps = (n + seg - 1) / seg;
-  const long long nunits = (long long)S_ * wps;
-  if (wps > 1) {
-    TRY(ws->partials.ensure((size_t)nunits * kAcc * sizeof(double)));
-    TRY(ws->ensure_tickets((size_t)S_));
-  }
-  const size_t ent = (size_t)nunits * (size_t)seg;
-  TRY(ws->lst.ensure(ent * (sizeof(double) + sizeof(int)) + (size_t)nunits * sizeof(int2) + 16));
-  double* ld = (double*)ws->lst.p;
-  int* li = (int*)(ld + ent);
-  int2* uc = (int2*)(((uintptr_t)(li + ent) + 15) & ~(uintptr_t)15);
-  PoseIO io{};
-  io.x = nullptr; io.v = d_v;
-  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
-  io.slot = d_slot; io.accel = d_accel;
-  io.partials = (double*)ws->partials.p;
-  io.tickets = (unsigned*)ws->tickets.p;
-  const long long blocks = (nunits + kWarps - 1) / kWarps;
-  if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
-  // lidar_kernel = 7: pipeline the two phases over scan chunks.  Compact of
-  // chunk c+1 (HBM stream) runs on `st` while the list policy of chunk c
-  // (fp64 chains) runs on a high-priority side stream forked / joined by
-  // events, so the byte stream hides under the policy.  Chunks are whole
-  // scans and every unit still owns its list region: the per-unit work and
-  // the per-scan fold order are those of the one-shot launch (bitwise equal).
-  const int64_t chunks = pipe ? std::min<int64_t>(g_opt_lidar_chunks.load(), S_) : 1;
-  if (chunks > 1) {
-    TRY(ws->ensure_side(st));
-    const int64_t spc = (S_ + chunks - 1) / chunks;
-    for (int64_t s0 = 0; s0 < S_; s0 += spc) {
-      const long long a0 = (long long)s0 * wps;
-      const long long a1 = (long long)std::min<int64_t>(s0 + spc, S_) * wps;
-      const unsigned cb = (unsigned)((a1 - a0 + kWarps - 1) / kWarps);
-      k_lidar_compact<Src><<<cb, kBlock, 0, st>>>(src, pp, (int)wps, (int)seg, a1, ld, li, uc, a0);
-      CKL();
-      CK(cudaEventRecord(ws->ev_fork, st));
-      CK(cudaStreamWaitEvent(ws->side, ws->ev_fork, 0));
-      k_lidar_listpolicy<Src><<<cb, kBlock, 0, ws->side>>>(src, io, pp, (int)wps, (int)seg, a1,
-                                                          ld, li, uc, a0);
-      CKL();
-    }
-    CK(cudaEventRecord(ws->ev_join, ws->side));
-    CK(cudaStreamWaitEvent(st, ws->ev_join, 0));
-    return RMPB_OK;
-  }
-  k_lidar_compact<Src><<<(unsigned)blocks, kBlock, 0, st>>>(src, pp, (int)wps, (int)seg, nunits,
-                                                           ld, li, uc);
-  CKL();
-  k_lidar_listpolicy<Src><<<(unsigned)blocks, kBlock, 0, st>>>(src, io, pp, (int)wps, (int)seg,
-                                                              nunits, ld, li, uc);
-  CKL();
-  return RMPB_OK;
-}
-
 static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
                         const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                         cudaStream_t st) {
-  const int64_t kopt = g_opt_lidar_kernel.load();
-  if (kopt == 4 || kopt == 5) {
-    if (kopt == 5) {
-      LatticeTma<4> src{};
-      src.sc = sc;
-      return launch_lidar_tma<LatticeTma<4>, 2, 4>(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
-    }
-    LatticeTma<2> src{};
-    src.sc = sc;
-    return launch_lidar_tma<LatticeTma<2>, 2, 2>(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
-  }
-  if (kopt == 6 || kopt == 7) {
-    LatticeSrc src{};
-    src.sc = sc;
-    return launch_lidar_two(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st, kopt == 7);
-  }
-  if (kopt == 0 || kopt == 3) {
-    LatticeSrc src{};
-    src.sc = sc;
-    return launch_lidar_warp(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
-  }
-  int segs, seg_rays;
-  choose_segments(S_, sc.n, &segs, &seg_rays);
-  if (segs > 1) {
-    TRY(ws->partials.ensure((size_t)S_ * segs * kAcc * sizeof(double)));
-    TRY(ws->ensure_tickets((size_t)S_));
-  }
-  PoseIO io{};
-  io.x = nullptr; io.v = d_v;
-  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
-  io.slot = d_slot; io.accel = d_accel;
-  io.partials = (double*)ws->partials.p;
-  io.tickets = (unsigned*)ws->tickets.p;
-  const long long units = (long long)S_ * segs;
-  if (kopt == 1)
-    k_lidar_policy<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
-  else
-    k_lidar_policy2<<<(unsigned)units, kBlock, 0, st>>>(sc, io, pp, segs, seg_rays);
-  CKL();
-  return RMPB_OK;
+  LatticeSrc src{};
+  src.sc = sc;
+  return launch_lidar_warp(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
 }
 
 static int lidar_host(const double* d_dirs_or_null, const double* dirs, const double* R,
@@ -1786,42 +1746,9 @@ extern "C" int rmpb_lidar_policy_batch_device(const double* d_dirs, const double
 static int points_launch(PointsIO pt, int64_t S_, const double* d_v, double v0[3],
                          const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
                          cudaStream_t st) {
-  const int64_t kopt = g_opt_lidar_kernel.load();
-  if (kopt == 4 || kopt == 5) {
-    if (kopt == 5) {
-      PointTma<4> src{};
-      src.pt = pt;
-      return launch_lidar_tma<PointTma<4>, 2, 4>(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
-    }
-    PointTma<2> src{};
-    src.pt = pt;
-    return launch_lidar_tma<PointTma<2>, 2, 2>(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
-  }
-  if (kopt == 6 || kopt == 7) {
-    PointSrc src{};
-    src.pt = pt;
-    return launch_lidar_two(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st, kopt == 7);
-  }
-  if (kopt == 0 || kopt == 3) {
-    PointSrc src{};
-    src.pt = pt;
-    return launch_lidar_warp(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
-  }
-  int segs, seg_rays;
-  choose_segments(S_, pt.n, &segs, &seg_rays);
-  if (segs > 1) {
-    TRY(ws->partials.ensure((size_t)S_ * segs * kAcc * sizeof(double)));
-    TRY(ws->ensure_tickets((size_t)S_));
-  }
-  PoseIO io{};
-  io.x = nullptr; io.v = d_v;
-  if (v0) for (int k = 0; k < 3; ++k) io.v0[k] = v0[k];
-  io.slot = d_slot; io.accel = d_accel;
-  io.partials = (double*)ws->partials.p;
-  io.tickets = (unsigned*)ws->tickets.p;
-  k_lidar_points<<<(unsigned)(S_ * segs), kBlock, 0, st>>>(pt, io, pp, segs, seg_rays);
-  CKL();
-  return RMPB_OK;
+  PointSrc src{};
+  src.pt = pt;
+  return launch_lidar_warp(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
 }
 
 extern "C" int rmpb_lidar_points(const float* xyz, const double* R, int64_t n, const double v[3],
@@ -1945,6 +1872,11 @@ extern "C" int rmpb_policy_reduce(const double* dirs, const double* dists, int64
 }
 
 extern "C" int rmpb_pinv_psd(const double* a, int64_t n, double* out, void* stream) {
+  return rmpb_pinv_psd_rcond(a, n, 1e-8, out, stream);
+}
+
+extern "C" int rmpb_pinv_psd_rcond(const double* a, int64_t n, double rcond, double* out,
+                                   void* stream) {
   if (!a || !out) return fail(RMPB_ERR_INVALID, "NULL a / out");
   if (n < 1) return RMPB_OK;
   int dev;
@@ -1955,7 +1887,7 @@ extern "C" int rmpb_pinv_psd(const double* a, int64_t n, double* out, void* stre
   TRY(ws->in.ensure(n * 9 * sizeof(double)));
   TRY(ws->out.ensure(n * 9 * sizeof(double)));
   CK(cudaMemcpyAsync(ws->in.p, a, n * 9 * sizeof(double), cudaMemcpyHostToDevice, st));
-  k_pinv_psd<<<(unsigned)((n + 127) / 128), 128, 0, st>>>((const double*)ws->in.p, (int)n,
+  k_pinv_psd<<<(unsigned)((n + 127) / 128), 128, 0, st>>>((const double*)ws->in.p, (int)n, rcond,
                                                          (double*)ws->out.p);
   CKL();
   CK(cudaMemcpyAsync(out, ws->out.p, n * 9 * sizeof(double), cudaMemcpyDeviceToHost, st));
@@ -2004,7 +1936,7 @@ extern "C" int rmpb_scene_create(const int8_t* kinds, const int8_t* ops, const d
 extern "C" int rmpb_scene_destroy(rmpb_scene* s) {
   if (!s) return RMPB_OK;
   DeviceGuard dg(s->device);
-  cudaFree(s->d_mem);
+  rfree(s->d_mem);
   delete s;
   return RMPB_OK;
 }
@@ -2110,7 +2042,7 @@ extern "C" int rmpb_bake_grid(const rmpb_scene* s, double ox, double oy, double 
     }
   }
   cudaStreamSynchronize(st);
-  if (tmp) cudaFree(tmp);
+  if (tmp) rfree(tmp);
   cudaStreamDestroy(st);
   if (rc != RMPB_OK) return rc;
   *out = g.release();
@@ -2348,8 +2280,8 @@ extern "C" int rmpb_rollout_destroy(rmpb_rollout* r) {
   DeviceGuard dg(r->g->device);
   if (r->st) cudaStreamSynchronize(r->st);
   if (r->graph) cudaGraphExecDestroy(r->graph);
-  cudaFree(r->mem);
-  if (r->h_active) cudaFreeHost(r->h_active);
+  rfree(r->mem);
+  if (r->h_active) rfree_host(r->h_active);
   if (r->st) cudaStreamDestroy(r->st);
   delete r;
   return RMPB_OK;
@@ -2380,7 +2312,7 @@ extern "C" int rmpb_occupancy_create(const rmpb_grid* g, rmpb_occupancy** out) {
     CKL();
     return RMPB_OK;
   }));
-  CK(cudaDeviceSynchronize());
+  CK(rdevsync());
   Occupancy& o = oc->o;
   o.bits = oc->bits; o.nx = nx; o.ny = ny; o.nz = nz; o.nzw = nzw;
   o.ox = (float)g->geom.ox; o.oy = (float)g->geom.oy; o.oz = (float)g->geom.oz;
@@ -2392,7 +2324,7 @@ extern "C" int rmpb_occupancy_create(const rmpb_grid* g, rmpb_occupancy** out) {
 extern "C" int rmpb_occupancy_destroy(rmpb_occupancy* oc) {
   if (!oc) return RMPB_OK;
   DeviceGuard dg(oc->device);
-  cudaFree(oc->bits);
+  rfree(oc->bits);
   delete oc;
   return RMPB_OK;
 }

@@ -104,7 +104,12 @@ __global__ void k_gather_dirs(int n, const double* __restrict__ dirs_aos, const 
   dz[i] = c[2];
   for (int a = 0; a < 3; ++a) {
     double hi = 0.0, lo = 0.0;
-    if (c[a] != 0.0) recip_dd(c[a], hi, lo);
+    // |d| < 2^-1000 (subnormal included): 1/d overflows or exdiv's error
+    // analysis fails -> NaN reciprocal = "divide with IEEE /" (slab_div)
+    if (c[a] != 0.0) {
+      if (fabs(c[a]) < 0x1p-1000) hi = lo = CUDART_NAN;
+      else recip_dd(c[a], hi, lo);
+    }
     rcp[(2 * a) * n + i] = hi;
     rcp[(2 * a + 1) * n + i] = lo;
   }
@@ -170,22 +175,38 @@ __global__ void k_build_pair64(int nx, int ny, int nz, const T* __restrict__ v, 
   }
 }
 
-// QUADB builder: the QUAD record of cell (i,j,k) (i < nx, j < ny-1, k < nz-1)
-// at its 2x2x2-blocked index; padding records stay zero (never read).
-__global__ void k_build_quadb(int nx, int ny, int nz, int bny, int bnz, const float* __restrict__ v,
-                              float4* __restrict__ q) {
-  long long n = (long long)nx * (ny - 1) * (nz - 1);
+// In-place patch of node sub-box [i0, i0+ni) x [j0, j0+nj) x [k0, k0+nk) of a
+// LINEAR / QUAD / PAIR64 map (EsdfGrid.update): every stored copy of a node
+// is rewritten -- in QUAD up to 4 records hold it (as the z / y neighbour of
+// the records below it), in PAIR64 up to 2.  Each stored slot belongs to one
+// node, so threads never write the same address.  `sub` is f64, C-order.
+template <typename T>
+__global__ void k_patch_nodes(int layout, int nx, int ny, int nz, int i0, int j0, int k0, int ni,
+                              int nj, int nk, const double* __restrict__ sub, void* __restrict__ dst) {
+  const long long n = (long long)ni * nj * nk;
   long long t = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  long long stride = (long long)gridDim.x * blockDim.x;
+  const long long stride = (long long)gridDim.x * blockDim.x;
   for (; t < n; t += stride) {
-    int k = (int)(t % (nz - 1));
-    long long r = t / (nz - 1);
-    int j = (int)(r % (ny - 1));
-    int i = (int)(r / (ny - 1));
-    const float* b = v + ((long long)i * ny + j) * nz + k;
-    unsigned idx = ((((unsigned)(i >> 1) * bny + (unsigned)(j >> 1)) * bnz + (unsigned)(k >> 1)) << 3) |
-                   ((i & 1) << 2) | ((j & 1) << 1) | (k & 1);
-    q[idx] = make_float4(b[0], b[1], b[nz], b[nz + 1]);
+    const int k = k0 + (int)(t % nk);
+    const long long r = t / nk;
+    const int j = j0 + (int)(r % nj);
+    const int i = i0 + (int)(r / nj);
+    const double v = sub[t];
+    if (layout == 0) {  // LINEAR
+      reinterpret_cast<T*>(dst)[((long long)i * ny + j) * nz + k] = (T)v;
+    } else if (layout == 1) {  // QUAD: {v[i,j,k], v[i,j,k+1], v[i,j+1,k], v[i,j+1,k+1]}
+      T* q = reinterpret_cast<T*>(dst);
+      auto rec = [&](int jj, int kk) { return 4 * (((long long)i * (ny - 1) + jj) * (nz - 1) + kk); };
+      if (j <= ny - 2 && k <= nz - 2) q[rec(j, k) + 0] = (T)v;
+      if (j <= ny - 2 && k >= 1) q[rec(j, k - 1) + 1] = (T)v;
+      if (j >= 1 && k <= nz - 2) q[rec(j - 1, k) + 2] = (T)v;
+      if (j >= 1 && k >= 1) q[rec(j - 1, k - 1) + 3] = (T)v;
+    } else {  // PAIR64: {v[i,j,k], v[i,j,k+1]} in f64
+      double* q = reinterpret_cast<double*>(dst);
+      const long long p = ((long long)i * ny + j) * (nz - 1);
+      if (k <= nz - 2) q[2 * (p + k)] = v;
+      if (k >= 1) q[2 * (p + k - 1) + 1] = v;
+    }
   }
 }
 

@@ -33,13 +33,10 @@ constexpr int kAcc = 10;          // a00 a01 a02 a11 a12 a22 b0 b1 b2 cnt
 //           unallocated bricks read as `fill`).
 // Values are copied verbatim (f32 storage only when every value is exactly
 // representable in f32), so all layouts interpolate bit-identically.
-//   QUADB : QUAD records stored in 2x2x2 blocks of cells (128 B = one L1 line
-//           per block), so the two x-planes of a step and the next steps'
-//           cells share lines far more often than in the z-fastest order.
 //   PAIR64: f64 z-pairs {v[i,j,k], v[i,j,k+1]} (double2): 4 aligned 16-B loads
 //           per step and no f32->f64 conversions.
-enum Layout : int { LAYOUT_LINEAR = 0, LAYOUT_QUAD = 1, LAYOUT_BRICK = 2, LAYOUT_QUADB = 3,
-                    LAYOUT_PAIR64 = 4 };
+enum Layout : int { LAYOUT_LINEAR = 0, LAYOUT_QUAD = 1, LAYOUT_BRICK = 2,
+                    LAYOUT_PAIR64 = 4 };  // (3: the 2x2x2-blocked QUADB of round 1, removed)
 
 struct GridGeom {
   int nx, ny, nz;
@@ -121,24 +118,6 @@ struct QuadGridF32 {
   }
 };
 
-struct QuadGridF32B {
-  const float4* __restrict__ q;
-  int bny, bnz;  // 2-cell blocks along y and z of the cell grid
-  __device__ __forceinline__ unsigned idx(int i, int j, int k) const {
-    return ((((unsigned)(i >> 1) * bny + (unsigned)(j >> 1)) * bnz + (unsigned)(k >> 1)) << 3) |
-           ((i & 1) << 2) | ((j & 1) << 1) | (k & 1);
-  }
-  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    const unsigned i0 = idx(ix, iy, iz);
-    const unsigned i1 = (ix & 1) ? idx(ix + 1, iy, iz) : i0 + 4u;
-    float4 a = __ldg(q + i0), c = __ldg(q + i1);
-    Corners k;
-    k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
-    k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;
-    return k;
-  }
-};
-
 struct PairGridF64 {
   const double2* __restrict__ q;
   int py, px;  // strides in pairs: (nz-1), ny*(nz-1)
@@ -146,20 +125,6 @@ struct PairGridF64 {
     const double2* b = q + (unsigned)(ix * px + iy * py + iz);
     double2 a0 = __ldg(b), a1 = __ldg(b + (unsigned)py);
     double2 c0 = __ldg(b + (unsigned)px), c1 = __ldg(b + (unsigned)(px + py));
-    Corners k;
-    k.v000 = a0.x; k.v001 = a0.y; k.v010 = a1.x; k.v011 = a1.y;
-    k.v100 = c0.x; k.v101 = c0.y; k.v110 = c1.x; k.v111 = c1.y;
-    return k;
-  }
-};
-
-struct QuadGridF64 {
-  const double2* __restrict__ q;  // 2 double2 per quad
-  int qy, qx;
-  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    const double2* b = q + 2 * (int64_t)(ix * qx + iy * qy + iz);
-    const double2* c = b + 2 * (int64_t)qx;
-    double2 a0 = __ldg(b), a1 = __ldg(b + 1), c0 = __ldg(c), c1 = __ldg(c + 1);
     Corners k;
     k.v000 = a0.x; k.v001 = a0.y; k.v010 = a1.x; k.v011 = a1.y;
     k.v100 = c0.x; k.v101 = c0.y; k.v110 = c1.x; k.v111 = c1.y;
@@ -336,8 +301,22 @@ __device__ __forceinline__ float interp_f(const G& grid, const GeomF& g, float p
   return __fmaf_rn(fx, c1 - c0, c0);
 }
 
-// Per-ray reciprocal of a direction component (0 -> unused).
+// Per-ray reciprocal of a direction component (0 -> unused; NaN -> the
+// component is below 2^-1000: use IEEE division).
 struct RecipDir { double hx, lx, hy, ly, hz, lz; };
+
+// Slab quotient (bound - s) / d with the per-ray reciprocal.  exdiv equals
+// IEEE `/` for |a| >= 2^-960 and a normal divisor of moderate size; outside
+// that (a tiny numerator, |d| < 2^-1000 flagged by a NaN reciprocal, a
+// quotient that overflows -> exdiv NaN) the rare branch divides with IEEE
+// `/`, so the slab interval -- and the MISS decisions built on it -- stay
+// bit-identical to the reference's _box_span (_ckern.pyx:171-212) for every
+// input, subnormal direction components included.
+__device__ __forceinline__ double slab_div(double a, double d, double hi, double lo) {
+  double q = exdiv(a, d, hi, lo);
+  if (!(fabs(a) >= 0x1p-960) || q != q) q = a / d;
+  return q;
+}
 
 // box_span with exdiv by the per-ray reciprocals: bit-identical to box_span.
 __device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, double sy, double sz,
@@ -345,7 +324,7 @@ __device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, doub
                                               double& t0, double& t1) {
   double tlo = -CUDART_INF, thi = CUDART_INF, ta, tb, tmp;
   if (dx != 0.0) {
-    ta = exdiv(g.ox - sx, dx, q.hx, q.lx); tb = exdiv(g.hx - sx, dx, q.hx, q.lx);
+    ta = slab_div(g.ox - sx, dx, q.hx, q.lx); tb = slab_div(g.hx - sx, dx, q.hx, q.lx);
     if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
     if (ta > tlo) tlo = ta;
     if (tb < thi) thi = tb;
@@ -353,7 +332,7 @@ __device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, doub
     return false;
   }
   if (dy != 0.0) {
-    ta = exdiv(g.oy - sy, dy, q.hy, q.ly); tb = exdiv(g.hy - sy, dy, q.hy, q.ly);
+    ta = slab_div(g.oy - sy, dy, q.hy, q.ly); tb = slab_div(g.hy - sy, dy, q.hy, q.ly);
     if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
     if (ta > tlo) tlo = ta;
     if (tb < thi) thi = tb;
@@ -361,7 +340,7 @@ __device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, doub
     return false;
   }
   if (dz != 0.0) {
-    ta = exdiv(g.oz - sz, dz, q.hz, q.lz); tb = exdiv(g.hz - sz, dz, q.hz, q.lz);
+    ta = slab_div(g.oz - sz, dz, q.hz, q.lz); tb = slab_div(g.hz - sz, dz, q.hz, q.lz);
     if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
     if (ta > tlo) tlo = ta;
     if (tb < thi) thi = tb;
@@ -523,7 +502,8 @@ __device__ __forceinline__ int warp_sum_i(int x) {
 }
 
 // Returns the block total in thread 0 (other threads: undefined).
-// `sm` must hold kWarps*kAcc doubles.
+// `sm` must hold NW*kAcc doubles (NW = warps per CTA).
+template <int NW = kWarps>
 __device__ __forceinline__ void block_reduce(Acc& acc, double* sm) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   bool any = __any_sync(0xffffffffu, acc.a00 != 0.0 || acc.a11 != 0.0 || acc.a22 != 0.0 ||
@@ -546,7 +526,7 @@ __device__ __forceinline__ void block_reduce(Acc& acc, double* sm) {
     double s[kAcc];
 #pragma unroll
     for (int k = 0; k < kAcc; ++k) s[k] = sm[k];
-    for (int w = 1; w < kWarps; ++w) {
+    for (int w = 1; w < NW; ++w) {
 #pragma unroll
       for (int k = 0; k < kAcc; ++k) s[k] += sm[w * kAcc + k];
     }

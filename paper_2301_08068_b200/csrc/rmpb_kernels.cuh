@@ -181,12 +181,12 @@ __device__ __forceinline__ void acc_to_arr(const Acc& a, double* o) {
 // Returns true in the one thread that wrote the pose's final slot.  EX: the
 // K4 exchange epilogue is compiled in (only the lean kernel serves it; the
 // throughput kernel stays free of its code and registers).
-template <bool EX = false>
+template <bool EX = false, int NW = kWarps>
 __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose, int seg,
                                             int segs, const ExArgs* xa = nullptr) {
-  __shared__ double sm[kWarps * kAcc];
+  __shared__ double sm[NW * kAcc];
   __shared__ int s_last;
-  block_reduce(acc, sm);
+  block_reduce<NW>(acc, sm);
   if (io.seg_out && threadIdx.x == 0) acc_to_arr(acc, io.seg_out + (size_t)(pose * segs + seg) * kAcc);
   if (segs == 1) {
     if (EX) {  // warp 0 runs the exchange (lane 0 holds the total)
@@ -218,7 +218,7 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
   f.zero();
   double cnt = 0.0;
   const double* base = io.partials + (size_t)pose * segs * kAcc;
-  for (int j = threadIdx.x; j < segs; j += kBlock) {
+  for (int j = threadIdx.x; j < segs; j += NW * 32) {
     const double* q = base + (size_t)j * kAcc;
     f.a00 += __ldcg(q + 0); f.a01 += __ldcg(q + 1); f.a02 += __ldcg(q + 2);
     f.a11 += __ldcg(q + 3); f.a12 += __ldcg(q + 4); f.a22 += __ldcg(q + 5);
@@ -226,7 +226,7 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
     cnt += __ldcg(q + 9);
   }
   f.cnt = (int)cnt;
-  block_reduce(f, sm);
+  block_reduce<NW>(f, sm);
   if (EX) {
     if (threadIdx.x < 32) {
       if (threadIdx.x == 0) io.tickets[pose] = 0u;  // self-reset
@@ -416,14 +416,14 @@ k_ray_server(G grid, GridGeom g, Bundle b, PolicyParams p, double max_range, dou
         while (true) {
           const ulonglong2 rs = ld_sys_u64x2(&mail->req);
           e = rs.x;
+          if (e != last) break;  // a posted request is served before any exit
           if (rs.y || globaltimer_ns() - t0 > idle_ns) { e = kServerExit; break; }
-          if (e != last) break;
         }
         if (e != kServerExit) {
           // the pose: three independent 16-B reads (in flight together);
           // the host wrote it before `req`
-          const double2 a = ld_sys_f64x2(mail->x), b2 = ld_sys_f64x2(mail->x + 2),
-                        c = ld_sys_f64x2(mail->x + 4);
+          const char* xv = reinterpret_cast<const char*>(mail) + offsetof(ServerMail, x);
+          const double2 a = ld_sys_f64x2(xv), b2 = ld_sys_f64x2(xv + 16), c = ld_sys_f64x2(xv + 32);
           dev->xv[0] = a.x; dev->xv[1] = a.y; dev->xv[2] = b2.x;
           dev->xv[3] = b2.y; dev->xv[4] = c.x; dev->xv[5] = c.y;
           __threadfence();
@@ -476,13 +476,14 @@ k_ray_server(G grid, GridGeom g, Bundle b, PolicyParams p, double max_range, dou
 constexpr int kQueue = 64;
 constexpr int kPrep = 32;
 
+template <int NW>
 struct K2Smem {
-  double acc[kWarps][9];
-  double qt[kWarps][kQueue];
-  int qr[kWarps][kQueue];
-  double pt[kWarps][kPrep], pe[kWarps][kPrep];
-  double px[kWarps][kPrep], py[kWarps][kPrep], pz[kWarps][kPrep];
-  int pr[kWarps][kPrep];
+  double acc[NW][9];
+  double qt[NW][kQueue];
+  int qr[NW][kQueue];
+  double pt[NW][kPrep], pe[NW][kPrep];
+  double px[NW][kPrep], py[NW][kPrep], pz[NW][kPrep];
+  int pr[NW][kPrep];
 };
 
 // Evaluates queue entry `lane` (when `valid`) and adds the warp's batch sum
@@ -527,8 +528,8 @@ __device__ __forceinline__ void policy_flush(SM& sm, int warp, int lane, bool va
 // INSIDE: the pose lies inside the map domain (CTA-uniform: one pose per
 // CTA), so the body is compiled without the per-refill domain test
 // (13.78 -> 13.55 ms per 4096-pose C1 step).
-template <class G, bool RAYOUT, bool FAST, bool INSIDE>
-__device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, const GridGeom& g,
+template <class G, bool RAYOUT, bool FAST, bool INSIDE, int NW>
+__device__ __forceinline__ void ray_policy2_body(K2Smem<NW>& sm, const G& grid, const GridGeom& g,
                                                  const Bundle& b, const PoseIO& io,
                                                  const PolicyParams& p, double max_range,
                                                  double eps, double step_scale, int segs,
@@ -551,6 +552,23 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
   const GeomF gf{(float)g.ox, (float)g.oy, (float)g.oz, (float)(1.0 / g.res), g.nx - 2, g.ny - 2,
                  g.nz - 2};
   (void)gf;
+  // Shared first step (exact): a pose inside the domain starts every ray at
+  // t = 0, where p = s + 0 * d = s for any finite direction, so step 1 is the
+  // same interpolation for all rays of the pose (_ckern.pyx:236-246).  It is
+  // evaluated once here; each ray then starts at t1 = 0 + step * d0 with one
+  // step counted.  Not taken when the pose is in an obstacle (d0 < eps: every
+  // ray hits at t = 0) or a coordinate is -0.0 (s + (+/-0) could flip the
+  // sign of that zero per ray).  ~1 of the ~7 steps per ray on C1.
+  bool skip1 = false;
+  double t1s = 0.0;
+  if constexpr (INSIDE && !FAST) {
+    int cx, cy, cz;
+    const double d0 = interp_fast(grid, g, sx, sy, sz, cx, cy, cz);
+    const bool negz = (sx == 0.0 && signbit(sx)) || (sy == 0.0 && signbit(sy)) ||
+                      (sz == 0.0 && signbit(sz));
+    skip1 = !(d0 < eps) && !negz;
+    t1s = 0.0 + step_scale * d0;
+  }
   __syncwarp();
   while (true) {
     // ---- refill from the prepared-ray buffer (prepare a chunk when empty);
@@ -562,8 +580,8 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
     while (need != 0u && (pcount > 0 || chunk < nchunks)) {
       if (pcount == 0) {
         const int r = begin + (chunk << 5) + lane;
-        chunk += kWarps;
-        bool ok = r < end;
+        chunk += NW;
+        bool ok = r < end, first = false;
         double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
         if (ok) {
           ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
@@ -571,20 +589,27 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
             const RecipDir q = b.recip(r);
             double thi = CUDART_INF;
             if (ex != 0.0) {
-              const double tb = exdiv((ex > 0.0 ? g.hx : g.ox) - sx, ex, q.hx, q.lx);
+              const double tb = slab_div((ex > 0.0 ? g.hx : g.ox) - sx, ex, q.hx, q.lx);
               thi = tb < thi ? tb : thi;
             }
             if (ey != 0.0) {
-              const double tb = exdiv((ey > 0.0 ? g.hy : g.oy) - sy, ey, q.hy, q.ly);
+              const double tb = slab_div((ey > 0.0 ? g.hy : g.oy) - sy, ey, q.hy, q.ly);
               thi = tb < thi ? tb : thi;
             }
             if (ez != 0.0) {
-              const double tb = exdiv((ez > 0.0 ? g.hz : g.oz) - sz, ez, q.hz, q.lz);
+              const double tb = slab_div((ez > 0.0 ? g.hz : g.oz) - sz, ez, q.hz, q.lz);
               thi = tb < thi ? tb : thi;
             }
             t0 = 0.0;
             t1 = thi < max_range ? thi : max_range;
             ok = !(t0 > t1);
+            // shared first step: rays with a finite direction start at t1s
+            // (1 step done); those with t1s > t_end end there (a miss)
+            if (skip1 && ok && isfinite(ex) && isfinite(ey) && isfinite(ez)) {
+              t0 = t1s;
+              first = true;
+              ok = t1s <= t1;  // !(t > t_end): NaN ends the ray
+            }
           } else {
             ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, b.recip(r), t0,
                                t1);
@@ -598,7 +623,7 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
             const int o = b.perm ? b.perm[r] : r;
             ro.t[o] = CUDART_INF;
             if (ro.cell) { ro.cell[3 * o] = -1; ro.cell[3 * o + 1] = -1; ro.cell[3 * o + 2] = -1; }
-            if (ro.steps) ro.steps[o] = 0;
+            if (ro.steps) ro.steps[o] = first ? 1 : 0;
           }
         }
         const unsigned m = __ballot_sync(FULL, ok);
@@ -613,9 +638,10 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
           double vx, vy, vz;
           io.vel(pose, vx, vy, vz);
           const double toward = ex * vx + ey * vy + ez * vz;
-          sm.pr[warp][pos] = (toward > 0.0) ? (int)((unsigned)r | 0x80000000u) : r;
+          sm.pr[warp][pos] = (int)((unsigned)r | (toward > 0.0 ? 0x80000000u : 0u) |
+                                   (first ? 0x40000000u : 0u));
 #else
-          sm.pr[warp][pos] = r;
+          sm.pr[warp][pos] = (int)((unsigned)r | (first ? 0x40000000u : 0u));
 #endif
         }
         pcount = __popc(m);
@@ -630,7 +656,7 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
         dx = (real)sm.px[warp][e]; dy = (real)sm.py[warp][e]; dz = (real)sm.pz[warp][e];
         ray = sm.pr[warp][e];
         alive = true;
-        if (RAYOUT) steps = 0;
+        if (RAYOUT) steps = (ray >> 30) & 1;  // 1 when the shared first step was taken
       }
       const int take = min(pcount, __popc(need));
       phead += take;
@@ -669,11 +695,10 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
     }
 #if RMPB_TOWARD_FILTER
     const bool enq = hit_now && (double)t < p.radius && ray < 0;
-    const int rid = ray & 0x7fffffff;
 #else
     const bool enq = hit_now && (double)t < p.radius;
-    const int rid = ray;
 #endif
+    const int rid = ray & 0x3fffffff;  // bit 31: closing, bit 30: first step shared
     if (RAYOUT && was_alive && !alive) {
       my_steps += steps;
       if (ro.t) {
@@ -736,14 +761,27 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem& sm, const G& grid, cons
     acc.b0 = sm.acc[warp][6]; acc.b1 = sm.acc[warp][7]; acc.b2 = sm.acc[warp][8];
     acc.cnt = cnt;  // warp-uniform count: contributed once per warp
   }
-  finish_unit(acc, io, pose, seg, segs);
+  finish_unit<false, NW>(acc, io, pose, seg, segs);
 }
 
-template <class G, bool RAYOUT, bool FAST = false>
-__global__ void __launch_bounds__(kBlock, RMPB_MINB)
+// NW warps per CTA (kTraceWarps): one (pose, ray segment) unit per CTA.
+// (Measured, round 2: a whole pose per 16- / 32-warp CTA raises the L1 hit
+// rate 26.7 -> 32 % but the wider CTAs' tails cost more: 13.72 / 14.07 ms
+// vs 13.39 ms per 4096-pose C1 step.)
+#ifndef RMPB_NW
+#define RMPB_NW 8
+#endif
+#ifndef RMPB_TRACE_MINB
+#define RMPB_TRACE_MINB (RMPB_MINB * kWarps / RMPB_NW)
+#endif
+constexpr int kTraceWarps = RMPB_NW;
+template <class G, bool RAYOUT, bool FAST = false, int NW = kTraceWarps>
+__global__ void __launch_bounds__(NW * 32, RMPB_TRACE_MINB)
 k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
               double eps, double step_scale, int segs, int seg_rays, RayOut ro) {
-  __shared__ K2Smem sm;
+  // dynamic: sizeof(K2Smem<32>) = 72 KB exceeds the 48 KB static limit
+  extern __shared__ __align__(16) unsigned char k2_dsm[];
+  K2Smem<NW>& sm = *reinterpret_cast<K2Smem<NW>*>(k2_dsm);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int unit = blockIdx.x;
   const int pose = unit / segs, seg = unit - pose * segs;
@@ -758,11 +796,13 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   if (lane < 9) sm.acc[warp][lane] = 0.0;
   __syncthreads();
   if (inside)
-    ray_policy2_body<G, RAYOUT, FAST, true>(sm, grid, g, b, io, p, max_range, eps, step_scale,
-                                            segs, seg_rays, ro, pose, seg, sx, sy, sz);
+    ray_policy2_body<G, RAYOUT, FAST, true, NW>(sm, grid, g, b, io, p, max_range, eps,
+                                                step_scale, segs, seg_rays, ro, pose, seg, sx, sy,
+                                                sz);
   else
-    ray_policy2_body<G, RAYOUT, FAST, false>(sm, grid, g, b, io, p, max_range, eps, step_scale,
-                                             segs, seg_rays, ro, pose, seg, sx, sy, sz);
+    ray_policy2_body<G, RAYOUT, FAST, false, NW>(sm, grid, g, b, io, p, max_range, eps,
+                                                 step_scale, segs, seg_rays, ro, pose, seg, sx,
+                                                 sy, sz);
 }
 
 // K2: LiDAR-direct policy (policies.py:195-205, rays.py:172-173).  Beam k of
@@ -775,160 +815,6 @@ struct ScanIO {
   const unsigned char* __restrict__ valid;  // [S][N] or null (all valid)
   int n;
 };
-
-__global__ void __launch_bounds__(kBlock)
-k_lidar_policy(ScanIO sc, PoseIO io, PolicyParams p, int segs, int seg_rays) {
-  const int unit = blockIdx.x;
-  const int scan = unit / segs, seg = unit - scan * segs;
-  double vx, vy, vz;
-  io.vel(scan, vx, vy, vz);
-  double R[9];
-  const bool rot = sc.R != nullptr;
-  if (rot) {
-#pragma unroll
-    for (int k = 0; k < 9; ++k) R[k] = sc.R[9 * scan + k];
-  }
-  const double* rg = sc.ranges + (size_t)scan * sc.n;
-  const unsigned char* vl = sc.valid ? sc.valid + (size_t)scan * sc.n : nullptr;
-  Acc acc;
-  acc.zero();
-  const int begin = seg * seg_rays;
-  const int end = min(begin + seg_rays, sc.n);
-  for (int i = begin + threadIdx.x; i < end; i += kBlock) {
-    double d = rg[i];
-    if (vl && !vl[i]) d = CUDART_INF;
-    if (d != d || d == CUDART_INF || d < p.min_range) continue;
-    double ex = sc.dirs[3 * i], ey = sc.dirs[3 * i + 1], ez = sc.dirs[3 * i + 2];
-    double wx = ex, wy = ey, wz = ez;
-    if (rot) {  // directions @ orientation.T  (rays.py:172-173)
-      wx = ex * R[0] + ey * R[1] + ez * R[2];
-      wy = ex * R[3] + ey * R[4] + ez * R[5];
-      wz = ex * R[6] + ey * R[7] + ez * R[8];
-    }
-    policy_accumulate(acc, wx, wy, wz, d, vx, vy, vz, p);
-  }
-  finish_unit(acc, io, scan, seg, segs);
-}
-
-// K2 v2: the same reduction, streaming-first.  Lanes stream 32 beams per
-// chunk (4 chunks' range / validity loads in flight), count the valid beams
-// with a ballot and queue (range, beam index) of the beams inside the
-// activation radius.  Each full batch of 32 queued beams is then evaluated
-// by the whole warp: one converged gather of the 32 lattice directions,
-// rotation, closing-velocity test and policy, butterfly-reduced.  Beam ->
-// warp assignment and queue order are data-determined: bitwise reproducible.
-struct LidarSmem {
-  double acc[kWarps][9];
-  double qd[kWarps][kQueue];
-  int qi[kWarps][kQueue];
-};
-
-__device__ __forceinline__ void lidar_flush(LidarSmem& sm, const ScanIO& sc, const double* R,
-                                            bool rot, int warp, int lane, bool valid, int i,
-                                            double d, double vx, double vy, double vz,
-                                            const PolicyParams& p) {
-  Acc a;
-  a.zero();
-  if (valid) {
-    const double ex = sc.dirs[3 * i], ey = sc.dirs[3 * i + 1], ez = sc.dirs[3 * i + 2];
-    double wx = ex, wy = ey, wz = ez;
-    if (rot) {  // directions @ orientation.T  (rays.py:172-173)
-      wx = ex * R[0] + ey * R[1] + ez * R[2];
-      wy = ex * R[3] + ey * R[4] + ez * R[5];
-      wz = ex * R[6] + ey * R[7] + ez * R[8];
-    }
-    policy_accumulate(a, wx, wy, wz, d, vx, vy, vz, p);
-  }
-  const bool nz = a.a00 != 0.0 || a.a11 != 0.0 || a.a22 != 0.0 || a.b0 != 0.0 || a.b1 != 0.0 ||
-                  a.b2 != 0.0 || a.a01 != 0.0 || a.a02 != 0.0 || a.a12 != 0.0;
-  if (!__any_sync(0xffffffffu, nz)) return;
-  double v[9] = {a.a00, a.a01, a.a02, a.a11, a.a12, a.a22, a.b0, a.b1, a.b2};
-#pragma unroll
-  for (int k = 0; k < 9; ++k) v[k] = warp_sum(v[k]);
-  if (lane == 0) {
-#pragma unroll
-    for (int k = 0; k < 9; ++k) sm.acc[warp][k] += v[k];
-  }
-}
-
-__global__ void __launch_bounds__(kBlock, 4)
-k_lidar_policy2(ScanIO sc, PoseIO io, PolicyParams p, int segs, int seg_rays) {
-  __shared__ LidarSmem sm;
-  __shared__ double sR[9];
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const int unit = blockIdx.x;
-  const int scan = unit / segs, seg = unit - scan * segs;
-  const bool rot = sc.R != nullptr;
-  if (rot && tid < 9) sR[tid] = sc.R[9 * scan + tid];
-  const double* rg = sc.ranges + (size_t)scan * sc.n;
-  const unsigned char* vl = sc.valid ? sc.valid + (size_t)scan * sc.n : nullptr;
-  if (lane < 9) sm.acc[warp][lane] = 0.0;
-  __syncthreads();
-  const int begin = seg * seg_rays;
-  const int end = min(begin + seg_rays, sc.n);
-  const int nchunks = (end - begin + 31) >> 5;
-  int qn = 0, cnt = 0;
-  constexpr int U = 4;
-  for (int c0 = warp; c0 < nchunks; c0 += U * kWarps) {
-    double dd[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int i = begin + ((c0 + u * kWarps) << 5) + lane;
-      const bool in = c0 + u * kWarps < nchunks && i < end;
-      dd[u] = in ? __ldcs(rg + i) : CUDART_INF;
-      if (in && vl && !__ldcs(vl + i)) dd[u] = CUDART_INF;
-    }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const double d = dd[u];
-      const bool counted = !(d != d || d == CUDART_INF || d < p.min_range);
-      const bool enq = counted && d < p.radius;
-      cnt += __popc(__ballot_sync(FULL, counted));
-      const unsigned em = __ballot_sync(FULL, enq);
-      if (em) {
-        if (enq) {
-          const int pos = qn + __popc(em & lt);
-          sm.qd[warp][pos] = d;
-          sm.qi[warp][pos] = begin + ((c0 + u * kWarps) << 5) + lane;
-        }
-        qn += __popc(em);
-        if (qn >= 32) {
-          __syncwarp();
-          double vx, vy, vz;
-          io.vel(scan, vx, vy, vz);
-          lidar_flush(sm, sc, sR, rot, warp, lane, true, sm.qi[warp][lane], sm.qd[warp][lane], vx,
-                      vy, vz, p);
-          __syncwarp();
-          if (lane < qn - 32) {
-            sm.qd[warp][lane] = sm.qd[warp][lane + 32];
-            sm.qi[warp][lane] = sm.qi[warp][lane + 32];
-          }
-          qn -= 32;
-          __syncwarp();
-        }
-      }
-    }
-  }
-  __syncwarp();
-  if (qn > 0) {
-    double vx, vy, vz;
-    io.vel(scan, vx, vy, vz);
-    const bool valid = lane < qn;
-    lidar_flush(sm, sc, sR, rot, warp, lane, valid, valid ? sm.qi[warp][lane] : 0,
-                valid ? sm.qd[warp][lane] : 1.0, vx, vy, vz, p);
-  }
-  __syncwarp();
-  Acc acc;
-  acc.zero();
-  if (lane == 0) {
-    acc.a00 = sm.acc[warp][0]; acc.a01 = sm.acc[warp][1]; acc.a02 = sm.acc[warp][2];
-    acc.a11 = sm.acc[warp][3]; acc.a12 = sm.acc[warp][4]; acc.a22 = sm.acc[warp][5];
-    acc.b0 = sm.acc[warp][6]; acc.b1 = sm.acc[warp][7]; acc.b2 = sm.acc[warp][8];
-    acc.cnt = cnt;
-  }
-  finish_unit(acc, io, scan, seg, segs);
-}
 
 // K2 v3 (and K2b): warp units.  A warp owns `seg` consecutive beams of one scan (no
 // CTA-wide barrier anywhere: warps never wait for each other).  Streaming:
@@ -1210,519 +1096,6 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
   }
 }
 
-// K2 v4 / K2b v2 (option lidar_kernel = 4 / 5; measured, NOT the default):
-// the warp-unit kernel fed by TMA bulk copies.  v3 keeps one 128-beam group
-// of loads in flight per warp and ncu attributes ~40 % of its stall samples
-// to that load; here lane 0 of each warp keeps NST stages of GPS groups in
-// flight with cp.async.bulk.shared::cluster.global (one bulk copy per array
-// per stage, completion counted on a per-stage mbarrier), so bytes in flight
-// no longer depend on warps or registers.  Lanes read their beams from
-// shared memory; stages 1 / 2 and the fold are those of k_lidar_warp, with
-// the per-lane running sums in registers (frees shared memory for stages).
-// Ragged tails and rows that are not 16-B aligned take the direct loads.
-// Measured on C3 (profiles/README.md): 0.54-0.57 ms vs v3's 0.50 ms -- with
-// the stream hidden, the warps stall on the stage-1 direction gather and the
-// fp64 policy chains instead, and the stages cost occupancy (24 vs 32 warps
-// per SM): the kernel is bound by per-warp dependent latency, not the stream.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra W;\n}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
-}
-// global -> shared bulk copy (16-B aligned, size a multiple of 16),
-// completion signalled on mbarrier `b`; streaming data: L2 evict-first.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* b) {
-  asm volatile(
-      "{\n .reg .b64 pol;\n"
-      " createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], pol;\n}" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-
-// Beam sources of the TMA kernel.  Stage layout per 128-beam group:
-// lattice: 1024 B ranges | 128 B validity; points: 1536 B xyz.
-template <int GPS>
-struct LatticeTma : LatticeSrc {
-  static constexpr unsigned kStage = 1152 * GPS;  // GPS x 1024 B ranges | GPS x 128 B validity
-  bool tma;  // rows 16-B aligned: bulk copies allowed
-  __device__ __forceinline__ void bind_tma(int scan) {
-    bind(scan);
-    tma = ((reinterpret_cast<uintptr_t>(rg) & 15) == 0) &&
-          (!vl || (reinterpret_cast<uintptr_t>(vl) & 15) == 0);
-  }
-  __device__ __forceinline__ void issue(unsigned char* st, int base, unsigned long long* b) const {
-    mbar_expect_tx(b, vl ? 1152u * GPS : 1024u * GPS);
-    bulk_g2s(st, rg + base, 1024u * GPS, b);
-    if (vl) bulk_g2s(st + 1024 * GPS, vl + base, 128u * GPS, b);
-  }
-  // group j of the stage; lane's beams {2l, 2l+1, 64+2l, 65+2l}
-  // (conflict-free 16-B reads); their in-group indices through `idx`
-  __device__ __forceinline__ void read4(const unsigned char* st, int j, int lane, double (&o)[4],
-                                        int (&idx)[4]) const {
-    const unsigned char* r = st + 1024 * j;
-    const double2 x0 = *reinterpret_cast<const double2*>(r + 16 * lane);
-    const double2 x1 = *reinterpret_cast<const double2*>(r + 512 + 16 * lane);
-    o[0] = x0.x; o[1] = x0.y; o[2] = x1.x; o[3] = x1.y;
-    idx[0] = 2 * lane; idx[1] = 2 * lane + 1; idx[2] = 64 + 2 * lane; idx[3] = 65 + 2 * lane;
-    if (vl) {
-      const unsigned char* m = st + 1024 * GPS + 128 * j;
-      const unsigned short m0 = *reinterpret_cast<const unsigned short*>(m + 2 * lane);
-      const unsigned short m1 = *reinterpret_cast<const unsigned short*>(m + 64 + 2 * lane);
-      if (!(m0 & 0xffu)) o[0] = CUDART_INF;
-      if (!(m0 >> 8)) o[1] = CUDART_INF;
-      if (!(m1 & 0xffu)) o[2] = CUDART_INF;
-      if (!(m1 >> 8)) o[3] = CUDART_INF;
-    }
-  }
-};
-
-template <int GPS>
-struct PointTma : PointSrc {
-  static constexpr unsigned kStage = 1536 * GPS;
-  bool tma;
-  __device__ __forceinline__ void bind_tma(int scan) {
-    bind(scan);
-    tma = vec;
-  }
-  __device__ __forceinline__ void issue(unsigned char* st, int base, unsigned long long* b) const {
-    mbar_expect_tx(b, 1536u * GPS);
-    bulk_g2s(st, P + 3 * (size_t)base, 1536u * GPS, b);
-  }
-  // group j of the stage; lane's points 4l..4l+3 (48-B stride: conflict-free
-  // 16-B reads)
-  __device__ __forceinline__ void read4(const unsigned char* st, int j, int lane, double (&o)[4],
-                                        int (&idx)[4]) const {
-    const float4* q = reinterpret_cast<const float4*>(st + 1536 * j + 48 * lane);
-    const float4 a = q[0], b = q[1], c = q[2];
-    o[0] = range(a.x, a.y, a.z); o[1] = range(a.w, b.x, b.y);
-    o[2] = range(b.z, b.w, c.x); o[3] = range(c.y, c.z, c.w);
-#pragma unroll
-    for (int k = 0; k < 4; ++k) idx[k] = 4 * lane + k;
-  }
-};
-
-struct LidarTmaSmem {
-  double R[9], v[3];
-  double q1d[kRing1];
-  int q1i[kRing1];
-  double q2d[kRing2], q2x[kRing2], q2y[kRing2], q2z[kRing2];
-};
-
-template <class Src, int NST, int GPS>
-__global__ void __launch_bounds__(kBlock, 3)
-k_lidar_tma(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits) {
-  extern __shared__ __align__(128) unsigned char lidar_tsm[];
-  // [kWarps][NST][kStage] stages | [kWarps][NST] mbarriers | [kWarps] LidarTmaSmem
-  unsigned char* stages = lidar_tsm;
-  unsigned long long* bars =
-      reinterpret_cast<unsigned long long*>(lidar_tsm + (size_t)kWarps * NST * Src::kStage);
-  LidarTmaSmem* smw = reinterpret_cast<LidarTmaSmem*>(bars + kWarps * NST);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const long long unit = (long long)blockIdx.x * kWarps + warp;
-  if (unit >= nunits) return;
-  const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
-  LidarTmaSmem& w = smw[warp];
-  unsigned char* st0 = stages + (size_t)warp * NST * Src::kStage;
-  unsigned long long* bar = bars + warp * NST;
-  const double* Rall = src.rot();
-  const bool rot = Rall != nullptr;
-  if (rot && lane < 9) w.R[lane] = Rall[9 * scan + lane];
-  if (lane == 0) io.vel(scan, w.v[0], w.v[1], w.v[2]);
-  src.bind_tma(scan);
-  const int begin = wu * seg;
-  const int end = min(begin + seg, src.count());
-  // full stages (GPS groups of 128 beams) go through shared memory; the
-  // remaining groups are loaded directly
-  constexpr int SB = 128 * GPS;  // beams per stage
-  const int nstages = src.tma ? (end - begin) / SB : 0;
-  const int nbulk = nstages * GPS;  // groups served from the stages
-  if (lane == 0 && nstages > 0) {
-    for (int s = 0; s < NST; ++s) mbar_init(bar + s, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    for (int s = 0; s < NST && s < nstages; ++s) src.issue(st0 + s * Src::kStage, begin + SB * s, bar + s);
-  }
-  double acc[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) acc[k] = 0.0;
-  int h1 = 0, q1n = 0, h2 = 0, q2n = 0, cnt = 0;
-  int base = begin, g = 0;
-  __syncwarp();
-  while (true) {
-    const bool draining = base >= end;
-    if (!draining) {
-      double cur[4];
-      int idx[4];
-      const int sg = g / GPS, j = g - sg * GPS;  // stage sequence number, group in stage
-      if (g < nbulk) {
-        if (j == 0) mbar_wait(bar + sg % NST, (unsigned)((sg / NST) & 1));
-        src.read4(st0 + (sg % NST) * Src::kStage, j, lane, cur, idx);
-      } else {
-        src.load4(base + 4 * lane, end, cur);
-#pragma unroll
-        for (int j = 0; j < 4; ++j) idx[j] = 4 * lane + j;
-      }
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double d = cur[j];
-        const bool counted = !(d != d || d == CUDART_INF || d < p.min_range);
-        cnt += counted;
-        const bool enq = counted && d < p.radius;
-        const unsigned em = __ballot_sync(FULL, enq);
-        if (enq) {
-          int pos = h1 + q1n + __popc(em & lt);
-          if (pos >= kRing1) pos -= kRing1;
-          w.q1d[pos] = d;
-          w.q1i[pos] = base + idx[j];
-        }
-        q1n += __popc(em);
-      }
-      // every lane consumed the stage (ballots above): refill it
-      if (j == GPS - 1 && g < nbulk) {
-        __syncwarp();
-        if (lane == 0 && sg + NST < nstages)
-          src.issue(st0 + (sg % NST) * Src::kStage, begin + SB * (sg + NST), bar + sg % NST);
-      }
-      base += 128;
-      ++g;
-    }
-    __syncwarp();
-    // ---- stage 1 (one call site): direction gather, rotation, closing test
-    while (q1n >= 32 || (draining && (q1n > 0 || q2n > 0))) {
-      const int take = min(q1n, 32);
-      bool keep = false;
-      double d = 0, wx = 0, wy = 0, wz = 0;
-      if (lane < take) {
-        int e = h1 + lane;
-        if (e >= kRing1) e -= kRing1;
-        const int i = w.q1i[e];
-        d = w.q1d[e];
-        double ex, ey, ez;
-        src.dir(i, d, ex, ey, ez);
-        wx = ex; wy = ey; wz = ez;
-        if (rot) {  // directions @ orientation.T  (rays.py:172-173)
-          wx = ex * w.R[0] + ey * w.R[1] + ez * w.R[2];
-          wy = ex * w.R[3] + ey * w.R[4] + ez * w.R[5];
-          wz = ex * w.R[6] + ey * w.R[7] + ez * w.R[8];
-        }
-        keep = wx * w.v[0] + wy * w.v[1] + wz * w.v[2] > 0.0;  // policy_accumulate's test
-      }
-      h1 += take;
-      if (h1 >= kRing1) h1 -= kRing1;
-      q1n -= take;
-      const unsigned km = __ballot_sync(FULL, keep);
-      if (keep) {
-        const int pos = (h2 + q2n + __popc(km & lt)) & (kRing2 - 1);
-        w.q2d[pos] = d; w.q2x[pos] = wx; w.q2y[pos] = wy; w.q2z[pos] = wz;
-      }
-      q2n += __popc(km);
-      __syncwarp();
-      // ---- stage 2 (one call site): transcendental policy, 32 at a time
-      const bool last = draining && q1n == 0;
-      if (q2n >= 32 || (last && q2n > 0)) {
-        const int t2 = min(q2n, 32);
-        Acc a;
-        a.zero();
-        if (lane < t2) {
-          const int e = (h2 + lane) & (kRing2 - 1);
-          policy_accumulate(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2], p);
-        }
-        h2 = (h2 + t2) & (kRing2 - 1);
-        q2n -= t2;
-        if (lane < t2) {  // lane-private running sums (registers)
-          acc[0] += a.a00; acc[1] += a.a01; acc[2] += a.a02;
-          acc[3] += a.a11; acc[4] += a.a12; acc[5] += a.a22;
-          acc[6] += a.b0; acc[7] += a.b1; acc[8] += a.b2;
-        }
-        __syncwarp();
-      }
-    }
-    if (draining) break;
-  }
-  __syncwarp();
-  cnt = warp_sum_i(cnt);
-  double ws[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) ws[k] = warp_sum(acc[k]);
-  Acc a;
-  a.a00 = ws[0]; a.a01 = ws[1]; a.a02 = ws[2]; a.a11 = ws[3]; a.a12 = ws[4];
-  a.a22 = ws[5]; a.b0 = ws[6]; a.b1 = ws[7]; a.b2 = ws[8]; a.cnt = cnt;
-  if (wps == 1) {
-    if (lane == 0 && io.slot)
-      write_slot(a, io.slot + (size_t)scan * 13, io.accel ? io.accel + (size_t)scan * 3 : nullptr);
-    return;
-  }
-  unsigned prev = 0;
-  if (lane == 0) {
-    acc_to_arr(a, io.partials + ((size_t)scan * wps + wu) * kAcc);
-    __threadfence();
-    prev = atomicAdd(io.tickets + scan, 1u);
-  }
-  prev = __shfl_sync(FULL, prev, 0);
-  if (prev != (unsigned)(wps - 1)) return;
-  __threadfence();
-  double f[kAcc];
-#pragma unroll
-  for (int k = 0; k < kAcc; ++k) f[k] = 0.0;
-  const double* pb = io.partials + (size_t)scan * wps * kAcc;
-  for (int j = lane; j < wps; j += 32) {
-#pragma unroll
-    for (int k = 0; k < kAcc; ++k) f[k] += __ldcg(pb + (size_t)j * kAcc + k);
-  }
-#pragma unroll
-  for (int k = 0; k < kAcc; ++k) f[k] = warp_sum(f[k]);
-  if (lane == 0) {
-    Acc t;
-    t.a00 = f[0]; t.a01 = f[1]; t.a02 = f[2]; t.a11 = f[3]; t.a12 = f[4]; t.a22 = f[5];
-    t.b0 = f[6]; t.b1 = f[7]; t.b2 = f[8]; t.cnt = (int)f[9];
-    if (io.slot)
-      write_slot(t, io.slot + (size_t)scan * 13, io.accel ? io.accel + (size_t)scan * 3 : nullptr);
-    io.tickets[scan] = 0u;  // self-reset
-  }
-}
-
-// K2 v5 / K2b v3: the LiDAR path as two kernels, so the byte stream runs at
-// the HBM roofline instead of at the pace of the policy's dependent chains.
-//  * k_lidar_compact: warp units stream their beams (the HBM-bound part:
-//    9 B per lattice beam, 12 B per raw point), count the valid ones and
-//    append the in-radius ones (range, beam index) to the unit's own region
-//    of a scratch list, in beam order.  No shared memory, few registers:
-//    up to 64 warps per SM, two groups of loads in flight per warp.
-//  * k_lidar_listpolicy: one warp per unit walks its list (~10 % of the
-//    beams on C3): direction gather + rotation + closing test, then the
-//    transcendental policy in converged batches of 32; per-unit partials are
-//    folded per scan in unit order by the last warp (atomic ticket).
-// Every order is data-determined: bitwise reproducible (and bitwise equal to
-// v3's results: the policy batches are the same).
-// Measured on C3 (ncu launch list, 1024 scans): compact 0.225 ms = 5.9 TB/s
-// = 0.90 of the HBM copy peak; list policy 0.33 ms (fp64 dependent chains,
-// per-unit fold) -- 0.55 ms in sequence vs v3's 0.50 ms, where the two phases
-// overlap across warps.  v3 stays the default; this is option
-// lidar_kernel = 6 (tested) and the evidence that the stream itself runs at
-// the roofline.
-template <class Src>
-__device__ __forceinline__ void compact_group(const double (&cur)[4], int base, int lane,
-                                              unsigned lt, const PolicyParams& p,
-                                              double* __restrict__ od, int* __restrict__ oi,
-                                              int& m, int& cnt) {
-#pragma unroll
-  for (int j = 0; j < 4; ++j) {
-    const double d = cur[j];
-    const bool counted = !(d != d || d == CUDART_INF || d < p.min_range);
-    cnt += counted;
-    const bool enq = counted && d < p.radius;
-    const unsigned em = __ballot_sync(0xffffffffu, enq);
-    if (enq) {
-      const int pos = m + __popc(em & lt);
-      od[pos] = d;
-      oi[pos] = base + 4 * lane + j;
-    }
-    m += __popc(em);
-  }
-}
-
-#ifndef RMPB_COMPACT_MINB
-#define RMPB_COMPACT_MINB 6
-#endif
-template <class Src>
-__global__ void __launch_bounds__(kBlock, RMPB_COMPACT_MINB)
-k_lidar_compact(Src src, PolicyParams p, int wps, int seg, long long nunits,
-                double* __restrict__ ld, int* __restrict__ li, int2* __restrict__ ucnt,
-                long long u0 = 0) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned lt = (1u << lane) - 1u;
-  const long long unit = u0 + (long long)blockIdx.x * kWarps + warp;  // units [u0, nunits)
-  if (unit >= nunits) return;
-  const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
-  src.bind(scan);
-  const int begin = wu * seg;
-  const int end = min(begin + seg, src.count());
-  double* od = ld + (size_t)unit * seg;
-  int* oi = li + (size_t)unit * seg;
-  int m = 0, cnt = 0;
-  int base = begin;
-  for (; base + 128 < end; base += 256) {  // two groups of loads in flight
-    double c0[4], c1[4];
-    src.load4(base + 4 * lane, end, c0);
-    src.load4(base + 128 + 4 * lane, end, c1);
-    compact_group<Src>(c0, base, lane, lt, p, od, oi, m, cnt);
-    compact_group<Src>(c1, base + 128, lane, lt, p, od, oi, m, cnt);
-  }
-  if (base < end) {
-    double c0[4];
-    src.load4(base + 4 * lane, end, c0);
-    compact_group<Src>(c0, base, lane, lt, p, od, oi, m, cnt);
-  }
-  cnt = warp_sum_i(cnt);
-  if (lane == 0) ucnt[unit] = make_int2(m, cnt);
-}
-
-struct ListSmem {
-  double R[9], v[3];
-  double q2d[kRing2], q2x[kRing2], q2y[kRing2], q2z[kRing2];
-};
-
-template <class Src>
-__global__ void __launch_bounds__(kBlock, RMPB_LIDAR_MINB)
-k_lidar_listpolicy(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits,
-                   const double* __restrict__ ld, const int* __restrict__ li,
-                   const int2* __restrict__ ucnt, long long u0 = 0) {
-  __shared__ ListSmem smw[kWarps];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const long long unit = u0 + (long long)blockIdx.x * kWarps + warp;  // units [u0, nunits)
-  if (unit >= nunits) return;
-  const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
-  ListSmem& w = smw[warp];
-  const double* Rall = src.rot();
-  const bool rot = Rall != nullptr;
-  if (rot && lane < 9) w.R[lane] = Rall[9 * scan + lane];
-  if (lane == 0) io.vel(scan, w.v[0], w.v[1], w.v[2]);
-  src.bind(scan);
-  const int2 mc = ucnt[unit];
-  const int m = mc.x;
-  const double* od = ld + (size_t)unit * seg;
-  const int* oi = li + (size_t)unit * seg;
-  double acc[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) acc[k] = 0.0;
-  int h2 = 0, q2n = 0;
-  __syncwarp();
-  for (int b0 = 0; b0 < m || q2n > 0; b0 += 32) {
-    if (b0 < m) {
-      // stage 1: direction gather, rotation, closing test
-      bool keep = false;
-      double d = 0, wx = 0, wy = 0, wz = 0;
-      if (b0 + lane < m) {
-        d = od[b0 + lane];
-        const int i = oi[b0 + lane];
-        double ex, ey, ez;
-        src.dir(i, d, ex, ey, ez);
-        wx = ex; wy = ey; wz = ez;
-        if (rot) {  // directions @ orientation.T  (rays.py:172-173)
-          wx = ex * w.R[0] + ey * w.R[1] + ez * w.R[2];
-          wy = ex * w.R[3] + ey * w.R[4] + ez * w.R[5];
-          wz = ex * w.R[6] + ey * w.R[7] + ez * w.R[8];
-        }
-        keep = wx * w.v[0] + wy * w.v[1] + wz * w.v[2] > 0.0;  // policy_accumulate's test
-      }
-      const unsigned km = __ballot_sync(FULL, keep);
-      if (keep) {
-        const int pos = (h2 + q2n + __popc(km & lt)) & (kRing2 - 1);
-        w.q2d[pos] = d; w.q2x[pos] = wx; w.q2y[pos] = wy; w.q2z[pos] = wz;
-      }
-      q2n += __popc(km);
-      __syncwarp();
-    }
-    // stage 2 (one call site): transcendental policy, 32 at a time
-    const bool last = b0 + 32 >= m;
-    if (q2n >= 32 || (last && q2n > 0)) {
-      const int t2 = min(q2n, 32);
-      Acc a;
-      a.zero();
-      if (lane < t2) {
-        const int e = (h2 + lane) & (kRing2 - 1);
-        policy_accumulate(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2], p);
-      }
-      h2 = (h2 + t2) & (kRing2 - 1);
-      q2n -= t2;
-      if (lane < t2) {
-        acc[0] += a.a00; acc[1] += a.a01; acc[2] += a.a02;
-        acc[3] += a.a11; acc[4] += a.a12; acc[5] += a.a22;
-        acc[6] += a.b0; acc[7] += a.b1; acc[8] += a.b2;
-      }
-      __syncwarp();
-    }
-  }
-  double ws[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) ws[k] = warp_sum(acc[k]);
-  Acc a;
-  a.a00 = ws[0]; a.a01 = ws[1]; a.a02 = ws[2]; a.a11 = ws[3]; a.a12 = ws[4];
-  a.a22 = ws[5]; a.b0 = ws[6]; a.b1 = ws[7]; a.b2 = ws[8]; a.cnt = mc.y;
-  if (wps == 1) {
-    if (lane == 0 && io.slot)
-      write_slot(a, io.slot + (size_t)scan * 13, io.accel ? io.accel + (size_t)scan * 3 : nullptr);
-    return;
-  }
-  unsigned prev = 0;
-  if (lane == 0) {
-    acc_to_arr(a, io.partials + ((size_t)scan * wps + wu) * kAcc);
-    __threadfence();
-    prev = atomicAdd(io.tickets + scan, 1u);
-  }
-  prev = __shfl_sync(FULL, prev, 0);
-  if (prev != (unsigned)(wps - 1)) return;
-  __threadfence();
-  double f[kAcc];
-#pragma unroll
-  for (int k = 0; k < kAcc; ++k) f[k] = 0.0;
-  const double* pb = io.partials + (size_t)scan * wps * kAcc;
-  for (int j = lane; j < wps; j += 32) {
-#pragma unroll
-    for (int k = 0; k < kAcc; ++k) f[k] += __ldcg(pb + (size_t)j * kAcc + k);
-  }
-#pragma unroll
-  for (int k = 0; k < kAcc; ++k) f[k] = warp_sum(f[k]);
-  if (lane == 0) {
-    Acc t;
-    t.a00 = f[0]; t.a01 = f[1]; t.a02 = f[2]; t.a11 = f[3]; t.a12 = f[4]; t.a22 = f[5];
-    t.b0 = f[6]; t.b1 = f[7]; t.b2 = f[8]; t.cnt = (int)f[9];
-    if (io.slot)
-      write_slot(t, io.slot + (size_t)scan * 13, io.accel ? io.accel + (size_t)scan * 3 : nullptr);
-    io.tickets[scan] = 0u;  // self-reset
-  }
-}
-
-// K2b v1: one point per thread per pass (kept as a measured alternative,
-// option lidar_kernel = 1 or 2).
-__global__ void __launch_bounds__(kBlock)
-k_lidar_points(PointsIO pt, PoseIO io, PolicyParams p, int segs, int seg_rays) {
-  const int unit = blockIdx.x;
-  const int scan = unit / segs, seg = unit - scan * segs;
-  double vx, vy, vz;
-  io.vel(scan, vx, vy, vz);
-  double R[9];
-  const bool rot = pt.R != nullptr;
-  if (rot) {
-#pragma unroll
-    for (int k = 0; k < 9; ++k) R[k] = pt.R[9 * scan + k];
-  }
-  const float* P = pt.xyz + (size_t)scan * pt.n * 3;
-  Acc acc;
-  acc.zero();
-  const int begin = seg * seg_rays;
-  const int end = min(begin + seg_rays, pt.n);
-  for (int i = begin + threadIdx.x; i < end; i += kBlock) {
-    double px = P[3 * i], py = P[3 * i + 1], pz = P[3 * i + 2];
-    double d = sqrt(px * px + py * py + pz * pz);
-    if (!(d > 0.0)) continue;  // zero ("no return") or NaN point: invalid beam
-    // d == inf / d < min_range are skipped (and not counted) by policy_accumulate
-    double ex = px / d, ey = py / d, ez = pz / d;
-    double wx = ex, wy = ey, wz = ez;
-    if (rot) {
-      wx = ex * R[0] + ey * R[1] + ez * R[2];
-      wy = ex * R[3] + ey * R[4] + ez * R[5];
-      wz = ex * R[6] + ey * R[7] + ez * R[8];
-    }
-    policy_accumulate(acc, wx, wy, wz, d, vx, vy, vz, p);
-  }
-  finish_unit(acc, io, scan, seg, segs);
-}
-
 // Unfused parity entry (ckern.policy_reduce, ckern.py:80-93): reduce given
 // (dirs, dists) -- AoS host layout -- into a slot.
 __global__ void __launch_bounds__(kBlock)
@@ -1773,7 +1146,8 @@ __global__ void k_fold_resolve(const double* __restrict__ slots, int n, double* 
 }
 
 // pinv_psd of a batch of 3x3 metrics (core.py:103-115), returns the matrix.
-__global__ void k_pinv_psd(const double* __restrict__ a, int n, double* __restrict__ out) {
+__global__ void k_pinv_psd(const double* __restrict__ a, int n, double rcond,
+                           double* __restrict__ out) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   double m[3][3], V[3][3];
@@ -1782,7 +1156,7 @@ __global__ void k_pinv_psd(const double* __restrict__ a, int n, double* __restri
   jacobi3(m, V);
   double lam[3] = {m[0][0], m[1][1], m[2][2]};
   double lmax = fmax(fmax(lam[0], lam[1]), lam[2]);
-  double cut = 1e-8 * (lmax > 0.0 ? lmax : 0.0);
+  double cut = rcond * (lmax > 0.0 ? lmax : 0.0);  // core.py:111: rcond * max(w.max(), 0)
   double inv[3];
   for (int k = 0; k < 3; ++k) inv[k] = lam[k] > cut ? 1.0 / lam[k] : 0.0;
   for (int r = 0; r < 3; ++r)

@@ -35,10 +35,15 @@ def _stream_ptr(stream=None) -> int:
     return int(s.cuda_stream)
 
 
-def _check_tensor(t, shape_tail, dtype_name, name):
+def _check_tensor(t, shape_tail, dtype_name, name, rows=None, device=None, min_numel=None):
+    """Validate a tensor handed to librmpb as a raw pointer: CUDA, dtype,
+    contiguous, trailing shape, leading dimension ``rows``, same device as
+    ``device``, at least ``min_numel`` elements.  A mismatch would be an
+    out-of-bounds device access (a poisoned CUDA context), so it raises
+    ValueError here instead."""
     torch = _torch()
     want = getattr(torch, dtype_name)
-    if not t.is_cuda:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
         raise ValueError(f"{name} must be a CUDA tensor")
     if t.dtype != want:
         raise ValueError(f"{name} must be {dtype_name}, got {t.dtype}")
@@ -46,6 +51,18 @@ def _check_tensor(t, shape_tail, dtype_name, name):
         raise ValueError(f"{name} must be contiguous")
     if shape_tail is not None and tuple(t.shape[1:]) != tuple(shape_tail):
         raise ValueError(f"{name} must have shape (P, {', '.join(map(str, shape_tail))})")
+    if rows is not None and (t.dim() == 0 or t.shape[0] != rows):
+        raise ValueError(f"{name} must have {rows} rows, got shape {tuple(t.shape)}")
+    if device is not None and t.device != device:
+        raise ValueError(f"{name} is on {t.device}, expected {device}")
+    if min_numel is not None and t.numel() < min_numel:
+        raise ValueError(f"{name} needs at least {min_numel} elements, got {t.numel()}")
+
+
+def _check_out(t, shape, name, device):
+    torch = _torch()
+    _check_tensor(t, shape[1:], "float64", name, rows=shape[0], device=device)
+    return t
 
 
 class RayPolicyEngine:
@@ -83,14 +100,17 @@ class RayPolicyEngine:
     def evaluate(self, x, v, out_slot=None, out_accel=None, step_counter=None, stream=None):
         torch = _torch()
         _check_tensor(x, (3,), "float64", "x")
-        _check_tensor(v, (3,), "float64", "v")
         P = x.shape[0]
-        if v.shape[0] != P:
-            raise ValueError("x and v must have the same number of poses")
+        _check_tensor(v, (3,), "float64", "v", rows=P, device=x.device)
         if out_slot is None:
             out_slot = torch.empty((P, 13), dtype=torch.float64, device=x.device)
+        _check_out(out_slot, (P, 13), "out_slot", x.device)
         if out_accel is None:
             out_accel = torch.empty((P, 3), dtype=torch.float64, device=x.device)
+        _check_out(out_accel, (P, 3), "out_accel", x.device)
+        if step_counter is not None:
+            _check_tensor(step_counter, None, "int64", "step_counter", device=x.device,
+                          min_numel=1)
         cnt = 0 if step_counter is None else step_counter.data_ptr()
         L.call("rmpb_ray_policy_batch_device_mode", self.grid.handle, self.bundle.handle,
                x.data_ptr(), v.data_ptr(), P, self.params.ctypes.data, self.max_range, self.eps,
@@ -101,10 +121,11 @@ class RayPolicyEngine:
     def partial(self, x, v, ray_begin: int, ray_end: int, out_slot=None, stream=None):
         """13-slot of stored rays [ray_begin, ray_end) for one pose (no pinv)."""
         torch = _torch()
-        _check_tensor(x, None, "float64", "x")
-        _check_tensor(v, None, "float64", "v")
+        _check_tensor(x, None, "float64", "x", min_numel=3)
+        _check_tensor(v, None, "float64", "v", device=x.device, min_numel=3)
         if out_slot is None:
             out_slot = torch.empty(13, dtype=torch.float64, device=x.device)
+        _check_tensor(out_slot, None, "float64", "out_slot", device=x.device, min_numel=13)
         L.call("rmpb_ray_policy_range_device", self.grid.handle, self.bundle.handle, x.data_ptr(),
                v.data_ptr(), int(ray_begin), int(ray_end), self.params.ctypes.data,
                self.max_range, self.eps, self.step_scale, out_slot.data_ptr(),
@@ -116,6 +137,8 @@ class RayPolicyEngine:
         """Fixed-order pairwise fold of (n, 13) slots + pinv, on device."""
         torch = _torch()
         _check_tensor(slots, (13,), "float64", "slots")
+        if slots.shape[0] < 1:
+            raise ValueError("resolve needs at least one slot")
         out_slot = torch.empty(13, dtype=torch.float64, device=slots.device)
         out_accel = torch.empty(3, dtype=torch.float64, device=slots.device)
         L.call("rmpb_fold_resolve_device", slots.data_ptr(), slots.shape[0], out_slot.data_ptr(),
@@ -129,12 +152,14 @@ class RayPolicyEngine:
         wait, the fixed-order fold and the solve -- one launch.  Returns
         (slot13, accel3) device tensors, identical on every rank."""
         torch = _torch()
-        _check_tensor(x, None, "float64", "x")
-        _check_tensor(v, None, "float64", "v")
+        _check_tensor(x, None, "float64", "x", min_numel=3)
+        _check_tensor(v, None, "float64", "v", device=x.device, min_numel=3)
         if out_slot is None:
             out_slot = torch.empty(13, dtype=torch.float64, device=x.device)
         if out_accel is None:
             out_accel = torch.empty(3, dtype=torch.float64, device=x.device)
+        _check_tensor(out_slot, None, "float64", "out_slot", device=x.device, min_numel=13)
+        _check_tensor(out_accel, None, "float64", "out_accel", device=x.device, min_numel=3)
         L.call("rmpb_ray_policy_range_exchange", self.grid.handle, self.bundle.handle, x.data_ptr(),
                v.data_ptr(), int(ray_begin), int(ray_end), self.params.ctypes.data,
                self.max_range, self.eps, self.step_scale, mailbox.handle, int(epoch), int(mode),
@@ -203,12 +228,14 @@ class DdaPolicyEngine:
     def evaluate(self, x, v, out_slot=None, out_accel=None, stream=None):
         torch = _torch()
         _check_tensor(x, (3,), "float64", "x")
-        _check_tensor(v, (3,), "float64", "v")
         P = x.shape[0]
+        _check_tensor(v, (3,), "float64", "v", rows=P, device=x.device)
         if out_slot is None:
             out_slot = torch.empty((P, 13), dtype=torch.float64, device=x.device)
         if out_accel is None:
             out_accel = torch.empty((P, 3), dtype=torch.float64, device=x.device)
+        _check_out(out_slot, (P, 13), "out_slot", x.device)
+        _check_out(out_accel, (P, 3), "out_accel", x.device)
         L.call("rmpb_ray_policy_dda_batch_device", self.occ.handle, self.bundle.handle,
                x.data_ptr(), v.data_ptr(), P, self.params.ctypes.data, self.max_range,
                out_slot.data_ptr(), out_accel.data_ptr(), _stream_ptr(stream))
@@ -220,15 +247,23 @@ def lidar_policy_batch_device(dirs, R, ranges, valid, v, params, min_range=0.3, 
     None), ranges (S x n f64), valid (S x n uint8 / bool or None), v (S x 3).
     Returns (slots S x 13, accels S x 3) CUDA tensors."""
     torch = _torch()
-    _check_tensor(dirs, (3,), "float64", "dirs")
+    if not isinstance(ranges, torch.Tensor) or ranges.dim() != 2:
+        raise ValueError("ranges must be a (S, n) float64 CUDA tensor")
     S, n = ranges.shape
+    dev = ranges.device
     _check_tensor(ranges, (n,), "float64", "ranges")
-    _check_tensor(v, (3,), "float64", "v")
+    _check_tensor(dirs, (3,), "float64", "dirs", rows=n, device=dev)
+    _check_tensor(v, (3,), "float64", "v", rows=S, device=dev)
     if R is not None:
+        if R.numel() != 9 * S:
+            raise ValueError(f"R must hold {S} row-major 3x3 matrices")
         R = R.reshape(S, 9).contiguous()
-        _check_tensor(R, (9,), "float64", "R")
+        _check_tensor(R, (9,), "float64", "R", rows=S, device=dev)
     if valid is not None:
+        if tuple(valid.shape) != (S, n):
+            raise ValueError(f"valid must have shape ({S}, {n}), got {tuple(valid.shape)}")
         valid = valid.to(torch.uint8).contiguous()
+        _check_tensor(valid, (n,), "uint8", "valid", rows=S, device=dev)
     p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
     slots = torch.empty((S, 13), dtype=torch.float64, device=ranges.device)
     accels = torch.empty((S, 3), dtype=torch.float64, device=ranges.device)
@@ -245,10 +280,15 @@ def lidar_points_batch_device(xyz, R, v, params, min_range=0.3, stream=None):
     if xyz.dtype != torch.float32 or not xyz.is_cuda or xyz.dim() != 3:
         raise ValueError("xyz must be a (S, n, 3) float32 CUDA tensor")
     xyz = xyz.contiguous()
-    S, n, _ = xyz.shape
-    _check_tensor(v, (3,), "float64", "v")
+    S, n, three = xyz.shape
+    if three != 3:
+        raise ValueError("xyz must have shape (S, n, 3)")
+    _check_tensor(v, (3,), "float64", "v", rows=S, device=xyz.device)
     if R is not None:
+        if R.numel() != 9 * S:
+            raise ValueError(f"R must hold {S} row-major 3x3 matrices")
         R = R.reshape(S, 9).contiguous()
+        _check_tensor(R, (9,), "float64", "R", rows=S, device=xyz.device)
     p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
     slots = torch.empty((S, 13), dtype=torch.float64, device=xyz.device)
     accels = torch.empty((S, 3), dtype=torch.float64, device=xyz.device)

@@ -148,9 +148,41 @@ def scene_distance(scene: Scene, x, t: float = 0.0) -> float:
     return float(scene_distance_many(scene, np.asarray(x, dtype=float).reshape(1, 3), t)[0])
 
 
+def deeply_frozen(a) -> bool:
+    """True when neither ``a`` nor any array it views is writable: its content
+    cannot change through NumPy without re-enabling a flag by hand."""
+    while isinstance(a, np.ndarray):
+        if a.flags.writeable:
+            return False
+        a = a.base
+    return True
+
+
+def immutable_f64(a, shape=None) -> np.ndarray:
+    """A read-only f64 C-contiguous array with the content of ``a``: ``a``
+    itself when it is already that and deeply frozen, else a private copy
+    whose buffer is read-only (device caches key on identity, so the content
+    behind a cached array must not change without them seeing it)."""
+    arr = np.asarray(a)
+    if (arr.dtype == np.float64 and arr.flags.c_contiguous and deeply_frozen(arr)
+            and (shape is None or arr.shape == tuple(shape))):
+        return arr
+    out = np.array(arr, dtype=np.float64, order="C", copy=True)
+    if shape is not None:
+        out = out.reshape(shape)
+    out.setflags(write=False)
+    return out
+
+
 @dataclass(frozen=True)
 class EsdfGrid:
-    """Regular node grid of signed distances (positive = free)."""
+    """Regular node grid of signed distances (positive = free).
+
+    Deviation from the reference (geometry.py:215-240, whose ``values`` may
+    alias the caller's array and stay writable): ``values`` is a read-only
+    private copy, so a device-resident copy of the map can never be served
+    stale.  Edit the map through :meth:`update`, which also patches every
+    cached device copy (only the touched nodes move over PCIe)."""
 
     origin: np.ndarray
     resolution: float
@@ -163,12 +195,57 @@ class EsdfGrid:
         dims = tuple(int(d) for d in self.dims)
         if len(dims) != 3 or min(dims) < 2:
             raise ValueError("grid needs at least 2 nodes per axis")
-        vals = np.ascontiguousarray(self.values, dtype=np.float64)
+        vals = np.asarray(self.values)
         if vals.shape != dims:
             raise ValueError(f"values shape {vals.shape} != dims {dims}")
         object.__setattr__(self, "origin", np.asarray(self.origin, dtype=float).reshape(3))
         object.__setattr__(self, "dims", dims)
-        object.__setattr__(self, "values", vals)
+        frozen = immutable_f64(vals)
+        object.__setattr__(self, "values", frozen)
+        object.__setattr__(self, "_owned", frozen is not vals)
+
+    def update(self, index, values) -> None:
+        """Write ``values`` into ``self.values[index]`` (``index``: a tuple of
+        three ints / unit-step slices) and bring every cached device copy of
+        this map up to date before returning."""
+        if not isinstance(index, tuple) or len(index) != 3:
+            raise ValueError("index must be a tuple of 3 ints / slices")
+        box = []
+        for ax, ix in enumerate(index):
+            n = self.dims[ax]
+            if isinstance(ix, slice):
+                a, b, st = ix.indices(n)
+                if st != 1:
+                    raise ValueError("update slices must have unit step")
+            else:
+                a = int(ix)
+                if a < 0:
+                    a += n
+                if not 0 <= a < n:
+                    raise IndexError(f"index {ix} out of range for axis {ax} of size {n}")
+                b = a + 1
+            if b <= a:
+                return
+            box.append((a, b))
+        sl = tuple(slice(a, b) for a, b in box)
+        new = np.broadcast_to(np.asarray(values, dtype=np.float64),
+                              tuple(b - a for a, b in box))
+        if not getattr(self, "_owned", False):
+            # shared with another owner (a frozen input array): copy first, so
+            # the edit stays private to this grid (a new array = new cache key)
+            own = np.array(self.values, dtype=np.float64, order="C", copy=True)
+            own.setflags(write=False)
+            object.__setattr__(self, "values", own)
+            object.__setattr__(self, "_owned", True)
+        buf = self.values
+        buf.setflags(write=True)
+        try:
+            buf[sl] = new
+        finally:
+            buf.setflags(write=False)
+        hook = getattr(get_backend(), "grid_updated", None)
+        if hook is not None:
+            hook(buf, tuple(a for a, _ in box), np.ascontiguousarray(buf[sl]))
 
     @property
     def domain(self) -> Aabb:

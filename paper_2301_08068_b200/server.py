@@ -9,8 +9,12 @@ writes the slot + acceleration back there: same kernel body and ray
 segmentation as ``ray_policy``, so the results are bitwise identical.
 
 The resident kernel holds its CTAs' SM resources while it runs; it exits by
-itself after ``idle_timeout_s`` without a request (the next call relaunches
-it) and on ``close()``.  One caller thread per server.
+itself after ``idle_timeout_s`` (default 1 s) without a request (the next
+call relaunches it) and on ``close()``.  Calls of librmpb that must
+synchronise the device (freeing a workspace / map / bundle, peer setup) first
+park the running servers of that device (stop + wait) instead of blocking
+behind them; the next ``evaluate`` relaunches transparently.  Requests of one
+server are serialised (a per-server lock).
 """
 
 from __future__ import annotations
@@ -29,7 +33,7 @@ from .rays import DEFAULT_MAX_RANGE, RayBundle
 
 class LatencyServer:
     def __init__(self, field: EsdfGrid, bundle: RayBundle, p: ObstacleParams,
-                 max_range: float = DEFAULT_MAX_RANGE, idle_timeout_s: float = 10.0,
+                 max_range: float = DEFAULT_MAX_RANGE, idle_timeout_s: float = 1.0,
                  storage: int | None = None, layout: int | None = None):
         """``storage`` / ``layout`` (librmpb STORE_* / LAYOUT_*) give the
         server its own device copy of the map in that layout; default: the

@@ -13,6 +13,8 @@ if os.environ.get("SEG_RAYS"):
     _lib.call("rmpb_set_option", b"seg_rays", int(os.environ["SEG_RAYS"]))
 if os.environ.get("CARVEOUT"):
     _lib.call("rmpb_set_option", b"carveout", int(os.environ["CARVEOUT"]))
+if os.environ.get("TRACE_WARPS"):
+    _lib.call("rmpb_set_option", b"trace_warps", int(os.environ["TRACE_WARPS"]))
 if os.environ.get("L2_WINDOW"):
     _lib.call("rmpb_set_option", b"l2_window", int(os.environ["L2_WINDOW"]))
 scene = synth.c1_scene(); grid = synth.c1_grid(scene)
@@ -34,6 +36,7 @@ print(json.dumps({"lib": os.path.basename(os.environ.get("RMPB_LIBRARY", "") or 
                   "l2_window": os.environ.get("L2_WINDOW", "default"),
                   "seg_rays": os.environ.get("SEG_RAYS", "auto"),
                   "carveout": os.environ.get("CARVEOUT", "default"),
+                  "trace_warps": os.environ.get("TRACE_WARPS", "8"),
                   "ms_min": round(min(ts), 3), "ms_med": round(sorted(ts)[len(ts) // 2], 3),
                   "hits": int(sl[:, 12].sum()), "sum_a00": float(sl[:, 0].sum()),
                   "sum_b0": float(sl[:, 9].sum())}), flush=True)

@@ -242,10 +242,9 @@ def test_layouts_and_storage_identical(be, oracle, c1):
                               0.05, 0.9)
     variants = [dict(storage=L.STORE_F32, layout=L.LAYOUT_LINEAR),
                 dict(storage=L.STORE_F32, layout=L.LAYOUT_QUAD),
-                dict(storage=L.STORE_F32, layout=L.LAYOUT_QUADB),
                 dict(storage=L.STORE_F32, layout=L.LAYOUT_PAIR64),
                 dict(storage=L.STORE_F64, layout=L.LAYOUT_LINEAR),
-                dict(storage=L.STORE_F64, layout=L.LAYOUT_QUAD)]
+                dict(storage=L.STORE_F64, layout=L.LAYOUT_PAIR64)]
     for kw in variants:
         dg = be.DeviceGrid(grid.values, grid.origin, grid.resolution, **kw)
         t, _, _ = be.grid_trace_ex(dg, grid.origin, grid.resolution, st.position, sub, 10.0,
@@ -699,17 +698,15 @@ def test_lidar_points_batch_device(be, oracle, c1):
         assert rel_err(accs[k], acc_r) <= 1e-5
 
 
-# 1: per-thread, 2: CTA streaming, 3: warp units, 4 / 5: TMA-fed warp units
-# (two stage sizes); 6: compact + list policy (two kernels); 7: variant 6
-# pipelined over scan chunks on two streams (bitwise variant 6); 14: variant 4 with long warp units (3 per launch:
-# many groups per warp, so the stage ring wraps and the mbarrier parity flips)
-LIDAR_VARIANTS = (1, 2, 3, 4, 5, 6, 7, 14)
-LIDAR_VARIANTS_PTS = (1, 3, 4, 5, 6, 7, 14)
+# LiDAR warp-unit decompositions: the default target (many short units,
+# multi-unit fold per scan), 1000 and 3 units per launch (long units: many
+# 128-beam groups per warp, ring wrap-around)
+LIDAR_WARP_TARGETS = (76000, 1000, 3)
 
 
 @pytest.mark.parametrize("n,S", [(131072, 1), (1000, 5), (131, 3), (97, 2), (4096, 40), (8192, 3)])
 def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
-    """All LiDAR kernel variants (LIDAR_VARIANTS) vs the oracle on ragged beam counts, odd rows (16-B misaligned
+    """The LiDAR kernel at every unit decomposition (LIDAR_WARP_TARGETS) vs the oracle on ragged beam counts, odd rows (16-B misaligned
     range rows / 4-B misaligned validity rows -> scalar path), with and
     without rotation / validity; variant 3 with the default warp targets
     also exercises the multi-warp fold (S = 1: 512 warp partials)."""
@@ -740,25 +737,22 @@ def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
                 d_R = torch.from_numpy(Rs.reshape(S, 9).copy()).cuda() if use_R else None
                 d_vl = torch.from_numpy(valid.astype(np.uint8)).cuda() if use_valid else None
                 outs = {}
-                for k in LIDAR_VARIANTS:
-                    _lib.call("rmpb_set_option", b"lidar_kernel", k % 10)
-                    _lib.call("rmpb_set_option", b"lidar_tma_warps", 3 if k >= 10 else 48000)
+                for k in LIDAR_WARP_TARGETS:
+                    _lib.call("rmpb_set_option", b"lidar_warps", k)
                     sl, ac = lidar_policy_batch_device(d_dirs, d_R, d_rg, d_vl, d_v, LIDAR, 0.3)
                     outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
-                assert np.array_equal(outs[6][0], outs[7][0], equal_nan=True)
                 for s in range(S):
                     wd = dirs @ Rs[s].T if use_R else dirs
                     vv = valid[s] if use_valid else np.ones(n, bool)
                     slot_r, acc_r = oracle.lidar_policy(wd, ranges[s], vv, v[s], LIDAR, 0.3)
-                    for k in LIDAR_VARIANTS:
+                    for k in LIDAR_WARP_TARGETS:
                         sl, ac = outs[k]
                         assert sl[s][12] == slot_r[12], (k, s)
                         assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
                         if slot_r[12] > 0 and np.abs(slot_r[:9]).max() > 0:
                             assert rel_err(ac[s], acc_r) <= ACC_TOL, (k, s)
     finally:
-        _lib.call("rmpb_set_option", b"lidar_kernel", 0)
-        _lib.call("rmpb_set_option", b"lidar_tma_warps", 48000)
+        _lib.call("rmpb_set_option", b"lidar_warps", 76000)
 
 
 @pytest.mark.parametrize("n,S", [(131072, 1), (1001, 4), (131, 3), (4096, 6)])
@@ -781,13 +775,11 @@ def test_lidar_points_kernels_ragged(be, oracle, n, S):
         for use_R in (True, False):
             d_R = torch.from_numpy(Rs.reshape(S, 9).copy()).cuda() if use_R else None
             outs = {}
-            for k in LIDAR_VARIANTS_PTS:
-                _lib.call("rmpb_set_option", b"lidar_kernel", k % 10)
-                _lib.call("rmpb_set_option", b"lidar_tma_warps", 3 if k >= 10 else 48000)
+            for k in LIDAR_WARP_TARGETS:
+                _lib.call("rmpb_set_option", b"lidar_warps", k)
                 sl, ac = lidar_points_batch_device(torch.from_numpy(pts).cuda(), d_R,
                                                    torch.from_numpy(v).cuda(), LIDAR, 0.3)
                 outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
-            assert np.array_equal(outs[6][0], outs[7][0], equal_nan=True)
             for s in range(S):
                 p64 = pts[s].astype(np.float64)
                 r = np.sqrt((p64 * p64).sum(1))
@@ -796,20 +788,25 @@ def test_lidar_points_kernels_ragged(be, oracle, n, S):
                     dd = np.where(ok[:, None], p64 / r[:, None], 0.0)
                 wd = dd @ Rs[s].T if use_R else dd
                 slot_r, acc_r = oracle.lidar_policy(wd, r, ok, v[s], LIDAR, 0.3)
-                for k in LIDAR_VARIANTS_PTS:
+                for k in LIDAR_WARP_TARGETS:
                     sl, ac = outs[k]
                     assert sl[s][12] == slot_r[12], (k, s)
                     assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
     finally:
-        _lib.call("rmpb_set_option", b"lidar_kernel", 0)
-        _lib.call("rmpb_set_option", b"lidar_tma_warps", 48000)
+        _lib.call("rmpb_set_option", b"lidar_warps", 76000)
 
 
 # --- host fast path: repeated calls with the same arrays -----------------------
 
-def test_public_ray_policy_repeated_and_in_place_edit(be, oracle):
+def test_public_ray_policy_repeated_and_map_edits(be, oracle):
     """The control-loop pattern: the same EsdfGrid / RayBundle objects every
-    call (identity cache), then an in-place edit of the map is picked up."""
+    call (identity cache), then map edits through EsdfGrid.update -- a
+    single node (patched in place on the device), a box of obstacle nodes,
+    and values that are not f32-exact (the f32 device copy cannot hold them:
+    re-uploaded) -- each seen by the very next call; the in-place write to
+    EsdfGrid.values itself raises (read-only)."""
+    import time
+
     import paper_2301_08068_b200 as P
     from paper_2301_08068_b200 import synth
 
@@ -821,19 +818,40 @@ def test_public_ray_policy_repeated_and_in_place_edit(be, oracle):
     bundle = P.RayBundle(dirs)
     params = P.preset("static_map").obstacle
     st = synth.bench_states(scene, count=1, seed=5, distance=synth.host_box_distance(scene))[0]
-    ref = oracle.ray_policy(grid.values, grid.origin, 0.1, st.position, st.velocity, dirs,
-                            params.as_tuple(), 10.0)
-    for _ in range(3):
+
+    def check():
+        ref = oracle.ray_policy(grid.values, grid.origin, 0.1, st.position, st.velocity, dirs,
+                                params.as_tuple(), 10.0)
         pol = P.ray_policy(st, grid, bundle, params, 10.0)
         assert rel_err(pol.metric, ref[0][:9].reshape(3, 3)) <= SUM_TOL
         assert rel_err(pol.accel, ref[1]) <= ACC_TOL
-    grid.values[...] -= 0.25  # in place: obstacles grow, every sampled node changes
-    ref2 = oracle.ray_policy(grid.values, grid.origin, 0.1, st.position, st.velocity, dirs,
-                             params.as_tuple(), 10.0)
-    pol2 = P.ray_policy(st, grid, bundle, params, 10.0)
-    assert rel_err(pol2.metric, ref2[0][:9].reshape(3, 3)) <= SUM_TOL
-    assert rel_err(pol2.accel, ref2[1]) <= ACC_TOL
-    assert not np.allclose(pol2.metric, pol.metric)
+        t = be.grid_trace(grid.values, grid.origin, 0.1, st.position, dirs, 10.0, 0.05, 0.9)
+        t_r = oracle.grid_trace(grid.values, grid.origin, 0.1, st.position, dirs, 10.0, 0.05, 0.9)
+        assert np.array_equal(t, t_r)
+        return pol
+
+    p0 = check()
+    for _ in range(2):
+        check()
+    # identity fast path of the map lookup stays cheap
+    be.device_grid(grid.values, grid.origin, 0.1)
+    t0 = time.perf_counter()
+    for _ in range(200):
+        be.device_grid(grid.values, grid.origin, 0.1)
+    assert (time.perf_counter() - t0) / 200 < 5e-6
+    with pytest.raises(ValueError):
+        grid.values[1, 1, 1] = 0.0
+    # one node of the pose's own cell (every ray's first interpolation),
+    # patched in place on the device
+    i, j, kk = (int(c) for c in np.floor(st.position / 0.1))
+    grid.update((i + 1, j, kk), -0.5)
+    p1 = check()
+    assert not np.array_equal(p1.metric, p0.metric)
+    grid.update((slice(i - 2, i + 3), slice(j - 2, j + 3), slice(kk - 1, kk + 2)), -0.25)
+    p2 = check()
+    assert not np.array_equal(p2.metric, p1.metric)
+    grid.update((slice(i, i + 2), j, kk), 0.1234567890123)  # not f32-exact
+    check()
 
 
 def test_concurrent_host_threads_bitwise(be, c1):

@@ -1,6 +1,7 @@
 """CPU: the host fast path of the single-pose call (identity cache of the
 grid / bundle arrays, trusted Policy construction) keeps the reference's
-semantics: in-place edits are seen, non-finite results still raise."""
+semantics: a map edit is always seen (never a stale device copy), non-finite
+results still raise."""
 
 import numpy as np
 import pytest
@@ -10,40 +11,122 @@ from paper_2301_08068_b200._kernels import b200
 
 
 class _Dev:  # stands in for a DeviceGrid / DeviceBundle (no GPU here)
-    pass
+    made = 0
+
+    def __init__(self, *a, **k):
+        _Dev.made += 1
 
 
-def test_identity_cache_sees_in_place_edits():
+def test_identity_cache_only_for_frozen_arrays(monkeypatch):
+    """Deeply read-only arrays (EsdfGrid.values, RayBundle.directions) are
+    served by identity; writable ones never take the identity path."""
     b200.invalidate_caches()
+    monkeypatch.setattr(b200, "DeviceGrid", _Dev)
     a = np.random.default_rng(0).random((40, 30, 20))
-    dev = _Dev()
-    extra = ([0.0, 0.0, 0.0], 0.1, 0)
-    b200._fast_put(a, extra, b200._frozen(a), dev)
-    assert b200._fast_get(a, extra) is dev
-    assert b200._fast_get(a, ([0.0, 0.0, 0.1], 0.1, 0)) is None  # other origin
-    assert b200._fast_get(a.copy(), extra) is None               # other object
-    idx = b200._sample_idx(a.size)
-    a.reshape(-1)[idx[5]] += 1.0                                  # a sampled node
-    assert b200._fast_get(a, extra) is None
+    origin = np.zeros(3)
+    g1 = b200.device_grid(a, origin, 0.1)
+    assert id(a) not in b200._fast                      # writable: keyed path only
+    f = a.copy()
+    f.setflags(write=False)
+    g2 = b200.device_grid(f, origin, 0.1)
+    assert b200._fast_get(f, ([0.0, 0.0, 0.0], 0.1, b200._device)) is g2
+    assert b200._fast_get(f, ([0.0, 0.0, 0.1], 0.1, b200._device)) is None  # other origin
+    assert g1 is not g2
     b200.invalidate_caches()
-    assert b200._fast_get(a, extra) is None
 
 
-def test_identity_cache_frozen_arrays_skip_sampling():
+def test_keyed_cache_sees_any_single_node_edit(monkeypatch):
+    """Writable arrays are re-validated bit for bit on every hit: an edit of
+    ONE node anywhere (not just at sampled positions) forces a re-upload --
+    the reference re-reads the map on every call (ckern.py:49-62)."""
     b200.invalidate_caches()
+    monkeypatch.setattr(b200, "DeviceGrid", _Dev)
+    a = np.random.default_rng(0).random((40, 30, 20))
+    origin = np.zeros(3)
+    g1 = b200.device_grid(a, origin, 0.1)
+    assert b200.device_grid(a, origin, 0.1) is g1       # unchanged: cache hit
+    rng = np.random.default_rng(1)
+    for _ in range(20):
+        i, j, k = (int(rng.integers(0, n)) for n in a.shape)
+        a[i, j, k] += 1e-12
+        g2 = b200.device_grid(a, origin, 0.1)
+        assert g2 is not g1
+        g1 = g2
+        assert b200.device_grid(a, origin, 0.1) is g1
+    a[3, 4, 5] = np.nan                                   # NaN-safe (bitwise) compare
+    g3 = b200.device_grid(a, origin, 0.1)
+    assert g3 is not g1 and b200.device_grid(a, origin, 0.1) is g3
+    b200.invalidate_caches()
+
+
+def test_bundle_cache_sees_in_place_edits(monkeypatch):
+    b200.invalidate_caches()
+    monkeypatch.setattr(b200, "DeviceBundle", _Dev)
     d = np.random.default_rng(1).normal(size=(1000, 3))
-    d.flags.writeable = False
-    dev = _Dev()
-    b200._fast_put(d, 0, b200._frozen(d), dev)
-    assert b200._fast.get(id(d))[2] is None
-    assert b200._fast_get(d, 0) is dev
+    b1 = b200.device_bundle(d)
+    assert b200.device_bundle(d) is b1
+    d[517, 1] *= -1.0
+    assert b200.device_bundle(d) is not b1
     b200.invalidate_caches()
 
 
-def test_sample_covers_both_ends():
-    idx = b200._sample_idx(10_000)
-    assert idx[0] == 0 and idx[-1] == 9_999 and len(idx) == 72
-    assert np.array_equal(b200._sample_idx(300), np.arange(300))
+def test_esdf_grid_values_are_private_and_read_only():
+    from paper_2301_08068_b200 import EsdfGrid
+
+    a = np.random.default_rng(2).random((6, 5, 4))
+    g = EsdfGrid(np.zeros(3), 0.1, a.shape, a)
+    assert not g.values.flags.writeable and g.values is not a
+    with pytest.raises(ValueError):
+        g.values[1, 1, 1] = 0.0
+    a[1, 1, 1] = 123.0                      # the caller's array is not aliased
+    assert g.values[1, 1, 1] != 123.0
+    assert b200._frozen(g.values)
+    # a deeply frozen input is adopted as is (no copy)
+    g2 = EsdfGrid(np.zeros(3), 0.1, a.shape, g.values)
+    assert g2.values is g.values
+
+
+def test_esdf_grid_update_patches_and_notifies(monkeypatch):
+    from paper_2301_08068_b200 import EsdfGrid
+
+    calls = []
+    monkeypatch.setattr(b200, "grid_updated", lambda v, c, sub: calls.append((v, c, sub.copy())))
+    a = np.random.default_rng(3).random((8, 7, 6))
+    g = EsdfGrid(np.zeros(3), 0.1, a.shape, a)
+    vid = id(g.values)
+    g.update((slice(2, 4), 3, slice(None)), -0.5)
+    assert (g.values[2:4, 3, :] == -0.5).all() and g.values[1, 3, 0] == a[1, 3, 0]
+    assert id(g.values) == vid and not g.values.flags.writeable
+    v, corner, sub = calls[-1]
+    assert v is g.values and corner == (2, 3, 0) and sub.shape == (2, 1, 6)
+    # an adopted (shared) array is copied before the first edit
+    g2 = EsdfGrid(np.zeros(3), 0.1, a.shape, g.values)
+    g2.update((0, 0, 0), 9.0)
+    assert g2.values is not g.values and g.values[0, 0, 0] != 9.0 and g2.values[0, 0, 0] == 9.0
+    with pytest.raises(ValueError):
+        g.update((slice(0, 4, 2), 0, 0), 1.0)
+    with pytest.raises(IndexError):
+        g.update((8, 0, 0), 1.0)
+
+
+def test_ray_bundle_private_copy():
+    from paper_2301_08068_b200 import RayBundle
+
+    d = np.random.default_rng(4).normal(size=(10, 3))
+    rb = RayBundle(d)
+    d[0, 0] = 99.0
+    assert rb.directions[0, 0] != 99.0 and not rb.directions.flags.writeable
+    assert RayBundle(rb.directions).directions is rb.directions
+
+
+def test_no_temporary_pointer_arguments():
+    """ctypes arguments must not be pointers into temporaries (the buffer is
+    freed before the C call runs): no `f(...).ctypes.data` in the backend."""
+    import pathlib
+    import re
+
+    src = pathlib.Path(b200.__file__).read_text()
+    assert not re.search(r"\)\.ctypes\.data", src)
 
 
 def test_trusted_policy_equals_checked_policy():
