@@ -1,5 +1,7 @@
-"""LiDAR kernel variants on C3 (1024 scans x 128x1024 beams, GPU box):
-best-of-5 ms per launch and max relative slot difference vs variant 2."""
+"""LiDAR kernels on C3 (1024 scans x 128x1024 beams, GPU box): best / median
+ms per launch (CUDA events, L2 flushed between launches), HBM fraction of the
+9 B/beam stream, and bitwise equality with kernel 3 at the same units.
+args: "K:T" = lidar_kernel K (3 or 6) with T target warp units."""
 import json
 import os
 import sys
@@ -15,64 +17,39 @@ from paper_2301_08068_b200.rays import scan_pattern  # noqa: E402
 scene = synth.c1_scene()
 states = synth.bench_states(scene, count=10, seed=123, distance=synth.host_box_distance(scene))
 scans = synth.lidar_scans(scene, states, 128, 1024, 20.0)
-_r = np.stack([s_.ranges for s_ in scans]); _ok = np.stack([s_.valid for s_ in scans])
-print("valid frac", _ok.mean(), "in-radius frac", (_ok & (_r < 1.3) & (_r >= 0.3)).mean(),
-      file=sys.stderr)
-S = 1024
+S = int(os.environ.get("LIDAR_S", "1024"))
 dirs = torch.from_numpy(np.ascontiguousarray(scan_pattern(128, 1024)).copy()).cuda()
 rg = torch.from_numpy(np.stack([scans[i % 10].ranges for i in range(S)])).cuda()
 vl = torch.from_numpy(np.stack([scans[i % 10].valid for i in range(S)]).astype(np.uint8)).cuda()
 R = torch.from_numpy(np.stack([scans[i % 10].orientation for i in range(S)]).reshape(S, 9).copy()).cuda()
 v = torch.from_numpy(np.stack([states[i % 10].velocity for i in range(S)])).cuda()
 LIDAR = (1.2, 1.5, 3.0, 1.0, 1e-6, 1.3, 1.0)
-out, ref = {}, None
-# args: "2" (kernel 2) or "3:19000" (kernel 3, target warp units)
-for arg in sys.argv[1:] or ["2", "3"]:
-    arg0, _, ch = arg.partition("/")  # "7/8": kernel 7 with 8 scan chunks
-    k, _, wt = arg0.partition(":")
-    k = int(k)
-    if ch:
-        _lib.call("rmpb_set_option", b"lidar_chunks", int(ch))
+flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
+peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
+                                   "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
+    "MEASURED_PEAKS.json") else 6547.8
+ref = {}
+for arg in sys.argv[1:] or ["3:76000", "6:76000"]:
+    k, t = (int(x) for x in arg.split(":"))
     _lib.call("rmpb_set_option", b"lidar_kernel", k)
-    if wt:
-        _lib.call("rmpb_set_option", b"lidar_tma_warps" if k in (4, 5) else b"lidar_warps", int(wt))
-    k = arg
-    s, a = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
+    _lib.call("rmpb_set_option", b"lidar_warps", t)
+    sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
     torch.cuda.synchronize()
-    if ref is None:
-        ref = s.clone()
-    rel = float(((s - ref).abs().max() / ref.abs().max()).item())
-    s2, _ = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
     ts = []
-    for _ in range(5):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
-        e1.record()
+    for _ in range(7):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(); sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3); e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
-    out[f"k{k}_ms"] = min(ts)
-    out[f"k{k}_rel_vs_first"] = rel
-    out[f"k{k}_repeat_bitexact"] = bool(torch.equal(s, s2))
-    out[f"k{k}_nhits_equal"] = bool(torch.equal(s[:, 12], ref[:, 12]))
-# raw points (K2b): the same scans as f32 xyz (invalid -> 0)
-from paper_2301_08068_b200.device import lidar_points_batch_device  # noqa: E402
-
-pts = torch.where(vl.bool()[:, :, None], dirs[None] * rg[:, :, None], 0.0).float().contiguous()
-pts = torch.nan_to_num(pts, nan=0.0, posinf=0.0, neginf=0.0)
-for k in [int(a) for a in os.environ.get("POINT_KERNELS", "1,3,4,5").split(",")]:
-    _lib.call("rmpb_set_option", b"lidar_kernel", k)
-    lidar_points_batch_device(pts, R, v, LIDAR, 0.3)
-    ts = []
-    for _ in range(5):
-        e0 = torch.cuda.Event(enable_timing=True)
-        e1 = torch.cuda.Event(enable_timing=True)
-        e0.record()
-        lidar_points_batch_device(pts, R, v, LIDAR, 0.3)
-        e1.record()
-        e1.synchronize()
-        ts.append(e0.elapsed_time(e1))
-    out[f"points_k{k}_ms"] = min(ts)
+    s_np = sl.cpu().numpy()
+    if k == 3:
+        ref[t] = s_np
+    same = bool(np.array_equal(ref[t], s_np, equal_nan=True)) if t in ref else None
+    ms = min(ts)
+    print(json.dumps({"kernel": k, "target_units": t, "ms_min": round(ms, 4),
+                      "ms_med": round(sorted(ts)[3], 4),
+                      "hbm_frac": round(9 * 131072 * S / (ms * 1e-3) / 1e9 / peak, 4),
+                      "bitwise_eq_v3": same, "hits": int(s_np[:, 12].sum())}), flush=True)
 _lib.call("rmpb_set_option", b"lidar_kernel", 0)
-print(json.dumps(out))
+_lib.call("rmpb_set_option", b"lidar_warps", 76000)

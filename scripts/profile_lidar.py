@@ -18,8 +18,6 @@ LIDAR = (1.2, 1.5, 3.0, 1.0, 1e-6, 1.3, 1.0)
 if os.environ.get("LIDAR_KERNEL"):
     from paper_2301_08068_b200 import _lib
     _lib.call("rmpb_set_option", b"lidar_kernel", int(os.environ["LIDAR_KERNEL"]))
-if os.environ.get("LIDAR_TMA_WARPS"):
-    _lib.call("rmpb_set_option", b"lidar_tma_warps", int(os.environ["LIDAR_TMA_WARPS"]))
 for _ in range(2):
     lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
 torch.cuda.synchronize()
