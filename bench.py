@@ -168,6 +168,9 @@ def run_b200(args):
     local = _env_int("LOCAL_RANK", 0)
     torch.cuda.set_device(local)
     if world > 1:
+        # communicator-init lines on stderr (the driver's rank check reads them)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     os.environ["RMPNAV_DEVICE"] = str(local)
 
@@ -275,6 +278,7 @@ def run_b200(args):
             if i >= 20:
                 lat_s.append(time.perf_counter() - t0)
     lat_srv = statistics.median(lat_s)
+    breakdown = latency_breakdown(grid, bundle, params, states, eng, dev, lat_med, lat_srv)
 
     # measured L2 read ceiling (untimed), CUDA events
     l2 = l2_peaks(dev, stream)
@@ -288,7 +292,16 @@ def run_b200(args):
     traffic = args.ncu_traffic
     if traffic is None and ncu is not None:
         traffic = ncu.get("dram_bytes_per_launch")
-    roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
+    limiter = ("latency: each sphere-trace step is a dependent chain of ~25 fp64 ops around "
+               "one L2 gather (map L2-resident); not HBM bandwidth")
+    if ncu is not None:
+        limiter += (f" -- ncu: issue slots {ncu.get('issue_active_pct')} %, fp64 pipe "
+                    f"{ncu.get('fp64_pipe_active_pct')} %, warps active "
+                    f"{ncu.get('warps_active_pct')} %")
+    roof = {"bound": "hbm", "limiter": limiter,
+            "fp64_pipe_active_pct": (ncu or {}).get("fp64_pipe_active_pct"),
+            "issue_active_pct": (ncu or {}).get("issue_active_pct"),
+            "achieved": round(achieved, 1), "peak": peaks["hbm_gbs"],
             "unit": "GB/s", "frac": round(achieved / peaks["hbm_gbs"], 4),
             "traffic": traffic, "peak_source": peak_src,
             "traffic_source": (ncu or {}).get("file"),
@@ -301,9 +314,19 @@ def run_b200(args):
             "voxel_steps_per_launch": vox_steps,
             "note": "bytes = voxel-steps x 8 corners x 4 B (f32 map); map is L2-resident"}
 
+    configs = {}
+    if rank == 0 and not args.no_configs:
+        configs["C3_lidar_1024_scans"] = c3_config(dev, stream, peaks["hbm_gbs"], flush,
+                                                   cpu=(world == 1 and not args.no_cpu_baseline))
+        configs["C2_1M_rays_10m"] = c2_config(grid, dev, stream, flush, params)
+
     out = None
     if rank == 0:
         cpu = None
+        parity = None
+        if not args.no_parity:
+            parity = parity_check(grid, x_h, v_h, bundle.directions, slots.cpu().numpy(),
+                                  accels.cpu().numpy())
         if world == 1 and not args.no_cpu_baseline:
             cpu = cpu_baseline(grid, states, args.cpu_seconds)
         out = {
@@ -324,7 +347,10 @@ def run_b200(args):
             "latency_us_median": round(lat_med * 1e6, 2),
             "latency_server_hz": round(1.0 / lat_srv, 1),
             "latency_server_us_median": round(lat_srv * 1e6, 2),
+            "latency_breakdown": breakdown,
             "roofline": roof,
+            "parity": parity,
+            "configs": configs,
             "cpu_baseline": cpu,
             "e2e": {"value": round(e2e_value, 1), "unit": "rays/s",
                     "h2d_bytes_per_step": int(P * 6 * 8), "d2h_bytes_per_step": int(P * 16 * 8),
@@ -332,6 +358,323 @@ def run_b200(args):
             "gpu_launches": int(launches),
             "clocks": clk,
         }
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+    return out
+
+
+def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n=200):
+    """Where the single-pose call's time goes (C1, 65536 rays): the public
+    Python call, the bare C-ABI call (ctypes, pre-staged pointers: host
+    staging + launch + kernel + readback + sync), and the kernel alone on the
+    device timeline (CUDA events around a device-resident P = 1 launch)."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    from paper_2301_08068_b200 import _lib
+    from paper_2301_08068_b200._kernels import b200
+
+    g = b200.device_grid(grid.values, grid.origin, grid.resolution)
+    b = b200.device_bundle(bundle.directions)
+    xv = np.empty(6)
+    out = np.empty(16)
+    pa = np.ascontiguousarray(np.asarray(params.as_tuple(), dtype=np.float64))
+    fn = _lib.load().rmpb_ray_policy
+    eps = 0.5 * grid.resolution
+    xvp, outp, pap = xv.ctypes.data, out.ctypes.data, pa.ctypes.data
+    c_us = []
+    for i in range(n + 20):
+        st = states[i % len(states)]
+        xv[0:3] = st.position
+        xv[3:6] = st.velocity
+        t0 = time.perf_counter()
+        rc = fn(g.handle, b.handle, xvp, xvp + 24, pap, MAX_RANGE, eps, 0.9, outp, outp + 104,
+                None, None, None, None)
+        t1 = time.perf_counter()
+        if rc != 0:
+            raise RuntimeError(_lib.last_error())
+        if i >= 20:
+            c_us.append((t1 - t0) * 1e6)
+    x_all = torch.from_numpy(np.stack([s.position for s in states[:64]])).to(dev)
+    v_all = torch.from_numpy(np.stack([s.velocity for s in states[:64]])).to(dev)
+    k_us = []
+    for i in range(n + 20):
+        x1 = x_all[i % 64:i % 64 + 1]
+        v1 = v_all[i % 64:i % 64 + 1]
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200000)  # GPU busy while the host enqueues: e0 -> e1 is the kernel
+        e0.record()
+        eng.evaluate(x1, v1)
+        e1.record()
+        e1.synchronize()
+        if i >= 20:
+            k_us.append(e0.elapsed_time(e1) * 1e3)
+    c_med = statistics.median(c_us)
+    k_med = statistics.median(k_us)
+    return {"python_ray_policy_us": round(lat_py * 1e6, 2),
+            "c_abi_rmpb_ray_policy_us": round(c_med, 2),
+            "device_kernel_us": round(k_med, 2),
+            "python_overhead_us": round(lat_py * 1e6 - c_med, 2),
+            "host_launch_sync_readback_us": round(c_med - k_med, 2),
+            "latency_server_us": round(lat_srv * 1e6, 2),
+            "note": "medians of 200 calls; device_kernel_us = CUDA events around one "
+                    "device-resident P=1 launch (segments of 256 rays: the pose's longest "
+                    "ray is the floor)"}
+
+
+def parity_check(grid, x_h, v_h, dirs, slots, accels, poses=8):
+    """Checker (outside every timed region): `poses` strided poses of the
+    LAST timed launch against the reference's own compiled kernels
+    (oracle/_ref, the C port if absent) on the same direction array."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import oracle as O
+
+    P = slots.shape[0]
+    idx = list(range(0, P, max(1, P // poses)))[:poses]
+    kind = "reference" if O.ref_available() else "port"
+    pool = O.RefPool(_cpu_threads()) if kind == "reference" else None
+    n_eq, rel_s, rel_a = True, 0.0, 0.0
+    try:
+        for k in idx:
+            if kind == "reference":
+                m, w, nh, acc, _ = O.ref_ray_policy(grid.values, grid.origin, grid.resolution,
+                                                    x_h[k], v_h[k], dirs, PARAMS, MAX_RANGE, pool)
+                ref = np.concatenate([np.asarray(m).reshape(9), np.asarray(w).reshape(3), [nh]])
+            else:
+                ref, acc, _ = O.ray_policy(grid.values, grid.origin, grid.resolution, x_h[k],
+                                           v_h[k], dirs, PARAMS, MAX_RANGE, workers=_cpu_threads())
+            n_eq &= bool(slots[k][12] == ref[12])
+            sc = max(1e-300, float(np.abs(ref[:12]).max()))
+            rel_s = max(rel_s, float(np.abs(slots[k][:12] - ref[:12]).max()) / sc)
+            sa = max(1e-300, float(np.abs(acc).max()))
+            rel_a = max(rel_a, float(np.abs(accels[k] - acc).max()) / sa)
+    finally:
+        if pool is not None:
+            pool.close()
+    return {"poses": len(idx), "pose_indices": idx, "checker": kind, "n_hits_equal": n_eq,
+            "max_rel_sums": rel_s, "max_rel_accel": rel_a, "tolerance_sums": 1e-5,
+            "pass": bool(n_eq and rel_s <= 1e-5 and rel_a <= 1e-5)}
+
+
+def _ev_ms(fn, stream, flush, reps=5):
+    import torch
+
+    fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(reps):
+        flush.zero_()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        fn()
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return min(ts), statistics.median(ts)
+
+
+def c3_config(dev, stream, hbm_peak, flush, cpu=True, S=1024):
+    """Config C3 (LiDAR-direct, 128x1024 OS0 scans): 1024 scans per launch,
+    device resident (K2 k_lidar_warp), HBM fraction of its 9 B/beam stream,
+    and the single-scan public call; the reference's CPU lidar_policy on the
+    box's cores beside it."""
+    import torch
+
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200.device import lidar_policy_batch_device
+    from paper_2301_08068_b200.policies import lidar_policy, preset
+    from paper_2301_08068_b200.rays import scan_pattern
+
+    scene = synth.c1_scene()
+    states = synth.bench_states(scene, count=10, seed=123, distance=synth.host_box_distance(scene))
+    scans = synth.lidar_scans(scene, states, 128, 1024, 20.0)
+    n = 128 * 1024
+    lidar = preset("lidar").obstacle
+    lp = lidar.as_tuple()
+    dirs = torch.from_numpy(np.ascontiguousarray(scan_pattern(128, 1024)).copy()).to(dev)
+    rg = torch.from_numpy(np.stack([scans[i % 10].ranges for i in range(S)])).to(dev)
+    vl = torch.from_numpy(np.stack([scans[i % 10].valid for i in range(S)]).astype(np.uint8)).to(dev)
+    R = torch.from_numpy(np.stack([scans[i % 10].orientation for i in range(S)])
+                         .reshape(S, 9).copy()).to(dev)
+    v = torch.from_numpy(np.stack([states[i % 10].velocity for i in range(S)])).to(dev)
+    best, med = _ev_ms(lambda: lidar_policy_batch_device(dirs, R, rg, vl, v, lp, 0.3), stream,
+                       flush)
+    gbs = S * n * 9 / (best * 1e-3) / 1e9
+    lat = []
+    for i in range(120):
+        t0 = time.perf_counter()
+        lidar_policy(states[i % 10].velocity, scans[i % 10], lidar)
+        if i >= 20:
+            lat.append(time.perf_counter() - t0)
+    rec = {"scans_per_launch": S, "beams_per_scan": n, "ms_per_launch_best": round(best, 4),
+           "ms_per_launch_median": round(med, 4), "scans_per_s": round(S / (best * 1e-3), 1),
+           "beams_per_s": round(S * n / (best * 1e-3), 1),
+           "roofline": {"bound": "hbm", "achieved": round(gbs, 1), "peak": hbm_peak,
+                        "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
+                        "bytes_per_beam": 9, "kernel": "k_lidar_warp<LatticeSrc>"},
+           "single_scan_public_api_us_median": round(statistics.median(lat) * 1e6, 1)}
+    if cpu:
+        sys.path.insert(0, os.path.join(ROOT, "oracle"))
+        import oracle as O
+
+        if O.ref_available():
+            wd = [np.ascontiguousarray(s.world_directions()) for s in scans]
+            out = {}
+            for w in (_cpu_threads(), 1):
+                pool = O.RefPool(w)
+                ts = []
+                for i in range(30):
+                    t0 = time.perf_counter()
+                    O.ref_lidar_policy(wd[i % 10], scans[i % 10].ranges, scans[i % 10].valid,
+                                       states[i % 10].velocity, lp, 0.3, pool)
+                    ts.append(time.perf_counter() - t0)
+                pool.close()
+                out[f"threads_{w}"] = {"ms_median": round(statistics.median(ts[5:]) * 1e3, 3),
+                                       "ms_best": round(min(ts) * 1e3, 3),
+                                       "scans_per_s": round(1.0 / statistics.median(ts[5:]), 1)}
+            rec["cpu_reference"] = {**out, "kind": "reference",
+                                    "sample": "30 scans per thread count (world directions "
+                                              "precomputed, as rmpnav's lidar_policy passes them)"}
+    return rec
+
+
+def c2_config(grid, dev, stream, flush, params, P=64):
+    """Config C2 subset: 1 M Halton rays @ 10 m on the C1 map, P poses per
+    launch (device resident)."""
+    import torch
+
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200.device import RayPolicyEngine
+    from paper_2301_08068_b200.rays import sample_directions
+
+    n = 1 << 20
+    scene = synth.c1_scene()
+    states = synth.bench_states(scene, count=P, seed=7, distance=synth.host_box_distance(scene))
+    x_h, v_h = synth.states_arrays(states)
+    eng = RayPolicyEngine(grid, sample_directions(n), params.as_tuple(), MAX_RANGE)
+    x = torch.from_numpy(x_h).to(dev)
+    v = torch.from_numpy(v_h).to(dev)
+    best, med = _ev_ms(lambda: eng.evaluate(x, v), stream, flush, reps=3)
+    return {"poses_per_launch": P, "rays_per_pose": n, "max_range_m": MAX_RANGE,
+            "ms_per_launch_best": round(best, 3), "ms_per_launch_median": round(med, 3),
+            "rays_per_s": round(P * n / (best * 1e-3), 1),
+            "evaluations_per_s": round(P / (best * 1e-3), 1)}
+
+
+def run_c5(args):
+    """`--workload c5`: config C5 -- ONE pose of 1 M Halton rays on the
+    1000x1000x200 @0.05 m block-hashed TSDF (tau 0.2 m), its rays split over
+    the WORLD_SIZE ranks (strong scaling: the work per step is fixed).  Each
+    step is one K4 launch per rank (FusedRaySplit: trace the rank's ray range
+    -> post the partial 13-slot into every rank's mailbox over peer memory ->
+    wait -> fixed-order fold -> pinv, rmpnav/_kernels/_pool.py:61-72); the
+    all_gather path (partial kernel, NCCL all_gather of the 13-slots, fold
+    kernel) is timed alongside.  Device time, max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    world = _env_int("WORLD_SIZE", 1)
+    rank = _env_int("RANK", 0)
+    local = _env_int("LOCAL_RANK", 0)
+    torch.cuda.set_device(local)
+    if world > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    os.environ["RMPNAV_DEVICE"] = str(local)
+    from paper_2301_08068_b200 import _lib, synth
+    from paper_2301_08068_b200._kernels import b200
+    from paper_2301_08068_b200.device import PeerMailbox, RayPolicyEngine
+    from paper_2301_08068_b200.parallel import FusedRaySplit, balanced_range, split_ray_policy
+
+    b200.set_device(local)
+    dev = torch.device("cuda", local)
+    t0 = time.perf_counter()
+    scene = synth.c5_scene()
+    _dense, brick, info = synth.c5_grids(scene)
+    del _dense
+    build_s = time.perf_counter() - t0
+    states = synth.bench_states(scene, count=8, seed=123, distance=synth.host_box_distance(scene))
+    n = 1 << 20
+    bundle = b200.DeviceBundle(halton_n=n)
+    eng = RayPolicyEngine(brick, bundle, PARAMS, MAX_RANGE, device=local)
+    xs = [torch.tensor(s.position, dtype=torch.float64, device=dev) for s in states]
+    vs = [torch.tensor(s.velocity, dtype=torch.float64, device=dev) for s in states]
+    if world > 1:
+        split = FusedRaySplit(eng)
+    else:
+        mb = PeerMailbox(1, 0, local)
+        mb.open([mb.ipc_handle])
+        ep = [0]
+        b0, e0 = balanced_range(n, 1, 0)
+
+        def split(x, v):
+            ep[0] += 1
+            return eng.exchange(x, v, mb, ep[0], b0, e0)
+    stream = torch.cuda.current_stream()
+
+    def timed(fn, steps):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ms = 0.0
+        for k in range(steps):
+            e0_ = torch.cuda.Event(enable_timing=True)
+            e1_ = torch.cuda.Event(enable_timing=True)
+            e0_.record(stream)
+            fn(xs[k % 8], vs[k % 8])
+            e1_.record(stream)
+            e1_.synchronize()
+            ms += e0_.elapsed_time(e1_)
+        t = torch.tensor([ms], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item()) / steps
+
+    for k in range(args.warmup):
+        split(xs[k % 8], vs[k % 8])
+    n0 = _lib.launch_count()
+    ms_fused = timed(split, args.steps)
+    launches = _lib.launch_count() - n0
+    res_f = split(xs[0], vs[0])
+    if world > 1:
+        gather = lambda x, v: split_ray_policy(eng, x, v)  # noqa: E731
+    else:
+        gather = lambda x, v: eng.resolve(eng.partial(x, v, 0, n).view(1, 13))  # noqa: E731
+    for k in range(args.warmup):
+        gather(xs[k % 8], vs[k % 8])
+    ms_gather = timed(gather, args.steps)
+    res_g = gather(xs[0], vs[0])
+    torch.cuda.synchronize()
+    sf, sg = res_f[0].view(-1).cpu().numpy(), res_g[0].view(-1).cpu().numpy()
+    fused_rel = float(np.abs(sf[:12] - sg[:12]).max() / max(1e-300, np.abs(sg[:12]).max()))
+    same_hits = bool(sf[12] == sg[12])
+    out = None
+    if rank == 0:
+        out = {"metric": METRIC, "value": round(n / (ms_fused * 1e-3), 1), "unit": "rays/s",
+               "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+               "ms_per_step": round(ms_fused, 4), "higher_is_better": True, "scaling": "strong",
+               "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+               "config": {"workload": "C5: one pose x 1 M Halton rays, 1000x1000x200 @0.05 m "
+                                      "block-hashed TSDF (tau 0.2 m), max range 10 m, rays "
+                                      f"split over {world} GPU(s)",
+                          "rays_per_pose": n, "map": "BRICK 8^3, f32", **info,
+                          "build_s": round(build_s, 2),
+                          "parallelism": f"ray-split x{world} (K4 peer-mailbox exchange)"},
+               "hz": round(1e3 / ms_fused, 1),
+               "allgather_baseline": {"ms_per_step": round(ms_gather, 4),
+                                      "hz": round(1e3 / ms_gather, 1),
+                                      "path": "partial kernel + NCCL all_gather + fold kernel"
+                                              if world > 1 else "partial kernel + fold kernel"},
+               "fused_vs_allgather": {"n_hits_equal": same_hits, "max_rel_sums": fused_rel,
+                                      "note": "different ray segmentations per kernel: sums "
+                                              "agree to the last bits, not bitwise"},
+               "gpu_launches": int(launches)}
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()
@@ -369,6 +712,17 @@ def l2_peaks(dev, stream, mib=32):
 # ----------------------------------------------------------------------------
 # CPU legs (reference kernels from oracle/_ref; C port fallback)
 
+def _cpu_model():
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return None
+
+
 def _cpu_threads():
     try:
         return len(os.sched_getaffinity(0))
@@ -388,15 +742,18 @@ def cpu_baseline(grid, states, seconds=10.0, threads=None, seconds_1t=4.0):
     kind = "reference" if O.ref_available() else "port"
     pool = O.RefPool(threads)
     done, t0 = 0, time.perf_counter()
+    per = []
     try:
         while True:
             st = states[done % len(states)]
+            tc = time.perf_counter()
             if kind == "reference":
                 O.ref_ray_policy(vals, grid.origin, grid.resolution, st.position, st.velocity,
                                  dirs, PARAMS, MAX_RANGE, pool)
             else:
                 O.ray_policy(vals, grid.origin, grid.resolution, st.position, st.velocity, dirs,
                              PARAMS, MAX_RANGE, workers=threads)
+            per.append(time.perf_counter() - tc)
             done += 1
             el = time.perf_counter() - t0
             if (el >= seconds and done >= 3) or done >= 100000:
@@ -422,8 +779,13 @@ def cpu_baseline(grid, states, seconds=10.0, threads=None, seconds_1t=4.0):
                 break
     finally:
         pool1.close()
+    per_ms = sorted(1e3 * t for t in per)
     return {"value": round(rays_s, 1), "unit": "rays/s", "cores": threads, "kind": kind,
             "hz": round(done / el, 2),
+            "call_ms_median": round(statistics.median(per_ms), 3),
+            "call_ms_best": round(per_ms[0], 3),
+            "call_ms_p95": round(per_ms[min(len(per_ms) - 1, int(0.95 * len(per_ms)))], 3),
+            "cpu_model": _cpu_model(),
             "value_1_thread": round(one * N_RAYS / el1, 1), "hz_1_thread": round(one / el1, 2),
             "sample": f"{done} poses x {N_RAYS} rays of the same workload in {el:.1f} s "
                       f"({threads} threads, reference chunk pool, CHUNK=2048)"}
@@ -523,17 +885,29 @@ def main(argv=None):
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--workload", default="c4", choices=["c4", "c5"],
+                    help="c4 (default, the driver line): 4096 poses x 65536 rays per GPU; "
+                         "c5: one 1 M-ray pose on the C5 TSDF split over the GPUs")
     ap.add_argument("--poses", type=int, default=4096, help="poses per rank per step")
     ap.add_argument("--latency-calls", type=int, default=200)
     ap.add_argument("--cpu-seconds", type=float, default=10.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true",
+                    help="skip the post-run check of 8 timed poses against the reference")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the extra C3 / C2 lines")
     ap.add_argument("--ref-poses-per-step", type=int, default=8)
     ap.add_argument("--ncu-traffic", type=float, default=None,
                     help="dram bytes per launch from an ncu --set full capture")
     args = ap.parse_args(argv)
     if args.warmup < 3 and args.impl == "b200":
         print("warning: fewer than 3 warm-up steps", file=sys.stderr)
-    out = run_reference(args) if args.impl == "reference" else run_b200(args)
+    if args.impl == "reference":
+        out = run_reference(args)
+    elif args.workload == "c5":
+        out = run_c5(args)
+    else:
+        out = run_b200(args)
     if out is not None:
         print(json.dumps(out), flush=True)
 

@@ -331,6 +331,16 @@ def _snapshot(a: np.ndarray, frozen: bool):
     return None if frozen else a.copy()
 
 
+def _entry_valid(a: np.ndarray, snap) -> bool:
+    """A keyed entry (same address, shape, dtype) serves ``a`` when it was
+    stored for a deeply frozen array and ``a`` is frozen too (the entry keeps
+    that buffer alive, so the address cannot belong to another allocation,
+    and its content cannot change), or when ``a`` equals its snapshot."""
+    if snap is None:
+        return _frozen(a)
+    return _same_content(a, snap)
+
+
 def invalidate_caches() -> None:
     """Drop every cached device grid / bundle / scene."""
     with _lock:
@@ -391,7 +401,7 @@ def _device_grid_keyed(values, origin, res) -> DeviceGrid:
     key = (v.ctypes.data, v.shape, v.dtype.str, o, float(res), _device)
     with _lock:
         hit = _grids.get(key)
-        if hit is not None and hit[1] is v and _same_content(v, hit[2]):
+        if hit is not None and _entry_valid(v, hit[2]):
             _grids.move_to_end(key)
             return hit[0]
         frozen = _frozen(v)
@@ -417,8 +427,9 @@ def grid_updated(values: np.ndarray, corner, sub: np.ndarray) -> None:
         for k, e in list(_fast.items()):
             if e[0] is values:
                 targets.append(("fast", k, e[2]))
+        ptr = values.ctypes.data
         for k, e in list(_grids.items()):
-            if e[1] is values:
+            if k[0] == ptr and k[1] == values.shape:  # this buffer, any view of it
                 targets.append(("keyed", k, e[0]))
         done = {}
         for kind, k, g in targets:
@@ -449,7 +460,7 @@ def _device_bundle_keyed(dirs) -> DeviceBundle:
     key = (d.ctypes.data, d.shape[0], _device)
     with _lock:
         hit = _bundles.get(key)
-        if hit is not None and hit[1] is d and _same_content(d, hit[2]):
+        if hit is not None and _entry_valid(d, hit[2]):
             _bundles.move_to_end(key)
             return hit[0]
         b = DeviceBundle(d)
@@ -686,7 +697,7 @@ def device_bundle_identity(d: np.ndarray) -> DeviceBundle:
     key = (d.ctypes.data, d.shape[0], _device)
     with _lock:
         hit = _patterns.get(key)
-        if hit is not None and hit[1] is d and _same_content(d, hit[2]):
+        if hit is not None and _entry_valid(d, hit[2]):
             return hit[0]
         b = DeviceBundle(d, order=L.ORDER_IDENTITY)
         _patterns[key] = (b, d, _snapshot(d, _frozen(d)))

@@ -41,7 +41,6 @@ static std::atomic<int64_t> g_opt_carveout{-1};
 static std::atomic<int64_t> g_opt_l2_window{1};  // map access-policy window on trace launches
 static std::atomic<int64_t> g_opt_graphs{1};     // CUDA-graph replay of rollout ticks
 static std::atomic<int64_t> g_opt_lidar_warps{76000};  // LiDAR: target warp units per launch
-static std::atomic<int64_t> g_opt_lidar_kernel{0};  // 0: v6 pairs (default), 3: v3 warp units
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -224,25 +223,31 @@ static int with_grid(const rmpb_grid* g, F&& f) {
   const GridGeom& G = g->geom;
   if (g->layout == LAYOUT_LINEAR) {
     if (g->storage == RMPB_STORE_F32) {
-      LinearGrid<float> a{(const float*)g->d_values, G.nz, G.ny * G.nz};
+      LinearGrid<float> a{(const float*)g->d_values, G.nz, G.ny * G.nz,
+                           (unsigned)(g->nx * g->ny * g->nz)};
       return f(a);
     }
-    LinearGrid<double> a{(const double*)g->d_values, G.nz, G.ny * G.nz};
+    LinearGrid<double> a{(const double*)g->d_values, G.nz, G.ny * G.nz,
+                          (unsigned)(g->nx * g->ny * g->nz)};
     return f(a);
   }
   if (g->layout == LAYOUT_PAIR64) {
-    PairGridF64 a{(const double2*)g->d_values, G.nz - 1, G.ny * (G.nz - 1)};
+    PairGridF64 a{(const double2*)g->d_values, G.nz - 1, G.ny * (G.nz - 1),
+                  (unsigned)(g->nx * g->ny * (g->nz - 1))};
     return f(a);
   }
   if (g->layout == LAYOUT_QUAD) {  // f32 storage only (grid_build)
-    QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1)};
+    QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1),
+                  (unsigned)(g->nx * (g->ny - 1) * (g->nz - 1))};
     return f(a);
   }
   if (g->storage == RMPB_STORE_F32) {
-    BrickGrid<float> a{(const float*)g->d_values, g->d_table, g->bny, g->bnz, (float)g->fill};
+    BrickGrid<float> a{(const float*)g->d_values, g->d_table, g->bny, g->bnz, (float)g->fill,
+                       (unsigned)(g->bnx * g->bny * g->bnz), (unsigned)g->bricks};
     return f(a);
   }
-  BrickGrid<double> a{(const double*)g->d_values, g->d_table, g->bny, g->bnz, g->fill};
+  BrickGrid<double> a{(const double*)g->d_values, g->d_table, g->bny, g->bnz, g->fill,
+                      (unsigned)(g->bnx * g->bny * g->bnz), (unsigned)g->bricks};
   return f(a);
 }
 
@@ -328,12 +333,6 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
   if (!strcmp(name, "l2_window")) {
     if (value < 0 || value > 1) return fail(RMPB_ERR_INVALID, "l2_window must be 0 or 1");
     g_opt_l2_window.store(value);
-    return RMPB_OK;
-  }
-  if (!strcmp(name, "lidar_kernel")) {
-    if (value != 0 && value != 3 && value != 6)
-      return fail(RMPB_ERR_INVALID, "lidar_kernel must be 0 (auto = 6), 3 or 6");
-    g_opt_lidar_kernel.store(value);
     return RMPB_OK;
   }
   if (!strcmp(name, "carveout")) {
@@ -1651,20 +1650,8 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
     cudaFuncSetAttribute(k_lidar_warp<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
   });
-  if (g_opt_lidar_kernel.load() == 3) {  // v3: one warp per unit (bitwise the default)
-    k_lidar_warp<Src><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps, (int)seg,
-                                                               nunits);
-  } else {  // v6: warp-specialised (NF filter + NP policy warps per CTA)
-    const long long wblocks = (nunits + kLidarNF - 1) / kLidarNF;
-    const size_t wsm = sizeof(LidarUnitSmem) * kLidarNF;
-    static std::once_flag once_ws[64];
-    std::call_once(once_ws[dev & 63], [&] {
-      cudaFuncSetAttribute(k_lidar_ws<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                           (int)wsm);
-    });
-    k_lidar_ws<Src><<<(unsigned)wblocks, 2 * kLidarNF * 32, wsm, st>>>(
-        src, io, pp, (int)wps, (int)seg, nunits);
-  }
+  k_lidar_warp<Src><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps, (int)seg,
+                                                             nunits);
   CKL();
   return RMPB_OK;
 }

@@ -16,6 +16,26 @@
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
+// Debug build (make checked -> librmpb_checked.so): device-side bounds
+// checks on every map / ring / partial index (a failed check prints its
+// location and traps).  compute-sanitizer is not available on the GPU pool
+// this was built on; this build plus the GPU test-suite stands in for it.
+#ifdef RMPB_CHECKED
+#include <cstdio>
+#define RMPB_CHECK(c)                                                               \
+  do {                                                                             \
+    if (!(c)) {                                                                    \
+      printf("RMPB_CHECK failed %s:%d: %s (block %d thread %d)\n", __FILE__, __LINE__, \
+             #c, (int)blockIdx.x, (int)threadIdx.x);                               \
+      __trap();                                                                    \
+    }                                                                              \
+  } while (0)
+#else
+#define RMPB_CHECK(c) \
+  do {                \
+  } while (0)
+#endif
+
 namespace rmpb {
 
 constexpr int kBlock = 256;       // threads per CTA for the policy kernels
@@ -94,7 +114,10 @@ template <typename T>
 struct LinearGrid {
   const T* __restrict__ v;
   int sy, sx;  // strides: nz, ny*nz (node counts < 2^31 checked at create)
+  unsigned lim;  // node count (RMPB_CHECKED builds)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 &&
+               (unsigned)(ix * sx + iy * sy + iz) + (unsigned)(sx + sy + 1) < lim);
     const T* b = v + (unsigned)(ix * sx + iy * sy + iz);  // < 2^31 nodes (checked at create)
     Corners c;
     c.v000 = (double)__ldg(b);           c.v001 = (double)__ldg(b + 1);
@@ -108,7 +131,10 @@ struct LinearGrid {
 struct QuadGridF32 {
   const float4* __restrict__ q;
   int qy, qx;  // strides in quads: (nz-1), (ny-1)*(nz-1)
+  unsigned lim;  // quad count (RMPB_CHECKED builds)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && iy < qx / qy && iz < qy &&
+               (unsigned)(ix * qx + iy * qy + iz) + (unsigned)qx < lim);
     const float4* b = q + (unsigned)(ix * qx + iy * qy + iz);
     float4 a = __ldg(b), c = __ldg(b + (unsigned)qx);
     Corners k;
@@ -121,7 +147,10 @@ struct QuadGridF32 {
 struct PairGridF64 {
   const double2* __restrict__ q;
   int py, px;  // strides in pairs: (nz-1), ny*(nz-1)
+  unsigned lim;  // pair count (RMPB_CHECKED builds)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && iz < py &&
+               (unsigned)(ix * px + iy * py + iz) + (unsigned)(px + py) < lim);
     const double2* b = q + (unsigned)(ix * px + iy * py + iz);
     double2 a0 = __ldg(b), a1 = __ldg(b + (unsigned)py);
     double2 c0 = __ldg(b + (unsigned)px), c1 = __ldg(b + (unsigned)(px + py));
@@ -140,9 +169,13 @@ struct BrickGrid {
   const int32_t* __restrict__ table;
   int bny, bnz;
   T fill;
+  unsigned tlim, plim;  // table entries, allocated bricks (RMPB_CHECKED builds)
   static constexpr int B = 8;
   __device__ __forceinline__ double at(int i, int j, int k) const {
+    RMPB_CHECK(i >= 0 && j >= 0 && k >= 0 &&
+               (unsigned)(((i >> 3) * bny + (j >> 3)) * bnz + (k >> 3)) < tlim);
     int s = __ldg(table + ((i >> 3) * bny + (j >> 3)) * bnz + (k >> 3));
+    RMPB_CHECK(s < (int)plim);
     if (s < 0) return (double)fill;
     return (double)__ldg(pool + (int64_t)s * 512 + (((i & 7) << 6) | ((j & 7) << 3) | (k & 7)));
   }
@@ -150,7 +183,10 @@ struct BrickGrid {
     Corners c;
     if (((ix & 7) < 7) & ((iy & 7) < 7) & ((iz & 7) < 7)) {
       // all 8 corners in one brick (343 of 512 cells): one table lookup
+      RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 &&
+                 (unsigned)(((ix >> 3) * bny + (iy >> 3)) * bnz + (iz >> 3)) < tlim);
       const int sl = __ldg(table + ((ix >> 3) * bny + (iy >> 3)) * bnz + (iz >> 3));
+      RMPB_CHECK(sl < (int)plim);
       if (sl < 0) {
         const double f = (double)fill;
         c.v000 = c.v001 = c.v010 = c.v011 = c.v100 = c.v101 = c.v110 = c.v111 = f;

@@ -204,6 +204,7 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
   }
   if (!io.slot) return false;
   if (threadIdx.x == 0) {
+    RMPB_CHECK(seg >= 0 && seg < segs && pose >= 0);
     acc_to_arr(acc, io.partials + (size_t)(pose * segs + seg) * kAcc);
     __threadfence();
     unsigned prev = atomicAdd(io.tickets + pose, 1u);
@@ -629,6 +630,7 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem<NW>& sm, const G& grid, 
         const unsigned m = __ballot_sync(FULL, ok);
         if (ok) {
           const int pos = __popc(m & lt);
+          RMPB_CHECK(pos < kPrep && r >= begin && r < end && r < b.n);
           sm.pt[warp][pos] = t0; sm.pe[warp][pos] = t1;
           sm.px[warp][pos] = ex; sm.py[warp][pos] = ey; sm.pz[warp][pos] = ez;
 #if RMPB_TOWARD_FILTER
@@ -721,6 +723,7 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem<NW>& sm, const G& grid, 
     if (em) {
       if (enq) {
         const int pos = qn + __popc(em & lt);
+        RMPB_CHECK(pos < kQueue && rid < b.n);
         qt[pos] = (double)t;
         qr[pos] = rid;
       }
@@ -858,35 +861,6 @@ __device__ __forceinline__ void l2_prefetch(const void* p, unsigned bytes) {
 #define RMPB_LIDAR_PF 0  // groups of 128 beams prefetched ahead into L2 (0 = off)
 #endif
 
-// mbarrier + 1-D bulk copy (TMA) helpers for the LiDAR filter's stage ring.
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-  return (unsigned)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(unsigned long long* b, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(unsigned long long* b, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(unsigned long long* b, unsigned parity) {
-  asm volatile(
-      "{\n .reg .pred p;\n"
-      "WAIT%=: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      " @!p bra WAIT%=;\n}" ::"r"(smem_u32(b)), "r"(parity) : "memory");
-}
-// global -> shared bulk copy (16-B aligned, size a multiple of 16),
-// completion counted on mbarrier `b`; streaming data: L2 evict-first.
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, unsigned bytes,
-                                         unsigned long long* b) {
-  asm volatile(
-      "{\n .reg .b64 pol;\n"
-      " createpolicy.fractional.L2::evict_first.b64 pol, 1.0;\n"
-      " cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint"
-      " [%0], [%1], %2, [%3], pol;\n}" ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(b))
-      : "memory");
-}
-
 // Beam sources of the warp-unit kernel: a lattice scan (sensor directions +
 // ranges + validity, policies.py:195-205) or raw sensor-frame points (K2b).
 struct LatticeSrc {
@@ -933,28 +907,6 @@ struct LatticeSrc {
     l2_prefetch(rg + i0, 128 * sizeof(double));
     if (vl && ((reinterpret_cast<uintptr_t>(vl + i0) & 15) == 0)) l2_prefetch(vl + i0, 128);
   }
-  // TMA stage of one 128-beam group: 1024 B ranges | 128 B validity
-  static constexpr unsigned kStageBytes = 1152;
-  __device__ __forceinline__ bool bulk_ok(int i0, int end) const {
-    return i0 + 128 <= end && ((reinterpret_cast<uintptr_t>(rg + i0) & 15) == 0) &&
-           (!vl || (reinterpret_cast<uintptr_t>(vl + i0) & 15) == 0);
-  }
-  __device__ __forceinline__ void issue(unsigned char* slot, int i0, unsigned long long* bar) const {
-    mbar_expect_tx(bar, vl ? 1152u : 1024u);
-    bulk_g2s(slot, rg + i0, 1024u, bar);
-    if (vl) bulk_g2s(slot + 1024, vl + i0, 128u, bar);
-  }
-  __device__ __forceinline__ void read4(const unsigned char* slot, int lane, double (&o)[4]) const {
-    const double2 x0 = reinterpret_cast<const double2*>(slot)[2 * lane];
-    const double2 x1 = reinterpret_cast<const double2*>(slot)[2 * lane + 1];
-    o[0] = x0.x; o[1] = x0.y; o[2] = x1.x; o[3] = x1.y;
-    if (vl) {
-      const unsigned m = reinterpret_cast<const unsigned*>(slot + 1024)[lane];
-#pragma unroll
-      for (int j = 0; j < 4; ++j)
-        if (!((m >> (8 * j)) & 0xffu)) o[j] = CUDART_INF;
-    }
-  }
 };
 
 struct PointSrc {
@@ -994,21 +946,6 @@ struct PointSrc {
     if (!vec || i0 + 128 > end) return;
     l2_prefetch(P + 3 * (size_t)i0, 128 * 12);
   }
-  // TMA stage of one 128-point group: 1536 B xyz
-  static constexpr unsigned kStageBytes = 1536;
-  __device__ __forceinline__ bool bulk_ok(int i0, int end) const {
-    return i0 + 128 <= end && ((reinterpret_cast<uintptr_t>(P + 3 * (size_t)i0) & 15) == 0);
-  }
-  __device__ __forceinline__ void issue(unsigned char* slot, int i0, unsigned long long* bar) const {
-    mbar_expect_tx(bar, 1536u);
-    bulk_g2s(slot, P + 3 * (size_t)i0, 1536u, bar);
-  }
-  __device__ __forceinline__ void read4(const unsigned char* slot, int lane, double (&o)[4]) const {
-    const float4* q = reinterpret_cast<const float4*>(slot) + 3 * lane;
-    const float4 a = q[0], b = q[1], c = q[2];
-    o[0] = range(a.x, a.y, a.z); o[1] = range(a.w, b.x, b.y);
-    o[2] = range(b.z, b.w, c.x); o[3] = range(c.y, c.z, c.w);
-  }
 };
 
 // End of a LiDAR warp unit (lane 0 holds the unit's sums): resolve directly
@@ -1024,6 +961,7 @@ __device__ __forceinline__ void lidar_unit_finish(const Acc& a, const PoseIO& io
   }
   unsigned prev = 0;
   if (lane == 0) {
+    RMPB_CHECK(wu >= 0 && wu < wps && scan >= 0);
     acc_to_arr(a, io.partials + ((size_t)scan * wps + wu) * kAcc);
     __threadfence();
     prev = atomicAdd(io.tickets + scan, 1u);
@@ -1099,6 +1037,7 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
         if (enq) {
           int pos = h1 + q1n + __popc(em & lt);
           if (pos >= kRing1) pos -= kRing1;
+          RMPB_CHECK(pos >= 0 && pos < kRing1 && q1n + __popc(em) <= kRing1);
           w.q1d[pos] = d;
           w.q1i[pos] = base + 4 * lane + j;
         }
@@ -1117,6 +1056,7 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
         if (e >= kRing1) e -= kRing1;
         const int i = w.q1i[e];
         d = w.q1d[e];
+        RMPB_CHECK(i >= begin && i < end);
         double ex, ey, ez;
         src.dir(i, d, ex, ey, ez);
         wx = ex; wy = ey; wz = ez;
@@ -1133,6 +1073,7 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
       const unsigned km = __ballot_sync(FULL, keep);
       if (keep) {
         const int pos = (h2 + q2n + __popc(km & lt)) & (kRing2 - 1);
+        RMPB_CHECK(q2n + __popc(km) <= kRing2);
         w.q2d[pos] = d; w.q2x[pos] = wx; w.q2y[pos] = wy; w.q2z[pos] = wz;
       }
       q2n += __popc(km);
@@ -1172,214 +1113,12 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
   lidar_unit_finish(a, io, scan, wu, wps, lane);
 }
 
-// K2 v6 (default): warp-specialised.  A CTA holds NF filter warps and NF
-// policy warps; filter f and policy warp f own warp unit blockIdx.x * NF + f
-// -- the same units, beams and orders as v3 (k_lidar_warp).
-//  * the FILTER warp only streams: it keeps RMPB_LIDAR_PFD 128-beam groups
-//    of loads in flight, counts the valid beams and pushes the in-radius ones
-//    (range, beam index) into the unit's shared-memory queue -- no dependent
-//    loads, no fp64 chains, so the byte stream never waits behind them;
-//  * the POLICY warp pops the queue 32 entries at a time (v3's stage 1:
-//    lattice direction gather, rotation, closing test -> a local ring) and
-//    runs the transcendental fp64 policy 32 closing beams at a time (v3's
-//    stage 2) into lane-private running sums, then ends the unit (v3's fold).
-// v3 interleaves the stream with the gathers and the ~1000-cycle dependent
-// fp64 chains inside every warp; here they overlap across the warp pair.
-// Batches are cut at v3's positions (exactly 32, the remainder when the
-// unit is drained), so every lane sums the same values in the same order:
-// results are bitwise those of v3.
-// Queue protocol (one producer warp, one consumer warp, shared memory):
-// entries, then the volatile `tail` count (lane 0, after __syncwarp); the
-// consumer reads `done` then `tail`, then the entries; it publishes `head`
-// after reading them.
-#ifndef RMPB_LIDAR_NF
-#define RMPB_LIDAR_NF 4  // (filter, policy) warp pairs per CTA
-#endif
-#ifndef RMPB_LIDAR_PFD
-#define RMPB_LIDAR_PFD 4  // 128-beam groups in flight ahead of the filter (TMA stage ring)
-#endif
-#ifndef RMPB_WS_QUEUE
-#define RMPB_WS_QUEUE 256
-#endif
-constexpr int kLidarNF = RMPB_LIDAR_NF;
-constexpr int kQueueWs = RMPB_WS_QUEUE;  // in-radius entries per unit queue
-constexpr int kStageMax = 1536;  // bytes of one 128-beam group (points: 12 B each)
-struct LidarUnitSmem {
-  alignas(16) unsigned char stage[RMPB_LIDAR_PFD][kStageMax];  // filter's TMA ring
-  unsigned long long bar[RMPB_LIDAR_PFD];                       // one mbarrier per slot
-  double acc[9][32];  // the policy warp's lane-private running sums
-  double R[9], v[3];
-  double qd[kQueueWs];  // in-radius beams (range, beam index), filter -> policy
-  int qi[kQueueWs];
-  double q2d[kRing2], q2x[kRing2], q2y[kRing2], q2z[kRing2];  // closing beams (policy-local)
-  volatile int tail, head, done, cnt;
-};
-
-__device__ __forceinline__ int ws_load(volatile int* p) {
-  int v = 0;
-  if ((threadIdx.x & 31) == 0) v = *p;
-  return __shfl_sync(0xffffffffu, v, 0);
-}
-
-template <class Src>
-__global__ void __launch_bounds__(2 * kLidarNF * 32, RMPB_LIDAR_MINB)
-k_lidar_ws(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits) {
-  extern __shared__ __align__(16) unsigned char lidar_ws_dsm[];
-  LidarUnitSmem* units = reinterpret_cast<LidarUnitSmem*>(lidar_ws_dsm);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const int f = warp % kLidarNF;
-  const bool filter = warp < kLidarNF;
-  const long long unit = (long long)blockIdx.x * kLidarNF + f;
-  if (unit >= nunits) return;  // both warps of the pair (only the pair's barrier follows)
-  const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
-  LidarUnitSmem& w = units[f];
-  if (filter && lane == 0) { w.tail = 0; w.head = 0; w.done = 0; w.cnt = 0; }
-  // pair barrier (named barrier 1 + f, 64 threads): the counters are set
-  asm volatile("bar.sync %0, 64;" ::"r"(1 + f) : "memory");
-  if (filter) {
-    // ---------------- filter warp: stream + count + in-radius queue
-    src.bind(scan);
-    const int begin = wu * seg;
-    const int end = min(begin + seg, src.count());
-    int cnt = 0, tail = 0, room = kQueueWs;  // room: known free entries (head lower bound)
-    constexpr int K = RMPB_LIDAR_PFD;
-    const int ngroups = (end - begin + 127) >> 7;
-    if (lane == 0) {
-#pragma unroll
-      for (int s = 0; s < K; ++s) mbar_init(&w.bar[s], 1);
-      asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-      for (int g = 0; g < K && g < ngroups; ++g)  // fill the ring
-        if (src.bulk_ok(begin + 128 * g, end)) src.issue(w.stage[g], begin + 128 * g, &w.bar[g]);
-    }
-    __syncwarp();
-    for (int g = 0; g < ngroups; ++g) {
-      const int base = begin + 128 * g;
-      const int s = g % K;
-      double cur[4];
-      if (src.bulk_ok(base, end)) {  // (warp-uniform)
-        mbar_wait(&w.bar[s], (unsigned)((g / K) & 1));
-        src.read4(w.stage[s], lane, cur);
-      } else {
-        src.load4(base + 4 * lane, end, cur);  // ragged tail / misaligned row
-      }
-      __syncwarp();  // every lane has read slot s: refill it
-      if (lane == 0 && g + K < ngroups && src.bulk_ok(base + 128 * K, end))
-        src.issue(w.stage[s], base + 128 * K, &w.bar[s]);
-      // a group pushes at most 128 entries: make sure they fit
-      if (room < 128) {
-        while (true) {
-          room = kQueueWs - (tail - ws_load(&w.head));
-          if (room >= 128) break;
-          __nanosleep(32);
-        }
-      }
-      const int t0 = tail;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        const double d = cur[j];
-        const bool counted = !(d != d || d == CUDART_INF || d < p.min_range);
-        cnt += counted;
-        const bool enq = counted && d < p.radius;
-        const unsigned em = __ballot_sync(FULL, enq);
-        if (enq) {
-          const int pos = (tail + __popc(em & lt)) & (kQueueWs - 1);
-          w.qd[pos] = d;
-          w.qi[pos] = base + 4 * lane + j;
-        }
-        tail += __popc(em);
-      }
-      room -= tail - t0;
-      if (tail != t0) {
-        __syncwarp();
-        if (lane == 0) w.tail = tail;
-      }
-    }
-    cnt = warp_sum_i(cnt);
-    __syncwarp();
-    if (lane == 0) { w.cnt = cnt; __threadfence_block(); w.done = 1; }
-    return;
-  }
-  // ---------------- policy warp: v3's stages 1 and 2 over the queue
-  const double* Rall = src.rot();
-  const bool rot = Rall != nullptr;
-  if (rot && lane < 9) w.R[lane] = Rall[9 * scan + lane];
-  if (lane == 0) io.vel(scan, w.v[0], w.v[1], w.v[2]);
-#pragma unroll
-  for (int k = 0; k < 9; ++k) w.acc[k][lane] = 0.0;
-  src.bind(scan);
-  __syncwarp();
-  int head = 0, h2 = 0, q2n = 0;
-  while (true) {
-    int done, tail;
-    while (true) {
-      done = ws_load(&w.done);  // before `tail`: a done filter's tail is final
-      tail = ws_load(&w.tail);
-      if (tail - head >= 32 || done) break;
-      __nanosleep(64);
-    }
-    const int q1n = tail - head;
-    const bool draining = done && q1n < 32;
-    if (q1n == 0 && q2n == 0) break;  // done and drained
-    // stage 1: 32 queue entries (the remainder once drained)
-    if (q1n > 0) {
-      const int take = min(q1n, 32);
-      bool keep = false;
-      double d = 0, wx = 0, wy = 0, wz = 0;
-      if (lane < take) {
-        const int e = (head + lane) & (kQueueWs - 1);
-        const int i = w.qi[e];
-        d = w.qd[e];
-        double ex, ey, ez;
-        src.dir(i, d, ex, ey, ez);
-        wx = ex; wy = ey; wz = ez;
-        if (rot) {  // directions @ orientation.T  (rays.py:172-173)
-          wx = ex * w.R[0] + ey * w.R[1] + ez * w.R[2];
-          wy = ex * w.R[3] + ey * w.R[4] + ez * w.R[5];
-          wz = ex * w.R[6] + ey * w.R[7] + ez * w.R[8];
-        }
-        keep = wx * w.v[0] + wy * w.v[1] + wz * w.v[2] > 0.0;  // policy_accumulate's test
-      }
-      head += take;
-      __syncwarp();
-      if (lane == 0) w.head = head;
-      const unsigned km = __ballot_sync(FULL, keep);
-      if (keep) {
-        const int pos = (h2 + q2n + __popc(km & lt)) & (kRing2 - 1);
-        w.q2d[pos] = d; w.q2x[pos] = wx; w.q2y[pos] = wy; w.q2z[pos] = wz;
-      }
-      q2n += __popc(km);
-      __syncwarp();
-    }
-    // stage 2: 32 closing beams (the remainder once everything is staged)
-    const bool last = draining && tail - head == 0;
-    if (q2n >= 32 || (last && q2n > 0)) {
-      const int t2 = min(q2n, 32);
-      Acc a;
-      a.zero();
-      if (lane < t2) {
-        const int e = (h2 + lane) & (kRing2 - 1);
-        policy_accumulate(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2], p);
-      }
-      h2 = (h2 + t2) & (kRing2 - 1);
-      q2n -= t2;
-      if (lane < t2) {  // lane-private running sums (v3's order)
-        w.acc[0][lane] += a.a00; w.acc[1][lane] += a.a01; w.acc[2][lane] += a.a02;
-        w.acc[3][lane] += a.a11; w.acc[4][lane] += a.a12; w.acc[5][lane] += a.a22;
-        w.acc[6][lane] += a.b0; w.acc[7][lane] += a.b1; w.acc[8][lane] += a.b2;
-      }
-      __syncwarp();
-    }
-  }
-  __syncwarp();
-  double ws[9];
-#pragma unroll
-  for (int k = 0; k < 9; ++k) ws[k] = warp_sum(w.acc[k][lane]);
-  Acc a;
-  a.a00 = ws[0]; a.a01 = ws[1]; a.a02 = ws[2]; a.a11 = ws[3]; a.a12 = ws[4];
-  a.a22 = ws[5]; a.b0 = ws[6]; a.b1 = ws[7]; a.b2 = ws[8]; a.cnt = ws_load(&w.cnt);
-  lidar_unit_finish(a, io, scan, wu, wps, lane);
-}
+// (Measured, round 2: a warp-specialised variant -- per CTA, filter warps
+// streaming through a TMA stage ring into shared-memory queues and paired
+// policy warps running stages 1 and 2 -- is bitwise equal to this kernel
+// but slower on C3: 0.62-0.70 ms vs 0.51 ms per 1024 scans (commit ae35050,
+// profiles/README.md).  Half the warps stream, and the pairs' per-unit
+// latency, not the byte stream, bounds it.)
 
 // Unfused parity entry (ckern.policy_reduce, ckern.py:80-93): reduce given
 // (dirs, dists) -- AoS host layout -- into a slot.

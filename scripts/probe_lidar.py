@@ -1,7 +1,6 @@
 """LiDAR kernels on C3 (1024 scans x 128x1024 beams, GPU box): best / median
 ms per launch (CUDA events, L2 flushed between launches), HBM fraction of the
-9 B/beam stream, and bitwise equality with kernel 3 at the same units.
-args: "K:T" = lidar_kernel K (3 or 6) with T target warp units."""
+9 B/beam stream.  args: target warp units per launch (option lidar_warps)."""
 import json
 import os
 import sys
@@ -28,10 +27,8 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     "MEASURED_PEAKS.json") else 6547.8
-ref = {}
-for arg in sys.argv[1:] or ["3:76000", "6:76000"]:
-    k, t = (int(x) for x in arg.split(":"))
-    _lib.call("rmpb_set_option", b"lidar_kernel", k)
+for arg in sys.argv[1:] or ["76000"]:
+    t = int(arg)
     _lib.call("rmpb_set_option", b"lidar_warps", t)
     sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
     torch.cuda.synchronize()
@@ -43,13 +40,9 @@ for arg in sys.argv[1:] or ["3:76000", "6:76000"]:
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     s_np = sl.cpu().numpy()
-    if k == 3:
-        ref[t] = s_np
-    same = bool(np.array_equal(ref[t], s_np, equal_nan=True)) if t in ref else None
     ms = min(ts)
-    print(json.dumps({"kernel": k, "target_units": t, "ms_min": round(ms, 4),
+    print(json.dumps({"target_units": t, "ms_min": round(ms, 4),
                       "ms_med": round(sorted(ts)[3], 4),
                       "hbm_frac": round(9 * 131072 * S / (ms * 1e-3) / 1e9 / peak, 4),
-                      "bitwise_eq_v3": same, "hits": int(s_np[:, 12].sum())}), flush=True)
-_lib.call("rmpb_set_option", b"lidar_kernel", 0)
+                      "hits": int(s_np[:, 12].sum())}), flush=True)
 _lib.call("rmpb_set_option", b"lidar_warps", 76000)

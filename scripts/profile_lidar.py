@@ -15,9 +15,6 @@ vl = torch.from_numpy(np.stack([scans[i % 10].valid for i in range(S)]).astype(n
 R = torch.eye(3, dtype=torch.float64, device="cuda").reshape(1, 9).repeat(S, 1).contiguous()
 v = torch.from_numpy(np.stack([states[i % 10].velocity for i in range(S)])).cuda()
 LIDAR = (1.2, 1.5, 3.0, 1.0, 1e-6, 1.3, 1.0)
-if os.environ.get("LIDAR_KERNEL"):
-    from paper_2301_08068_b200 import _lib
-    _lib.call("rmpb_set_option", b"lidar_kernel", int(os.environ["LIDAR_KERNEL"]))
 for _ in range(2):
     lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
 torch.cuda.synchronize()
