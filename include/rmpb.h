@@ -87,7 +87,12 @@ RMPB_EXPORT int rmpb_api_version(void);
 RMPB_EXPORT int rmpb_device_count(int* n);
 /* Number of kernels this library has launched (all devices, since load). */
 RMPB_EXPORT uint64_t rmpb_launch_count(void);
-/* Tuning knobs ("seg_rays": rays per CTA unit, 0 = heuristic). */
+/* Tuning knobs: "seg_rays" (rays per CTA unit, 0 = heuristic), "kernel"
+ * (0 auto, 1 one ray per thread, 2 lane refill), "lidar_warps" (target warp
+ * units per LiDAR launch), "l2_window" (0/1: the map's L2 access-policy
+ * window), "graphs" (0/1: CUDA-graph rollout ticks), "carveout" (-1 or the
+ * shared-memory carveout % of the trace kernel).  Results do not depend on
+ * them beyond the last bits of the sums (fixed per setting). */
 RMPB_EXPORT int rmpb_set_option(const char* name, int64_t value);
 
 /* ---- maps (EsdfGrid, rmpnav/geometry.py:215-255) ------------------------ */

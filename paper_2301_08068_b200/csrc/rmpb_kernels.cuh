@@ -70,6 +70,21 @@ __device__ __forceinline__ unsigned long long ld_acquire_gpu(const unsigned long
   asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
   return v;
 }
+// Last-arriver tickets: every arriver publishes its partial with a RELEASE
+// atomic (orders its prior stores; no L1 invalidation), and only the last
+// arriver issues an ACQUIRE fence before reading the others' partials.  The
+// former __threadfence() + atomicAdd emitted MEMBAR.SC.GPU + CCTL.IVALL at
+// every arrival, invalidating the whole SM's L1 (the map / lattice lines
+// the other CTAs were using) once per unit.
+__device__ __forceinline__ unsigned ticket_add_release(unsigned* p) {
+  unsigned old;
+  asm volatile("atom.release.gpu.global.add.u32 %0, [%1], 1;" : "=r"(old) : "l"(p) : "memory");
+  return old;
+}
+__device__ __forceinline__ void fence_acquire_gpu() {
+  asm volatile("fence.acq_rel.gpu;" ::: "memory");
+}
+
 __device__ __forceinline__ unsigned long long globaltimer_ns() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
@@ -206,13 +221,12 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
   if (threadIdx.x == 0) {
     RMPB_CHECK(seg >= 0 && seg < segs && pose >= 0);
     acc_to_arr(acc, io.partials + (size_t)(pose * segs + seg) * kAcc);
-    __threadfence();
-    unsigned prev = atomicAdd(io.tickets + pose, 1u);
+    const unsigned prev = ticket_add_release(io.tickets + pose);
     s_last = (prev == (unsigned)(segs - 1));
+    if (s_last) fence_acquire_gpu();  // the other segments' partials are visible
   }
   __syncthreads();
   if (!s_last) return false;
-  __threadfence();
   // Fixed-order fold of this pose's partials: thread j sums segments
   // j, j+kBlock, ... sequentially, then the fixed block tree.
   Acc f;
@@ -963,12 +977,12 @@ __device__ __forceinline__ void lidar_unit_finish(const Acc& a, const PoseIO& io
   if (lane == 0) {
     RMPB_CHECK(wu >= 0 && wu < wps && scan >= 0);
     acc_to_arr(a, io.partials + ((size_t)scan * wps + wu) * kAcc);
-    __threadfence();
-    prev = atomicAdd(io.tickets + scan, 1u);
+    prev = ticket_add_release(io.tickets + scan);
+    if (prev == (unsigned)(wps - 1)) fence_acquire_gpu();  // the other units' partials
   }
   prev = __shfl_sync(FULL, prev, 0);
   if (prev != (unsigned)(wps - 1)) return;
-  __threadfence();
+  __syncwarp();
   double f[kAcc];
 #pragma unroll
   for (int k = 0; k < kAcc; ++k) f[k] = 0.0;
