@@ -319,6 +319,8 @@ def run_b200(args):
         configs["C3_lidar_1024_scans"] = c3_config(dev, stream, peaks["hbm_gbs"], flush,
                                                    cpu=(world == 1 and not args.no_cpu_baseline))
         configs["C2_1M_rays_10m"] = c2_config(grid, dev, stream, flush, params)
+        if world == 1:
+            configs["C5_1M_rays_ray_split"] = c5_config(dev, stream)
 
     out = None
     if rank == 0:
@@ -564,6 +566,52 @@ def c2_config(grid, dev, stream, flush, params, P=64):
             "ms_per_launch_best": round(best, 3), "ms_per_launch_median": round(med, 3),
             "rays_per_s": round(P * n / (best * 1e-3), 1),
             "evaluations_per_s": round(P / (best * 1e-3), 1)}
+
+
+def c5_config(dev, stream, steps=20):
+    """Config C5 at N = 1 inside the default line: one 1 M-ray pose on the
+    1000x1000x200 block-hashed TSDF through the K4 exchange kernel (world-1
+    mailbox; `--workload c5` under torchrun splits it over GPUs)."""
+    import torch
+
+    from paper_2301_08068_b200 import synth
+    from paper_2301_08068_b200._kernels import b200
+    from paper_2301_08068_b200.device import PeerMailbox, RayPolicyEngine
+
+    scene = synth.c5_scene()
+    _dense, brick, info = synth.c5_grids(scene)
+    del _dense
+    states = synth.bench_states(scene, count=8, seed=123, distance=synth.host_box_distance(scene))
+    n = 1 << 20
+    eng = RayPolicyEngine(brick, b200.DeviceBundle(halton_n=n), PARAMS, MAX_RANGE)
+    xs = [torch.tensor(s.position, dtype=torch.float64, device=dev) for s in states]
+    vs = [torch.tensor(s.velocity, dtype=torch.float64, device=dev) for s in states]
+    mb = PeerMailbox(1, 0)
+    mb.open([mb.ipc_handle])
+    ep = [0]
+
+    def one(k):
+        ep[0] += 1
+        eng.exchange(xs[k % 8], vs[k % 8], mb, ep[0], 0, n)
+    for k in range(5):
+        one(k)
+    torch.cuda.synchronize()
+    ts = []
+    for k in range(steps):
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        one(k)
+        e1.record(stream)
+        e1.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    mb.close()
+    ms = statistics.median(ts)
+    return {"rays_per_pose": n, "map": "1000x1000x200 @0.05 m TSDF (tau 0.2 m), BRICK 8^3 f32",
+            "bricks_allocated": info["bricks_allocated"], "brick_bytes": info["brick_bytes"],
+            "ms_per_pose_median": round(ms, 4), "ms_per_pose_best": round(min(ts), 4),
+            "rays_per_s": round(n / (ms * 1e-3), 1), "hz": round(1e3 / ms, 1),
+            "kernel": "k_ray_policy<BrickGrid<float>, EX> (K4 exchange epilogue, world 1)"}
 
 
 def run_c5(args):
