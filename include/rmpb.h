@@ -89,7 +89,8 @@ RMPB_EXPORT int rmpb_device_count(int* n);
 RMPB_EXPORT uint64_t rmpb_launch_count(void);
 /* Tuning knobs: "seg_rays" (rays per CTA unit, 0 = heuristic), "kernel"
  * (0 auto, 1 one ray per thread, 2 lane refill), "lidar_warps" (target warp
- * units per LiDAR launch), "l2_window" (0/1: the map's L2 access-policy
+ * units per LiDAR launch), "lidar_persist" (0/1: persistent LiDAR warps
+ * claiming units from a counter), "l2_window" (0/1: the map's L2 access-policy
  * window), "graphs" (0/1: CUDA-graph rollout ticks), "carveout" (-1 or the
  * shared-memory carveout % of the trace kernel).  Results do not depend on
  * them beyond the last bits of the sums (fixed per setting). */

@@ -40,7 +40,8 @@ static std::atomic<int64_t> g_opt_kernel{0};  // 0 auto, 1 one ray per thread pe
 static std::atomic<int64_t> g_opt_carveout{-1};
 static std::atomic<int64_t> g_opt_l2_window{1};  // map access-policy window on trace launches
 static std::atomic<int64_t> g_opt_graphs{1};     // CUDA-graph replay of rollout ticks
-static std::atomic<int64_t> g_opt_lidar_warps{76000};  // LiDAR: target warp units per launch
+static std::atomic<int64_t> g_opt_lidar_warps{38000};  // LiDAR: target warp units per launch
+static std::atomic<int64_t> g_opt_lidar_persist{1};  // LiDAR: persistent warps claiming units
 
 static int fail(int code, const char* fmt, ...) {
   char buf[512];
@@ -161,6 +162,15 @@ struct Workspace {
   size_t tickets_n = 0;
   HostBuf hres;    // pinned + mapped results (slots / accels)
   HostBuf hin;     // pinned staging of host inputs
+  DevBuf sched;  // persistent-kernel unit counters (zeroed once, self-resetting)
+  bool sched_ok = false;
+  int ensure_sched() {
+    if (sched_ok) return RMPB_OK;
+    TRY(sched.ensure(2 * sizeof(unsigned long long)));
+    CK(cudaMemset(sched.p, 0, 2 * sizeof(unsigned long long)));
+    sched_ok = true;
+    return RMPB_OK;
+  }
   int ensure_tickets(size_t n) {
     if (n <= tickets_n) return RMPB_OK;
     TRY(tickets.ensure(n * sizeof(unsigned)));
@@ -333,6 +343,11 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
   if (!strcmp(name, "l2_window")) {
     if (value < 0 || value > 1) return fail(RMPB_ERR_INVALID, "l2_window must be 0 or 1");
     g_opt_l2_window.store(value);
+    return RMPB_OK;
+  }
+  if (!strcmp(name, "lidar_persist")) {
+    if (value < 0 || value > 1) return fail(RMPB_ERR_INVALID, "lidar_persist must be 0 or 1");
+    g_opt_lidar_persist.store(value);
     return RMPB_OK;
   }
   if (!strcmp(name, "carveout")) {
@@ -1640,9 +1655,21 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
   io.slot = d_slot; io.accel = d_accel;
   io.partials = (double*)ws->partials.p;
   io.tickets = (unsigned*)ws->tickets.p;
-  const long long blocks = (nunits + kWarps - 1) / kWarps;
+  long long blocks = (nunits + kWarps - 1) / kWarps;
   if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
   const size_t smem = sizeof(LidarWarpSmem) * kWarps;
+  unsigned long long* sched = nullptr;
+  if (g_opt_lidar_persist.load()) {  // persistent warps: one full wave of CTAs
+    int sms = 0, dv = 0;
+    CK(cudaGetDevice(&dv));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv));
+    const long long full = (long long)sms * RMPB_LIDAR_MINB;
+    if (blocks > full) {
+      blocks = full;
+      TRY(ws->ensure_sched());
+      sched = (unsigned long long*)ws->sched.p;
+    }
+  }
   static std::once_flag once[64];
   int dev = 0;
   CK(cudaGetDevice(&dev));
@@ -1651,7 +1678,7 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
                          (int)smem);
   });
   k_lidar_warp<Src><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps, (int)seg,
-                                                             nunits);
+                                                             nunits, sched);
   CKL();
   return RMPB_OK;
 }

@@ -1008,16 +1008,13 @@ __device__ __forceinline__ void lidar_unit_finish(const Acc& a, const PoseIO& io
 #define RMPB_LIDAR_MINB 4
 #endif
 template <class Src>
-__global__ void __launch_bounds__(kBlock, RMPB_LIDAR_MINB)
-k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits) {
-  extern __shared__ __align__(16) unsigned char lidar_dsm[];  // kWarps x LidarWarpSmem
-  LidarWarpSmem* smw = reinterpret_cast<LidarWarpSmem*>(lidar_dsm);
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+__device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const PolicyParams& p,
+                                                int wps, int seg, long long unit,
+                                                LidarWarpSmem& w) {
+  const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
-  const long long unit = (long long)blockIdx.x * kWarps + warp;
-  if (unit >= nunits) return;
   const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
-  LidarWarpSmem& w = smw[warp];
+  __syncwarp();  // the previous unit's reads of w are done
   const double* Rall = src.rot();
   const bool rot = Rall != nullptr;
   if (rot && lane < 9) w.R[lane] = Rall[9 * scan + lane];
@@ -1126,6 +1123,36 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
   a.a22 = ws[5]; a.b0 = ws[6]; a.b1 = ws[7]; a.b2 = ws[8]; a.cnt = cnt;
   lidar_unit_finish(a, io, scan, wu, wps, lane);
 }
+
+template <class Src>
+__global__ void __launch_bounds__(kBlock, RMPB_LIDAR_MINB)
+k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits,
+             unsigned long long* __restrict__ sched) {
+  extern __shared__ __align__(16) unsigned char lidar_dsm[];  // kWarps x LidarWarpSmem
+  LidarWarpSmem* smw = reinterpret_cast<LidarWarpSmem*>(lidar_dsm);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (sched == nullptr) {  // one unit per warp (the hardware block scheduler balances)
+    const long long unit = (long long)blockIdx.x * kWarps + warp;
+    if (unit < nunits) lidar_warp_unit(src, io, p, wps, seg, unit, smw[warp]);
+    return;
+  }
+  // Persistent warps claiming units from a counter (sched[0]); a unit's
+  // result does not depend on which warp runs it, so this is bitwise the
+  // one-unit-per-warp schedule.  sched[1] counts finished warps; the last
+  // one resets both (graph replays / the next call start at zero).
+  while (true) {
+    unsigned long long u = 0;
+    if (lane == 0) u = atomicAdd(sched, 1ull);
+    u = __shfl_sync(0xffffffffu, u, 0);
+    if ((long long)u >= nunits) break;
+    lidar_warp_unit(src, io, p, wps, seg, (long long)u, smw[warp]);
+  }
+  if (lane == 0) {
+    const unsigned long long W = (unsigned long long)gridDim.x * kWarps;
+    if (atomicAdd(sched + 1, 1ull) == W - 1) { sched[0] = 0ull; sched[1] = 0ull; }
+  }
+}
+
 
 // (Measured, round 2: a warp-specialised variant -- per CTA, filter warps
 // streaming through a TMA stage ring into shared-memory queues and paired

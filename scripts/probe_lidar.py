@@ -27,9 +27,11 @@ flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 peak = json.load(open(os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))),
                                    "MEASURED_PEAKS.json")))["hbm_gbs"] if os.path.exists(
     "MEASURED_PEAKS.json") else 6547.8
-for arg in sys.argv[1:] or ["76000"]:
-    t = int(arg)
+for arg in sys.argv[1:] or ["38000"]:
+    t, _, pers = arg.partition(":")
+    t = int(t)
     _lib.call("rmpb_set_option", b"lidar_warps", t)
+    _lib.call("rmpb_set_option", b"lidar_persist", int(pers or 1))
     sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
     torch.cuda.synchronize()
     ts = []
@@ -41,8 +43,9 @@ for arg in sys.argv[1:] or ["76000"]:
         ts.append(e0.elapsed_time(e1))
     s_np = sl.cpu().numpy()
     ms = min(ts)
-    print(json.dumps({"target_units": t, "ms_min": round(ms, 4),
+    print(json.dumps({"target_units": t, "persist": int(pers or 1), "ms_min": round(ms, 4),
                       "ms_med": round(sorted(ts)[3], 4),
                       "hbm_frac": round(9 * 131072 * S / (ms * 1e-3) / 1e9 / peak, 4),
                       "hits": int(s_np[:, 12].sum())}), flush=True)
-_lib.call("rmpb_set_option", b"lidar_warps", 76000)
+_lib.call("rmpb_set_option", b"lidar_warps", 38000)
+_lib.call("rmpb_set_option", b"lidar_persist", 1)

@@ -94,7 +94,7 @@ def main():
     rgs = rng.uniform(0.0, 3.0, (S, n))
     valid = rng.random((S, n)) < 0.8
     Rs = np.stack([np.linalg.qr(rng.normal(size=(3, 3)))[0] for _ in range(S)]).reshape(S, 9)
-    for tgt in (76000, 3):
+    for tgt in (38000, 3):
         _lib.set_option("lidar_warps", tgt)
         lidar_policy_batch_device(torch.from_numpy(d).cuda(), torch.from_numpy(Rs.copy()).cuda(),
                                   torch.from_numpy(rgs).cuda(),
@@ -103,7 +103,7 @@ def main():
         pts = torch.from_numpy(rng.uniform(-2, 2, (S, n, 3)).astype(np.float32)).cuda()
         lidar_points_batch_device(pts, None, torch.from_numpy(rng.normal(size=(S, 3))).cuda(),
                                   LIDAR, 0.3)
-    _lib.set_option("lidar_warps", 76000)
+    _lib.set_option("lidar_warps", 38000)
     scan = synth.lidar_scans(scene, states[:1], 16, 64, 10.0)[0]
     P.lidar_policy(states[0].velocity, scan, P.preset("lidar").obstacle)
     say("k_lidar_warp (lattice, points, fold) + scene trace")

@@ -701,7 +701,7 @@ def test_lidar_points_batch_device(be, oracle, c1):
 # LiDAR warp-unit decompositions: the default target (many short units,
 # multi-unit fold per scan), 1000 and 3 units per launch (long units: many
 # 128-beam groups per warp, ring wrap-around)
-LIDAR_WARP_TARGETS = (76000, 1000, 3)
+LIDAR_WARP_TARGETS = (38000, 1000, 3)
 
 
 @pytest.mark.parametrize("n,S", [(131072, 1), (1000, 5), (131, 3), (97, 2), (4096, 40), (8192, 3)])
@@ -739,8 +739,15 @@ def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
                 outs = {}
                 for k in LIDAR_WARP_TARGETS:
                     _lib.call("rmpb_set_option", b"lidar_warps", k)
-                    sl, ac = lidar_policy_batch_device(d_dirs, d_R, d_rg, d_vl, d_v, LIDAR, 0.3)
-                    outs[k] = (sl.cpu().numpy(), ac.cpu().numpy())
+                    got = []
+                    for persist in (1, 0):  # persistent warps claiming units / one unit per warp
+                        _lib.call("rmpb_set_option", b"lidar_persist", persist)
+                        sl, ac = lidar_policy_batch_device(d_dirs, d_R, d_rg, d_vl, d_v, LIDAR, 0.3)
+                        got.append((sl.cpu().numpy(), ac.cpu().numpy()))
+                    _lib.call("rmpb_set_option", b"lidar_persist", 1)
+                    assert np.array_equal(got[0][0], got[1][0], equal_nan=True)  # same units
+                    assert np.array_equal(got[0][1], got[1][1], equal_nan=True)
+                    outs[k] = got[0]
                 for s in range(S):
                     wd = dirs @ Rs[s].T if use_R else dirs
                     vv = valid[s] if use_valid else np.ones(n, bool)
@@ -752,7 +759,8 @@ def test_lidar_kernels_ragged_and_misaligned(be, oracle, n, S):
                         if slot_r[12] > 0 and np.abs(slot_r[:9]).max() > 0:
                             assert rel_err(ac[s], acc_r) <= ACC_TOL, (k, s)
     finally:
-        _lib.call("rmpb_set_option", b"lidar_warps", 76000)
+        _lib.call("rmpb_set_option", b"lidar_warps", 38000)
+        _lib.call("rmpb_set_option", b"lidar_persist", 1)
 
 
 @pytest.mark.parametrize("n,S", [(131072, 1), (1001, 4), (131, 3), (4096, 6)])
@@ -793,7 +801,8 @@ def test_lidar_points_kernels_ragged(be, oracle, n, S):
                     assert sl[s][12] == slot_r[12], (k, s)
                     assert rel_err(sl[s][:12], slot_r[:12]) <= SUM_TOL, (k, s)
     finally:
-        _lib.call("rmpb_set_option", b"lidar_warps", 76000)
+        _lib.call("rmpb_set_option", b"lidar_warps", 38000)
+        _lib.call("rmpb_set_option", b"lidar_persist", 1)
 
 
 # --- host fast path: repeated calls with the same arrays -----------------------
