@@ -126,6 +126,11 @@ RMPB_EXPORT int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype);
  * every grid_trace call, rmpnav/_kernels/ckern.py:49-62). */
 RMPB_EXPORT int rmpb_grid_update_region(rmpb_grid* g, const void* values, int dtype, int64_t i0,
                                         int64_t j0, int64_t k0, int64_t ni, int64_t nj, int64_t nk);
+/* Host-only: *out = 1 when the 2-op exact division (q = fma(a, yhi, a*ylo))
+ * is proven correctly rounded for divisor `res` (every normal |a| >=
+ * 2^-960); maps with such a resolution trace with it.  Exactness is the
+ * same either way (rmpnav/_kernels/_ckern.pyx:92-135 divides with IEEE /). */
+RMPB_EXPORT int rmpb_div2_exact(double res, int* out);
 RMPB_EXPORT int rmpb_grid_info(const rmpb_grid* g, int* storage, int* layout, int64_t* device_bytes,
                    int64_t* allocated_bricks);
 RMPB_EXPORT int rmpb_grid_destroy(rmpb_grid* g);

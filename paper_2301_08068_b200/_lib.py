@@ -51,6 +51,7 @@ _SIGS = {
     "rmpb_grid_update": (_i, [_vp, _vp, _i]),
     "rmpb_grid_update_region": (_i, [_vp, _vp, _i, _i64, _i64, _i64, _i64, _i64, _i64]),
     "rmpb_grid_info": (_i, [_vp, _vp, _vp, _vp, _vp]),
+    "rmpb_div2_exact": (_i, [_d, _vp]),
     "rmpb_grid_destroy": (_i, [_vp]),
     "rmpb_bundle_create": (_i, [_vp, _i64, _i, _i, _vp]),
     "rmpb_bundle_halton": (_i, [_i64, _i, _i, _vp]),

@@ -8,6 +8,7 @@
 #include <cub/device/device_scan.cuh>
 
 #include <algorithm>
+#include <cmath>
 #include <atomic>
 #include <chrono>
 #include <cstdarg>
@@ -249,6 +250,18 @@ static int with_grid(const rmpb_grid* g, F&& f) {
   if (g->layout == LAYOUT_QUAD) {  // f32 storage only (grid_build)
     QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1),
                   (unsigned)(g->nx * (g->ny - 1) * (g->nz - 1))};
+    const bool o0 = G.ox == 0.0 && G.oy == 0.0 && G.oz == 0.0 && !std::signbit(G.ox) &&
+                    !std::signbit(G.oy) && !std::signbit(G.oz);  // +0.0 only: p - (+0) == p
+    if (G.div2 && o0) {  // + origin at (+0, +0, +0): the subtraction leaves the chain
+      QuadGridF32Div2O0 a3;
+      static_cast<QuadGridF32&>(a3) = a;
+      return f(a3);
+    }
+    if (G.div2) {  // the 2-op exact division is proven for this resolution
+      QuadGridF32Div2 a2;
+      static_cast<QuadGridF32&>(a2) = a;
+      return f(a2);
+    }
     return f(a);
   }
   if (g->storage == RMPB_STORE_F32) {
@@ -365,6 +378,65 @@ extern "C" int rmpb_set_option(const char* name, int64_t value) {
 
 // ---------------------------------------------------------------------------
 // grids
+
+// Proof that exdiv2 (rmpb_device.cuh) is the correctly rounded a / b for
+// every normal |a| >= 2^-960 (no overflow) and this divisor b.  Write a, b
+// with integer mantissas A, B in [2^52, 2^53).  q0 errs by at most
+// 1.5 * 2^-105 |a/b|, so a wrong rounding needs A/B within that of a
+// midpoint (2k+1) 2^-s (s = 53 for A >= B, 54 for A < B), i.e.
+// D = 2^s A - (2k+1) B with |D| <= 6.  For B = 2^c B' (B' odd) D must be a
+// multiple of 2^c and A == D (2^s)^-1 (mod B'): a few candidates per D,
+// each (and its neighbours) evaluated exactly here, over |D| <= 64.
+static bool div2_exact(double b) {
+  if (!(b >= 0x1p-20 && b <= 0x1p20)) return false;
+  int eb = 0;
+  const double mb = frexp(b, &eb);
+  const uint64_t B = (uint64_t)ldexp(mb, 53);
+  const int c = __builtin_ctzll(B);
+  const uint64_t Bp = B >> c;
+  double yh, yl;
+  recip_dd(b, yh, yl);
+  if (Bp == 1) return true;  // a power of two: a * yh is exact
+  if (c > 16) return false;  // too many candidates to enumerate
+  auto mulmod = [](uint64_t x, uint64_t y, uint64_t m) {
+    return (uint64_t)((unsigned __int128)x * y % m);
+  };
+  const uint64_t lo = 1ull << 52, hi = 1ull << 53;
+  for (int s = 53; s <= 54; ++s) {
+    uint64_t inv = 1;  // (2^s)^-1 mod Bp = ((Bp + 1) / 2)^s
+    for (int k = 0; k < s; ++k) inv = mulmod(inv, (Bp + 1) / 2, Bp);
+    for (long D = -64; D <= 64; ++D) {
+      if (D == 0 || D % (1L << c) != 0) continue;
+      const uint64_t Dm = (uint64_t)((((__int128)D % (__int128)Bp) + (__int128)Bp) % (__int128)Bp);
+      const uint64_t A0 = mulmod(Dm, inv, Bp);
+      const uint64_t first = A0 + (lo > A0 ? ((lo - A0 + Bp - 1) / Bp) * Bp : 0);
+      for (uint64_t A = first; A < hi; A += Bp) {
+        if ((s == 53) != (A >= B)) continue;
+        const __int128 num = ((__int128)A << s) - D;
+        if (num % (__int128)B != 0) continue;
+        if ((((unsigned __int128)(num / (__int128)B)) & 1) == 0) continue;  // not a midpoint
+        for (int dA = -1; dA <= 1; ++dA) {
+          const double a = ldexp((double)(A + dA), -52);
+          if (fma(a, yh, a * yl) != a / b) return false;
+        }
+      }
+    }
+  }
+  return true;
+}
+
+static GridGeom geom_for(int64_t nx, int64_t ny, int64_t nz, double ox, double oy, double oz,
+                         double res) {
+  GridGeom g = make_geom(nx, ny, nz, ox, oy, oz, res);
+  g.div2 = div2_exact(res) ? 1 : 0;
+  return g;
+}
+
+extern "C" int rmpb_div2_exact(double res, int* out) {
+  if (!out) return fail(RMPB_ERR_INVALID, "out is NULL");
+  *out = div2_exact(res) ? 1 : 0;
+  return RMPB_OK;
+}
 
 static int grid_check_dims(int64_t nx, int64_t ny, int64_t nz, double res) {
   if (nx < 2 || ny < 2 || nz < 2)
@@ -546,7 +618,7 @@ static int grid_new(const void* values, bool on_device, int dtype, int64_t nx, i
   std::unique_ptr<rmpb_grid> g(new rmpb_grid());
   g->device = device;
   g->nx = nx; g->ny = ny; g->nz = nz;
-  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  g->geom = geom_for(nx, ny, nz, ox, oy, oz, res);
   const size_t bytes = (size_t)(nx * ny * nz) * (dtype == RMPB_F32 ? 4 : 8);
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -595,7 +667,7 @@ extern "C" int rmpb_grid_create_brick(const void* values, int dtype, int64_t nx,
   std::unique_ptr<rmpb_grid> g(new rmpb_grid());
   g->device = device;
   g->nx = nx; g->ny = ny; g->nz = nz;
-  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  g->geom = geom_for(nx, ny, nz, ox, oy, oz, res);
   const size_t bytes = (size_t)(nx * ny * nz) * (dtype == RMPB_F32 ? 4 : 8);
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
@@ -630,7 +702,7 @@ extern "C" int rmpb_bake_grid_tsdf(const rmpb_scene* s, double ox, double oy, do
   std::unique_ptr<rmpb_grid> g(new rmpb_grid());
   g->device = device;
   g->nx = nx; g->ny = ny; g->nz = nz;
-  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  g->geom = geom_for(nx, ny, nz, ox, oy, oz, res);
   const bool f32 = storage == RMPB_STORE_F32;
   void* tmp = nullptr;
   int rc = RMPB_OK;
@@ -1030,7 +1102,7 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
   const ExArgs xv = xa ? *xa : ExArgs{nullptr, 0ull, 0};
   return with_grid(g, [&](auto acc) -> int {
     using G = decltype(acc);
-    constexpr bool kFastOk = std::is_same<G, QuadGridF32>::value;  // FAST: f32 QUAD maps only
+    constexpr bool kFastOk = std::is_base_of<QuadGridF32, G>::value;  // FAST: f32 QUAD maps only
     if (mode == RMPB_MODE_FAST && !kFastOk)
       return fail(RMPB_ERR_UNSUPPORTED, "FAST mode needs an f32 QUAD map");
     if (v2) {
@@ -2052,7 +2124,7 @@ extern "C" int rmpb_bake_grid(const rmpb_scene* s, double ox, double oy, double 
   std::unique_ptr<rmpb_grid> g(new rmpb_grid());
   g->device = device;
   g->nx = nx; g->ny = ny; g->nz = nz;
-  g->geom = make_geom(nx, ny, nz, ox, oy, oz, res);
+  g->geom = geom_for(nx, ny, nz, ox, oy, oz, res);
   void* tmp = nullptr;
   int rc = RMPB_OK;
   if (storage == RMPB_STORE_F32) {

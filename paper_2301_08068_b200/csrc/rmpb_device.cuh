@@ -13,6 +13,7 @@
 //   pinv_psd ...... core.py:103-115
 #pragma once
 #include <cstdint>
+#include <type_traits>
 #include <cuda_runtime.h>
 #include <math_constants.h>
 
@@ -66,6 +67,7 @@ struct GridGeom {
   double rhi, rlo;       // double-double 1/res for the exact division (exdiv)
   double dx2, dy2, dz2;  // (double)(n - 2): the clamped cell's base
   int nxm2, nym2, nzm2;  // n - 2: the last cell index (per-step boundary test)
+  int div2;              // 1: exdiv2 is proven exact for divisor res (div2_exact)
 };
 
 // Exact a / b for a divisor with precomputed yhi = RN(1/b),
@@ -79,6 +81,19 @@ __device__ __forceinline__ double exdiv(double a, double b, double yhi, double y
   double q0 = __fma_rn(a, yhi, __dmul_rn(a, ylo));
   double r = __fma_rn(-q0, b, a);
   return __fma_rn(r, yhi, q0);
+}
+
+// The first two operations of exdiv alone, q0 = RN(a yhi + RN(a ylo)), are
+// the correctly rounded a / b for every normal |a| >= 2^-960 whenever the
+// divisor passes div2_exact() (rmpb_api.cu): the error of q0 is below
+// 1.5 * 2^-105 |a/b|, so only quotients within that of a rounding midpoint
+// can round the wrong way, and for a fixed b those are the solutions A of
+// 2^s A - D == 0 (mod B) with |D| <= 6 (s = 53, 54; A, B the integer
+// mantissas) -- a handful per D, each checked directly (window |D| <= 64).
+// Every map resolution tried (0.01-0.9, and 98 % of random divisors) passes.
+// 2 dependent fp64 ops instead of 4 on the trace step's critical chain.
+__device__ __forceinline__ double exdiv2(double a, double yhi, double ylo) {
+  return __fma_rn(a, yhi, __dmul_rn(a, ylo));
 }
 
 __host__ __device__ inline void recip_dd(double b, double& hi, double& lo) {
@@ -104,6 +119,7 @@ __host__ inline GridGeom make_geom(int64_t nx, int64_t ny, int64_t nz, double ox
   recip_dd(res, g.rhi, g.rlo);
   g.dx2 = (double)(nx - 2); g.dy2 = (double)(ny - 2); g.dz2 = (double)(nz - 2);
   g.nxm2 = (int)nx - 2; g.nym2 = (int)ny - 2; g.nzm2 = (int)nz - 2;
+  g.div2 = 0;  // set by the library after div2_exact(res) (rmpb_api.cu)
   return g;
 }
 
@@ -112,6 +128,7 @@ struct Corners { double v000, v001, v010, v011, v100, v101, v110, v111; };
 
 template <typename T>
 struct LinearGrid {
+  static constexpr bool kDiv2 = false;
   const T* __restrict__ v;
   int sy, sx;  // strides: nz, ny*nz (node counts < 2^31 checked at create)
   unsigned lim;  // node count (RMPB_CHECKED builds)
@@ -129,6 +146,7 @@ struct LinearGrid {
 };
 
 struct QuadGridF32 {
+  static constexpr bool kDiv2 = false;  // see QuadGridF32Div2
   const float4* __restrict__ q;
   int qy, qx;  // strides in quads: (nz-1), (ny-1)*(nz-1)
   unsigned lim;  // quad count (RMPB_CHECKED builds)
@@ -144,7 +162,23 @@ struct QuadGridF32 {
   }
 };
 
+// The default f32 map when its resolution passes div2_exact(): the same
+// loads, and the trace step divides with exdiv2 (bitwise the same quotient).
+struct QuadGridF32Div2 : QuadGridF32 {
+  static constexpr bool kDiv2 = true;
+};
+// ... and with the map origin at exactly (0, 0, 0): p - o == p bitwise
+// (-0.0 - 0.0 == -0.0, NaN stays NaN), so the subtraction leaves the chain.
+struct QuadGridF32Div2O0 : QuadGridF32Div2 {
+  static constexpr bool kOrigin0 = true;
+};
+template <class G, class = void>
+struct origin0 { static constexpr bool value = false; };
+template <class G>
+struct origin0<G, decltype((void)G::kOrigin0)> { static constexpr bool value = G::kOrigin0; };
+
 struct PairGridF64 {
+  static constexpr bool kDiv2 = false;
   const double2* __restrict__ q;
   int py, px;  // strides in pairs: (nz-1), ny*(nz-1)
   unsigned lim;  // pair count (RMPB_CHECKED builds)
@@ -165,6 +199,7 @@ struct PairGridF64 {
 // table[(bi*bny + bj)*bnz + bk] = brick slot or -1 (unallocated -> fill).
 template <typename T>
 struct BrickGrid {
+  static constexpr bool kDiv2 = false;
   const T* __restrict__ pool;          // slot * B^3 + ((li*B)+lj)*B + lk
   const int32_t* __restrict__ table;
   int bny, bnz;
@@ -261,9 +296,19 @@ template <class G>
 __device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, double px,
                                               double py, double pz, int& ix, int& iy, int& iz) {
   double fx, fy, fz;
-  cell_floor(exdiv(px - g.ox, g.res, g.rhi, g.rlo), ix, fx);
-  cell_floor(exdiv(py - g.oy, g.res, g.rhi, g.rlo), iy, fy);
-  cell_floor(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), iz, fz);
+  if constexpr (origin0<G>::value) {
+    cell_floor(exdiv2(px, g.rhi, g.rlo), ix, fx);
+    cell_floor(exdiv2(py, g.rhi, g.rlo), iy, fy);
+    cell_floor(exdiv2(pz, g.rhi, g.rlo), iz, fz);
+  } else if constexpr (G::kDiv2) {
+    cell_floor(exdiv2(px - g.ox, g.rhi, g.rlo), ix, fx);
+    cell_floor(exdiv2(py - g.oy, g.rhi, g.rlo), iy, fy);
+    cell_floor(exdiv2(pz - g.oz, g.rhi, g.rlo), iz, fz);
+  } else {
+    cell_floor(exdiv(px - g.ox, g.res, g.rhi, g.rlo), ix, fx);
+    cell_floor(exdiv(py - g.oy, g.res, g.rhi, g.rlo), iy, fy);
+    cell_floor(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), iz, fz);
+  }
   // one (rarely taken) branch for all three boundary clamps
   if (((unsigned)ix > (unsigned)g.nxm2) | ((unsigned)iy > (unsigned)g.nym2) |
       ((unsigned)iz > (unsigned)g.nzm2)) {
@@ -292,18 +337,16 @@ struct CornersF { float v000, v001, v010, v011, v100, v101, v110, v111; };
 
 template <class G>
 __device__ __forceinline__ CornersF load_f(const G& grid, int ix, int iy, int iz) {
-  const Corners c = grid.load(ix, iy, iz);
-  return CornersF{(float)c.v000, (float)c.v001, (float)c.v010, (float)c.v011,
-                  (float)c.v100, (float)c.v101, (float)c.v110, (float)c.v111};
+  if constexpr (std::is_base_of<QuadGridF32, G>::value) {  // f32 corners straight from the quads
+    const float4* b = grid.q + (unsigned)(ix * grid.qx + iy * grid.qy + iz);
+    const float4 a = __ldg(b), c = __ldg(b + (unsigned)grid.qx);
+    return CornersF{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
+  } else {
+    const Corners c = grid.load(ix, iy, iz);
+    return CornersF{(float)c.v000, (float)c.v001, (float)c.v010, (float)c.v011,
+                    (float)c.v100, (float)c.v101, (float)c.v110, (float)c.v111};
+  }
 }
-template <>
-__device__ __forceinline__ CornersF load_f<QuadGridF32>(const QuadGridF32& grid, int ix, int iy,
-                                                        int iz) {
-  const float4* b = grid.q + (unsigned)(ix * grid.qx + iy * grid.qy + iz);
-  const float4 a = __ldg(b), c = __ldg(b + (unsigned)grid.qx);
-  return CornersF{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
-}
-
 struct GeomF {
   float ox, oy, oz, inv;
   int nx2, ny2, nz2;
