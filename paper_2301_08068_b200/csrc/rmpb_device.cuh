@@ -550,11 +550,14 @@ __device__ __forceinline__ void policy_accumulate(Acc& acc, double dx, double dy
   double toward = dx * vx + dy * vy + dz * vz;
   if (!(d < p.radius) || !(toward > 0.0)) return;
   double rx = -dx, ry = -dy, rz = -dz;
-  // divisions by the constant parameters use exdiv (bit-identical to `/`)
-  double frep = p.eta_rep * exp(exdiv(-d, p.nu_rep, p.rnr_h, p.rnr_l));
+  // Divisions by the constant parameters: exdiv2 (within half an ulp + 2^-105
+  // of the quotient, usually the correctly rounded one).  The policy sums are
+  // compared at 1e-9 relative (libm exp / log1p differ by ulps anyway), and
+  // the shorter chain is what bounds a 32-lane policy batch.
+  double frep = p.eta_rep * exp(exdiv2(-d, p.rnr_h, p.rnr_l));
   double g = toward;
-  double fdamp = p.eta_damp / (exdiv(d, p.nu_damp, p.rnd_h, p.rnd_l) + p.eps_p) * g * g;
-  double w = exdiv(d * d, p.rr2, p.rr2_h, p.rr2_l) - exdiv(2.0 * d, p.radius, p.rr_h, p.rr_l) + 1.0;
+  double fdamp = p.eta_damp / (exdiv2(d, p.rnd_h, p.rnd_l) + p.eps_p) * g * g;
+  double w = exdiv2(d * d, p.rr2_h, p.rr2_l) - exdiv2(2.0 * d, p.rr_h, p.rr_l) + 1.0;
   double smag = fdamp / (fdamp + p.c * log1p(exp(-2.0 * p.c * fdamp)));
   double a = w * smag * smag;
   if (a != 0.0) {

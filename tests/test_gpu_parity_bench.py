@@ -299,3 +299,33 @@ def test_server_parks_for_device_sync(be, c1):
         assert time.perf_counter() - t0 < 5.0
         b = srv.policy(states[0])
         assert np.array_equal(a.accel, b.accel) and np.array_equal(a.metric, b.metric)
+
+
+@pytest.mark.parametrize("res,origin", [(0.375, (0.0, 0.0, 0.0)),      # division not proven: 4-op
+                                        (0.1, (-0.0, 0.0, -0.0)),      # -0 origin: 2-op, keeps p - o
+                                        (0.1, (0.3, -1.2, 0.05)),      # 2-op, p - o
+                                        (0.05, (0.0, 0.0, 0.0))])      # 2-op, origin +0 (no p - o)
+def test_quad_division_paths(be, oracle, res, origin):
+    """The three f32 QUAD trace paths (exdiv / exdiv2 / exdiv2 without p - o,
+    chosen per map by rmpb_div2_exact and the origin) are all bit-exact."""
+    rng = np.random.default_rng(int(res * 1000) + 7)
+    nx, ny, nz = 40, 30, 20
+    o = np.array(origin)
+    ii, jj, kk = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    c = np.array([nx, ny, nz]) * 0.5
+    vals = (np.sqrt(((ii - c[0]) * res) ** 2 + ((jj - c[1]) * res) ** 2) - 3.0 * res
+            + 0.02 * rng.standard_normal((nx, ny, nz)))
+    vals = vals.astype(np.float32).astype(np.float64)
+    dirs = _odd_dirs(rng, 3000)
+    center = o + c * res
+    hits = []
+    for start in (center + [0.0, 0.0, 0.1 * res], o + [1.5 * res, 2.5 * res, 1.0 * res],
+                  o - [2.0 * res, 0.0, 0.0]):
+        for kernel in (1, 2):
+            (slot, acc, t, cl, s), (t_r, c_r, s_r) = _trace_both(be, oracle, vals, o, res, start,
+                                                                 dirs, 50.0 * res, kernel)
+            assert np.array_equal(t, t_r), (start, kernel)
+            assert np.array_equal(cl, c_r), (start, kernel)
+            assert np.array_equal(s, s_r), (start, kernel)
+            hits.append(np.isfinite(t).mean())
+    assert max(hits) > 0.1  # the field is actually hit
