@@ -4,7 +4,7 @@ mkdir -p gpurun_out
 for rep in 1 2; do
 for v in "$@"; do
   if [ "$v" = default ]; then lib=""; else lib=$PWD/paper_2301_08068_b200/librmpb_$v.so; fi
-  RMPB_LIBRARY=$lib timeout 300 python scripts/probe_ab.py >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
+  RMPB_LIBRARY=$lib PROBE_REPS=7 timeout 300 python scripts/probe_ab.py >> gpurun_out/ab.jsonl 2>> gpurun_out/ab.err
 done
 done
 echo DONE
