@@ -9,5 +9,8 @@ $CMD > gpurun_out/plain.log 2>&1 && timeout 900 ncu --metrics gpu__time_duration
 python scripts/profile_target.py > gpurun_out/pt_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_ray_policy2 -s 1 -c 1 -f -o gpurun_out/prof_full python scripts/profile_target.py > gpurun_out/ncu_full.log 2>&1
 python scripts/profile_lidar.py > gpurun_out/pl_plain.log 2>&1 && timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_lidar_warp -s 1 -c 1 -f -o gpurun_out/prof_lidar python scripts/profile_lidar.py > gpurun_out/ncu_lidar.log 2>&1
 ncu -i gpurun_out/prof_full.ncu-rep --page source --csv --print-source sass > gpurun_out/prof_full_sass.csv 2>/dev/null; gzip -f gpurun_out/prof_full_sass.csv
+NCU_SUMMARY_DIR=gpurun_out python scripts/ncu_summary.py gpurun_out/prof_full.ncu-rep 02 > /dev/null 2>&1
+NCU_SUMMARY_DIR=gpurun_out python scripts/ncu_summary.py gpurun_out/prof_lidar.ncu-rep 02 lidar > /dev/null 2>&1
+rm -f gpurun_out/*.ncu-rep  # (64 MiB copy-back limit)
 ls -la gpurun_out > gpurun_out/ls.txt
 echo DONE

@@ -1,6 +1,7 @@
 """Summarise one `ncu --set full` capture of the hot kernel into profiles/.
 
     python scripts/ncu_summary.py gpurun_out/prof_full.ncu-rep [round] [tag]
+    (NCU_SUMMARY_DIR=gpurun_out: write there instead of profiles/, on the box)
 
 Writes profiles/r<round>_ncu_summary.json (the numbers bench.py quotes:
 DRAM bytes per launch, L2 read GB/s, pipe utilisations) and the raw/details
@@ -11,6 +12,7 @@ and r<round>_ncu_full_<tag>_{raw,details}.csv.
 import csv
 import io
 import json
+import os
 import subprocess
 import sys
 
@@ -67,8 +69,10 @@ def main():
     out["dram_bytes_per_launch"] = out["dram_bytes_read"] + out["dram_bytes_write"]
     out["l2_read_GBps"] = out["l2_read_sectors_from_l1"] * 32 / (out["duration_ms"] * 1e-3) / 1e9
     out["dram_GBps"] = out["dram_bytes_per_launch"] / (out["duration_ms"] * 1e-3) / 1e9
-    summ = f"profiles/r{rnd}_ncu_{tag}_summary.json" if tag else f"profiles/r{rnd}_ncu_summary.json"
-    stem = f"profiles/r{rnd}_ncu_full_{tag or 'k_ray_policy2'}"
+    outdir = os.environ.get("NCU_SUMMARY_DIR", "profiles")
+    summ = (f"{outdir}/r{rnd}_ncu_{tag}_summary.json" if tag
+            else f"{outdir}/r{rnd}_ncu_summary.json")
+    stem = f"{outdir}/r{rnd}_ncu_full_{tag or 'k_ray_policy2'}"
     with open(summ, "w") as fh:
         json.dump(out, fh, indent=1)
         fh.write("\n")
