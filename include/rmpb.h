@@ -114,7 +114,9 @@ RMPB_EXPORT int rmpb_grid_create_device(const void* d_values, int dtype, int64_t
 RMPB_EXPORT int rmpb_grid_create_brick(const void* values, int dtype, int64_t nx, int64_t ny, int64_t nz,
                            double ox, double oy, double oz, double res, double fill,
                            int storage, int device, rmpb_grid** out);
-/* Re-upload values into an existing grid (same shape); invalidates caches. */
+/* Re-upload all values into an existing grid (same shape), in place: every
+ * holder of the handle sees the new map (a QUAD grid whose new values are
+ * not f32-exact switches to the f64 layout; a BRICK grid is unsupported). */
 RMPB_EXPORT int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype);
 /* Overwrite the node sub-box [i0, i0+ni) x [j0, j0+nj) x [k0, k0+nk) of an
  * existing LINEAR / QUAD / PAIR64 grid with `values` (f64, C-order, ni*nj*nk)

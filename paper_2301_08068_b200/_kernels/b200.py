@@ -126,6 +126,11 @@ class DeviceGrid:
                 L.call("rmpb_grid_create_brick", v.ctypes.data, dt, *self.dims, o[0], o[1], o[2],
                        self.res, float(brick_fill), int(storage), self.device, ctypes.byref(h))
         self.handle = h
+        self.refresh_info()
+
+    def refresh_info(self) -> None:
+        """Storage / layout / sizes from the handle (they change when a map
+        update has to switch the layout)."""
         st, lay, nb, nbr = ctypes.c_int(), ctypes.c_int(), ctypes.c_int64(), ctypes.c_int64()
         L.call("rmpb_grid_info", self.handle, ctypes.byref(st), ctypes.byref(lay),
                ctypes.byref(nb), ctypes.byref(nbr))
@@ -416,9 +421,10 @@ def grid_updated(values: np.ndarray, corner, sub: np.ndarray) -> None:
     """EsdfGrid.update hook: ``values[corner : corner + sub.shape] = sub`` has
     just been written on the host.  Every cached device copy of ``values`` is
     patched in place (only the touched nodes cross PCIe; QUAD / LINEAR /
-    PAIR64 layouts); a copy that cannot take the patch (a BRICK map, or f32
-    storage and values that are not f32-exact) is dropped and re-uploaded on
-    its next use."""
+    PAIR64 layouts).  A copy that cannot take the patch (f32 storage and
+    values that are not f32-exact) is re-uploaded whole into the SAME handle
+    (rmpb_grid_update: holders such as a LatencyServer see the new map); one
+    that cannot be updated at all is dropped from the cache."""
     sub = np.ascontiguousarray(sub, dtype=np.float64)
     i0, j0, k0 = (int(c) for c in corner)
     ni, nj, nk = sub.shape
@@ -435,8 +441,14 @@ def grid_updated(values: np.ndarray, corner, sub: np.ndarray) -> None:
         for kind, k, g in targets:
             ok = done.get(id(g))
             if ok is None:
-                st = L.load().rmpb_grid_update_region(g.handle, sub.ctypes.data, L.RMPB_F64,
-                                                      i0, j0, k0, ni, nj, nk)
+                lib = L.load()
+                st = lib.rmpb_grid_update_region(g.handle, sub.ctypes.data, L.RMPB_F64,
+                                                 i0, j0, k0, ni, nj, nk)
+                if st != 0:  # whole re-upload into the same handle
+                    full = np.ascontiguousarray(values, dtype=np.float64)
+                    st = lib.rmpb_grid_update(g.handle, full.ctypes.data, L.RMPB_F64)
+                    if st == 0:
+                        g.refresh_info()
                 ok = done[id(g)] = st == 0
             if not ok:
                 (_fast if kind == "fast" else _grids).pop(k, None)

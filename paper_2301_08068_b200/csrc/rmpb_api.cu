@@ -759,12 +759,17 @@ extern "C" int rmpb_grid_update(rmpb_grid* g, const void* values, int dtype) {
   if (g->layout == LAYOUT_BRICK)
     return fail(RMPB_ERR_UNSUPPORTED, "update of a BRICK grid: recreate it");
   rmpb_grid* fresh = nullptr;
-  TRY(grid_new(values, false, dtype, g->nx, g->ny, g->nz, g->geom.ox, g->geom.oy, g->geom.oz,
-               g->geom.res, RMPB_STORE_AUTO, g->layout, g->device, &fresh));
+  int rc = grid_new(values, false, dtype, g->nx, g->ny, g->nz, g->geom.ox, g->geom.oy, g->geom.oz,
+                    g->geom.res, RMPB_STORE_AUTO, g->layout, g->device, &fresh);
+  if (rc == RMPB_ERR_UNSUPPORTED && g->layout == LAYOUT_QUAD)  // values no longer f32-exact
+    rc = grid_new(values, false, dtype, g->nx, g->ny, g->nz, g->geom.ox, g->geom.oy, g->geom.oz,
+                  g->geom.res, RMPB_STORE_AUTO, RMPB_LAYOUT_AUTO, g->device, &fresh);
+  if (rc != RMPB_OK) return rc;
   DeviceGuard dg(g->device);
-  rfree(g->d_values);
+  rfree(g->d_values);  // parks latency servers first; they relaunch on the new arrays
   g->d_values = fresh->d_values;
   g->storage = fresh->storage;
+  g->layout = fresh->layout;
   g->bytes = fresh->bytes;
   fresh->d_values = nullptr;
   delete fresh;

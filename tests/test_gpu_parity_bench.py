@@ -329,3 +329,34 @@ def test_quad_division_paths(be, oracle, res, origin):
             assert np.array_equal(s, s_r), (start, kernel)
             hits.append(np.isfinite(t).mean())
     assert max(hits) > 0.1  # the field is actually hit
+
+
+def test_map_update_reaches_latency_server(be, oracle):
+    """EsdfGrid.update on a map a LatencyServer is serving: a region patch
+    (f32-exact values) and a whole re-upload into the same handle (values
+    that are not f32-exact: the QUAD f32 copy switches to the f64 layout)
+    both reach the resident kernel; its next answer equals the oracle on the
+    edited map."""
+    import paper_2301_08068_b200 as P
+    from paper_2301_08068_b200 import synth
+
+    scene = synth.c1_scene(n_boxes=20, hi=np.array([5.9, 5.9, 2.9]))
+    vals = be.bake_values(scene.packed(), np.zeros(3), 0.1, (60, 60, 30))
+    vals = vals.astype(np.float32).astype(np.float64)
+    grid = P.EsdfGrid(np.zeros(3), 0.1, (60, 60, 30), vals)
+    dirs = oracle.sample_directions(4096)
+    bundle = P.RayBundle(dirs)
+    params = P.preset("static_map").obstacle
+    st = synth.bench_states(scene, count=1, seed=9, distance=synth.host_box_distance(scene))[0]
+    i, j, k = (int(c) for c in np.floor(st.position / 0.1))
+    with P.LatencyServer(grid, bundle, params, 10.0, idle_timeout_s=30.0) as srv:
+        for edit in ((slice(i + 1, i + 3), slice(j, j + 2), slice(k, k + 2), -0.5),
+                     ((i, j + 1, k), 0.1234567890123)):
+            srv.policy(st)
+            grid.update(tuple(edit[:-1]) if len(edit) == 4 else edit[0], edit[-1])
+            pol = srv.policy(st)
+            ref = oracle.ray_policy(grid.values, grid.origin, 0.1, st.position, st.velocity,
+                                    dirs, params.as_tuple(), 10.0)
+            assert pol.metric.ravel().tolist() != [0.0] * 9
+            assert rel_err(pol.metric.ravel(), ref[0][:9]) <= SUM_TOL
+            assert rel_err(pol.accel, ref[1]) <= ACC_TOL
