@@ -15,6 +15,7 @@ LIDAR = (1.2, 1.5, 3.0, 1.0, 1e-6, 1.3, 1.0)
 
 def pytest_configure(config):
     config.addinivalue_line("markers", "gpu: needs a CUDA device (B200); run with -m gpu")
+    config.addinivalue_line("markers", "gpu2: needs two CUDA devices (NVLink peers); -m gpu2")
 
 
 @pytest.fixture(scope="session")
