@@ -248,7 +248,7 @@ static int with_grid(const rmpb_grid* g, F&& f) {
     return f(a);
   }
   if (g->layout == LAYOUT_QUAD) {  // f32 storage only (grid_build)
-    QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, (G.ny - 1) * (G.nz - 1),
+    QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, G.nx,
                   (unsigned)(g->nx * (g->ny - 1) * (g->nz - 1))};
     const bool o0 = G.ox == 0.0 && G.oy == 0.0 && G.oz == 0.0 && !std::signbit(G.ox) &&
                     !std::signbit(G.oy) && !std::signbit(G.oz);  // +0.0 only: p - (+0) == p

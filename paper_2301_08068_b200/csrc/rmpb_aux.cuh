@@ -144,17 +144,18 @@ __global__ void k_check_f32(long long n, const double* __restrict__ src, int* __
   if (__any_sync(0xffffffffu, b) && (threadIdx.x & 31) == 0) atomicOr(bad, 1);
 }
 
-// QUAD layout builder: quad[(i*(ny-1)+j)*(nz-1)+k] = {v[i,j,k], v[i,j,k+1], v[i,j+1,k], v[i,j+1,k+1]}.
+// QUAD layout builder: quad[(j*(nz-1)+k)*nx+i] = {v[i,j,k], v[i,j,k+1], v[i,j+1,k], v[i,j+1,k+1]}
+// (x fastest: a trace step's two x-planes are adjacent records).
 template <typename T, typename Q>
 __global__ void k_build_quad(int nx, int ny, int nz, const T* __restrict__ v, Q* __restrict__ q) {
   long long n = (long long)nx * (ny - 1) * (nz - 1);
   long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   long long stride = (long long)gridDim.x * blockDim.x;
   for (; i < n; i += stride) {
-    int k = (int)(i % (nz - 1));
-    long long r = i / (nz - 1);
-    int j = (int)(r % (ny - 1));
-    int ii = (int)(r / (ny - 1));
+    int ii = (int)(i % nx);
+    long long r = i / nx;
+    int k = (int)(r % (nz - 1));
+    int j = (int)(r / (nz - 1));
     const T* b = v + ((long long)ii * ny + j) * nz + k;
     T* o = reinterpret_cast<T*>(q) + 4 * i;
     o[0] = b[0]; o[1] = b[1]; o[2] = b[nz]; o[3] = b[nz + 1];
@@ -196,7 +197,7 @@ __global__ void k_patch_nodes(int layout, int nx, int ny, int nz, int i0, int j0
       reinterpret_cast<T*>(dst)[((long long)i * ny + j) * nz + k] = (T)v;
     } else if (layout == 1) {  // QUAD: {v[i,j,k], v[i,j,k+1], v[i,j+1,k], v[i,j+1,k+1]}
       T* q = reinterpret_cast<T*>(dst);
-      auto rec = [&](int jj, int kk) { return 4 * (((long long)i * (ny - 1) + jj) * (nz - 1) + kk); };
+      auto rec = [&](int jj, int kk) { return 4 * (((long long)jj * (nz - 1) + kk) * nx + i); };
       if (j <= ny - 2 && k <= nz - 2) q[rec(j, k) + 0] = (T)v;
       if (j <= ny - 2 && k >= 1) q[rec(j, k - 1) + 1] = (T)v;
       if (j >= 1 && k <= nz - 2) q[rec(j - 1, k) + 2] = (T)v;

@@ -148,16 +148,24 @@ struct LinearGrid {
   }
 };
 
+// QUAD: f32 quads {v[i,j,k], v[i,j,k+1], v[i,j+1,k], v[i,j+1,k+1]} stored
+// x-fastest, index (iy*(nz-1) + iz)*nx + ix, so the two x-planes a step
+// reads are adjacent 16 B records (one 32 B sector when ix is even).  The
+// z-fastest order ((ix*(ny-1) + iy)*(nz-1) + iz) measured 12.40-12.58 ms on
+// the bench workload vs 12.19-12.22 ms for this one (profiles/README.md).
 struct QuadGridF32 {
   static constexpr bool kDiv2 = false;  // see QuadGridF32Div2
   const float4* __restrict__ q;
-  int qy, qx;  // strides in quads: (nz-1), (ny-1)*(nz-1)
+  int qy, qx;    // qy = nz-1, qx = nx (quads per x row)
   unsigned lim;  // quad count (RMPB_CHECKED builds)
+  __device__ __forceinline__ unsigned idx(int ix, int iy, int iz) const {
+    return (unsigned)((iy * qy + iz) * qx + ix);
+  }
+  __device__ __forceinline__ unsigned xstep() const { return 1u; }
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && iy < qx / qy && iz < qy &&
-               (unsigned)(ix * qx + iy * qy + iz) + (unsigned)qx < lim);
-    const float4* b = q + (unsigned)(ix * qx + iy * qy + iz);
-    float4 a = __ldg(b), c = __ldg(b + (unsigned)qx);
+    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && iz < qy && idx(ix, iy, iz) + xstep() < lim);
+    const float4* b = q + idx(ix, iy, iz);
+    float4 a = __ldg(b), c = __ldg(b + xstep());
     Corners k;
     k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
     k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;
@@ -360,8 +368,8 @@ struct CornersF { float v000, v001, v010, v011, v100, v101, v110, v111; };
 template <class G>
 __device__ __forceinline__ CornersF load_f(const G& grid, int ix, int iy, int iz) {
   if constexpr (std::is_base_of<QuadGridF32, G>::value) {  // f32 corners straight from the quads
-    const float4* b = grid.q + (unsigned)(ix * grid.qx + iy * grid.qy + iz);
-    const float4 a = __ldg(b), c = __ldg(b + (unsigned)grid.qx);
+    const float4* b = grid.q + grid.idx(ix, iy, iz);
+    const float4 a = __ldg(b), c = __ldg(b + grid.xstep());
     return CornersF{a.x, a.y, a.z, a.w, c.x, c.y, c.z, c.w};
   } else {
     const Corners c = grid.load(ix, iy, iz);
