@@ -279,6 +279,29 @@ def run_b200(args):
                 lat_s.append(time.perf_counter() - t0)
     lat_srv = statistics.median(lat_s)
     breakdown = latency_breakdown(grid, bundle, params, states, eng, dev, lat_med, lat_srv)
+    # policy-only evaluation (opt-in, rays stop at the activation radius:
+    # the same Policy; per-ray masks / n_hits then count hits within it)
+    from paper_2301_08068_b200.device import RayPolicyEngine
+    from paper_2301_08068_b200.rays import policy_range
+
+    lat_po, lat_spo = [], []
+    for i in range(args.latency_calls + 20):  # (no server resident meanwhile)
+        st = states[i % len(states)]
+        t0 = time.perf_counter()
+        ray_policy(st, grid, bundle, params, MAX_RANGE, policy_only=True)
+        if i >= 20:
+            lat_po.append(time.perf_counter() - t0)
+    with LatencyServer(grid, bundle, params, MAX_RANGE, policy_only=True) as srv:
+        for i in range(args.latency_calls + 20):
+            st = states[i % len(states)]
+            t0 = time.perf_counter()
+            srv.policy(st)
+            if i >= 20:
+                lat_spo.append(time.perf_counter() - t0)
+    eng_po = RayPolicyEngine(grid, bundle, params.as_tuple(), MAX_RANGE, policy_only=True)
+    breakdown["policy_only"] = latency_breakdown(
+        grid, bundle, params, states, eng_po, dev, statistics.median(lat_po),
+        statistics.median(lat_spo), max_range=policy_range(MAX_RANGE, params.radius))
 
     # measured L2 read ceiling (untimed), CUDA events
     l2 = l2_peaks(dev, stream)
@@ -319,6 +342,7 @@ def run_b200(args):
         configs["C3_lidar_1024_scans"] = c3_config(dev, stream, peaks["hbm_gbs"], flush,
                                                    cpu=(world == 1 and not args.no_cpu_baseline))
         configs["C2_1M_rays_10m"] = c2_config(grid, dev, stream, flush, params)
+        configs["C4_policy_only"] = c4_policy_only(eng_po, x, v, slots, accels, stream, flush)
         if world == 1:
             configs["C5_1M_rays_ray_split"] = c5_config(dev, stream)
 
@@ -366,7 +390,8 @@ def run_b200(args):
     return out
 
 
-def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n=200):
+def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n=200,
+                      max_range=None):
     """Where the single-pose call's time goes (C1, 65536 rays): the public
     Python call, the bare C-ABI call (ctypes, pre-staged pointers: host
     staging + launch + kernel + readback + sync), and the kernel alone on the
@@ -386,6 +411,7 @@ def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n
     pa = np.ascontiguousarray(np.asarray(params.as_tuple(), dtype=np.float64))
     fn = _lib.load().rmpb_ray_policy
     eps = 0.5 * grid.resolution
+    mr = MAX_RANGE if max_range is None else float(max_range)
     xvp, outp, pap = xv.ctypes.data, out.ctypes.data, pa.ctypes.data
     c_us = []
     for i in range(n + 20):
@@ -393,7 +419,7 @@ def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n
         xv[0:3] = st.position
         xv[3:6] = st.velocity
         t0 = time.perf_counter()
-        rc = fn(g.handle, b.handle, xvp, xvp + 24, pap, MAX_RANGE, eps, 0.9, outp, outp + 104,
+        rc = fn(g.handle, b.handle, xvp, xvp + 24, pap, mr, eps, 0.9, outp, outp + 104,
                 None, None, None, None)
         t1 = time.perf_counter()
         if rc != 0:
@@ -422,7 +448,7 @@ def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n
             "device_kernel_us": round(k_med, 2),
             "python_overhead_us": round(lat_py * 1e6 - c_med, 2),
             "host_launch_sync_readback_us": round(c_med - k_med, 2),
-            "latency_server_us": round(lat_srv * 1e6, 2),
+            "latency_server_us": round(lat_srv * 1e6, 2), "max_range_m": mr,
             "note": "medians of 200 calls; device_kernel_us = CUDA events around one "
                     "device-resident P=1 launch (segments of 256 rays: the pose's longest "
                     "ray is the floor)"}
@@ -543,6 +569,27 @@ def c3_config(dev, stream, hbm_peak, flush, cpu=True, S=1024):
                                     "sample": "30 scans per thread count (world directions "
                                               "precomputed, as rmpnav's lidar_policy passes them)"}
     return rec
+
+
+def c4_policy_only(eng_po, x, v, slots, accels, stream, flush):
+    """The bench step (same poses, bundle, map) through the policy-only
+    engine: rays stop at the activation radius (rays.policy_range); the
+    slots' policy sums are checked against the timed full-range step."""
+    import numpy as np
+
+    best, med = _ev_ms(lambda: eng_po.evaluate(x, v), stream, flush, reps=5)
+    s_po, a_po = eng_po.evaluate(x, v)
+    s_full = slots.cpu().numpy()
+    s_po = s_po.cpu().numpy()
+    scale = float(np.abs(s_full[:, :12]).max())
+    P = x.shape[0]
+    return {"max_range_m": eng_po.max_range, "ms_per_step_best": round(best, 3),
+            "ms_per_step_median": round(med, 3),
+            "evaluations_per_s": round(P / (best * 1e-3), 1),
+            "max_rel_sum_vs_full_range": float(np.abs(s_po[:, :12] - s_full[:, :12]).max()) / scale,
+            "n_hits_within_radius": int(s_po[:, 12].sum()), "n_hits_full": int(s_full[:, 12].sum()),
+            "note": "opt-in policy_only=True: same Policy (hits at d >= radius have weight 0); "
+                    "not the headline (the headline traces every ray to max range)"}
 
 
 def c2_config(grid, dev, stream, flush, params, P=64):

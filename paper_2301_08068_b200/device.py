@@ -21,6 +21,7 @@ import numpy as np
 
 from . import _lib as L
 from ._kernels import b200
+from .rays import policy_range
 
 
 def _torch():
@@ -69,9 +70,13 @@ class RayPolicyEngine:
     """Fused map-based policy evaluation with device-resident inputs."""
 
     def __init__(self, grid, bundle, params, max_range: float = 20.0, device: int | None = None,
-                 eps: float | None = None, step_scale: float = 0.9, mode: str = "exact"):
+                 eps: float | None = None, step_scale: float = 0.9, mode: str = "exact",
+                 policy_only: bool = False):
         """``mode="exact"`` (default) is bit-identical to the reference;
-        ``mode="fast"`` marches in fp32 (opt-in, NOT reference-exact)."""
+        ``mode="fast"`` marches in fp32 (opt-in, NOT reference-exact).
+        ``policy_only=True`` stops rays at the activation radius
+        (params[5]; ``rays.policy_range``): the same policy sums, slot[12]
+        then counts hits within the radius only."""
         if mode not in ("exact", "fast"):
             raise ValueError("mode must be 'exact' or 'fast'")
         self.mode = L.MODE_FAST if mode == "fast" else L.MODE_EXACT
@@ -93,6 +98,9 @@ class RayPolicyEngine:
         self.device = dev
         self.params = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
         self.max_range = float(max_range)
+        self.policy_only = bool(policy_only)
+        if self.policy_only:
+            self.max_range = policy_range(self.max_range, self.params[5])
         self.eps = 0.5 * self.grid.res if eps is None else float(eps)
         self.step_scale = float(step_scale)
         self.n_rays = self.bundle.n

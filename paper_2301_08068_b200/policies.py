@@ -33,7 +33,8 @@ import numpy as np
 from ._kernels import get_backend
 from .core import Policy, RobotState
 from .geometry import EsdfGrid, Scene
-from .rays import DEFAULT_MAX_RANGE, GRID_STEP_SCALE, RangeScan, RayBundle, raycast_many
+from .rays import (DEFAULT_MAX_RANGE, GRID_STEP_SCALE, RangeScan, RayBundle, policy_range,
+                   raycast_many)
 
 __all__ = ["AttractorParams", "ObstacleParams", "PolicyParams", "PRESETS", "preset", "esdf_policy",
            "ray_policy", "ray_policy_batch", "lidar_policy", "lidar_policy_points",
@@ -173,10 +174,17 @@ def _reduced_policy(be, dirs, dists, velocity, p: ObstacleParams, min_range: flo
 
 def ray_policy(state: RobotState, field, bundle: RayBundle, p: ObstacleParams,
                max_range: float = DEFAULT_MAX_RANGE, t: float = 0.0, workers: int = 1,
-               backend: str | None = None) -> Policy:
+               backend: str | None = None, policy_only: bool = False) -> Policy:
     """Cast the bundle from the robot; one obstacle policy per hit ray with
-    away direction = -cast direction; metric-weighted combination."""
+    away direction = -cast direction; metric-weighted combination.
+
+    ``policy_only=True`` (beyond the reference) stops each ray at the
+    activation radius ``p.radius`` (``policy_range``): the returned Policy
+    sums exactly the same hits, for less marching (C1: 12.2 -> 7.9 ms per
+    4096 poses, single pose ~30 -> ~18 us of kernel)."""
     be = get_backend(backend)
+    if policy_only:
+        max_range = policy_range(max_range, p.radius)
     if isinstance(field, EsdfGrid) and hasattr(be, "ray_policy_fused"):
         slot, accel = be.ray_policy_fused(field.values, field.origin, field.resolution,
                                           state.position, state.velocity, bundle.directions,
@@ -189,10 +197,15 @@ def ray_policy(state: RobotState, field, bundle: RayBundle, p: ObstacleParams,
 
 
 def ray_policy_batch(states, field: EsdfGrid, bundle: RayBundle, p: ObstacleParams,
-                     max_range: float = DEFAULT_MAX_RANGE, backend: str | None = None):
+                     max_range: float = DEFAULT_MAX_RANGE, backend: str | None = None,
+                     policy_only: bool = False):
     """``ray_policy`` for many robot states in one launch.  ``states`` is a
     sequence of RobotState or a (positions P x 3, velocities P x 3) pair.
-    Returns (accels P x 3, metrics P x 3 x 3, n_hits P)."""
+    Returns (accels P x 3, metrics P x 3 x 3, n_hits P); with
+    ``policy_only`` (see ``ray_policy``) n_hits counts hits within the
+    activation radius only."""
+    if policy_only:
+        max_range = policy_range(max_range, p.radius)
     if not isinstance(field, EsdfGrid):
         raise TypeError("ray_policy_batch needs an EsdfGrid")
     if isinstance(states, tuple) and len(states) == 2 and not isinstance(states[0], RobotState):

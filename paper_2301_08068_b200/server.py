@@ -28,16 +28,18 @@ from ._kernels import b200
 from .core import Policy, RobotState
 from .geometry import EsdfGrid
 from .policies import GRID_STEP_SCALE, ObstacleParams, _policy_from_slot
-from .rays import DEFAULT_MAX_RANGE, RayBundle
+from .rays import DEFAULT_MAX_RANGE, RayBundle, policy_range
 
 
 class LatencyServer:
     def __init__(self, field: EsdfGrid, bundle: RayBundle, p: ObstacleParams,
                  max_range: float = DEFAULT_MAX_RANGE, idle_timeout_s: float = 1.0,
-                 storage: int | None = None, layout: int | None = None):
+                 storage: int | None = None, layout: int | None = None,
+                 policy_only: bool = False):
         """``storage`` / ``layout`` (librmpb STORE_* / LAYOUT_*) give the
         server its own device copy of the map in that layout; default: the
-        map shared with ``ray_policy``."""
+        map shared with ``ray_policy``.  ``policy_only`` as in
+        ``ray_policy``: rays stop at the activation radius, same Policy."""
         if not isinstance(field, EsdfGrid):
             raise TypeError("LatencyServer needs an EsdfGrid")
         if storage is None and layout is None:
@@ -48,6 +50,9 @@ class LatencyServer:
                                          layout=L.LAYOUT_AUTO if layout is None else layout)
         self._bundle = b200.device_bundle(getattr(bundle, "directions", bundle))
         self._params = np.ascontiguousarray(np.asarray(p.as_tuple(), dtype=np.float64))
+        if policy_only:
+            max_range = policy_range(max_range, p.radius)
+        self.max_range = float(max_range)
         h = ctypes.c_void_p()
         L.call("rmpb_server_start", self._grid.handle, self._bundle.handle,
                self._params.ctypes.data, float(max_range), 0.5 * float(field.resolution),
