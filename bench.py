@@ -441,6 +441,15 @@ def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n
         e1.synchronize()
         if i >= 20:
             k_us.append(e0.elapsed_time(e1) * 1e3)
+    # the platform floor: one empty-ish kernel launch + stream sync (host clock)
+    z = torch.zeros(1, device=dev)
+    f_us = []
+    for i in range(n + 20):
+        t0 = time.perf_counter()
+        z.fill_(1.0)
+        torch.cuda.current_stream().synchronize()
+        if i >= 20:
+            f_us.append((time.perf_counter() - t0) * 1e6)
     c_med = statistics.median(c_us)
     k_med = statistics.median(k_us)
     return {"python_ray_policy_us": round(lat_py * 1e6, 2),
@@ -449,6 +458,7 @@ def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n
             "python_overhead_us": round(lat_py * 1e6 - c_med, 2),
             "host_launch_sync_readback_us": round(c_med - k_med, 2),
             "latency_server_us": round(lat_srv * 1e6, 2), "max_range_m": mr,
+            "empty_kernel_launch_sync_us": round(statistics.median(f_us), 2),
             "note": "medians of 200 calls; device_kernel_us = CUDA events around one "
                     "device-resident P=1 launch (segments of 256 rays: the pose's longest "
                     "ray is the floor)"}

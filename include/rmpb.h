@@ -154,7 +154,12 @@ RMPB_EXPORT int rmpb_bundle_destroy(rmpb_bundle* b);
 /* ray_policy (policies.py:182-192): trace + per-ray policy + reduce + pinv in
  * one launch.  eps / step_scale as rays.py:117-120 (0.5*res, 0.9).  Optional
  * per-ray outputs in ORIGINAL ray order: t (+inf = miss), hit cell (3 int32,
- * -1 on miss), interpolation steps. */
+ * -1 on miss), interpolation steps.
+ * Policy-only callers (who use the slot's sums / the acceleration, not the
+ * per-ray outputs or slot[12]) may pass max_range = min(max_range, radius),
+ * radius = params[5]: a hit at d >= radius has activation weight 0
+ * (_ckern.pyx:300-306), so the sums are those of the full range while every
+ * ray stops at the radius (Python: policy_only=True, rays.policy_range). */
 RMPB_EXPORT int rmpb_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, const double x[3], const double v[3],
                     const double params[7], double max_range, double eps, double step_scale,
                     double out_slot[13], double out_accel[3],

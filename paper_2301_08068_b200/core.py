@@ -50,8 +50,9 @@ class Policy:
         (3,) accel and a finite, exactly symmetric (3, 3) metric (what
         __post_init__ would produce unchanged)."""
         p = object.__new__(cls)
-        object.__setattr__(p, "accel", accel)
-        object.__setattr__(p, "metric", metric)
+        d = p.__dict__  # (frozen dataclass: bypass __setattr__)
+        d["accel"] = accel
+        d["metric"] = metric
         return p
 
     def is_psd(self, tol: float = _PSD_TOL) -> bool:

@@ -154,13 +154,12 @@ def _policy_from_slot(slot, accel) -> Policy:
     check-only path (~2 us instead of ~15 us of small NumPy ops); anything
     else goes through Policy's own construction (and its ValueError)."""
     if type(slot) is np.ndarray and type(accel) is np.ndarray and slot.dtype == np.float64 \
-            and accel.dtype == np.float64:
-        m = slot[0:9]
-        lm = m.tolist()
-        la = accel.tolist()
-        if (len(lm) == 9 and len(la) == 3 and lm[1] == lm[3] and lm[2] == lm[6] and lm[5] == lm[7]
-                and all(abs(x) < _SYM_SAFE for x in lm) and all(abs(x) < math.inf for x in la)):
-            return Policy._trusted(accel, m.reshape(3, 3))
+            and accel.dtype == np.float64 and slot.ndim == 1 and accel.shape == (3,):
+        lm = slot.tolist()
+        # sum(|x|) < bound: every |x| below it, and NaN / inf fail the test
+        if (len(lm) >= 9 and lm[1] == lm[3] and lm[2] == lm[6] and lm[5] == lm[7]
+                and sum(map(abs, lm[:9])) < _SYM_SAFE and sum(map(abs, accel.tolist())) < math.inf):
+            return Policy._trusted(accel, slot[0:9].reshape(3, 3))
     return Policy(np.asarray(accel, dtype=float), np.asarray(slot[0:9], dtype=float).reshape(3, 3))
 
 

@@ -58,9 +58,11 @@ int main() {
   double r10 = med([&](int i) { call(i, 10.0, nullptr); });
   double r0s = med([&](int i) { call(i, 1e-6, s); });
   double r10s = med([&](int i) { call(i, 10.0, s); });
+  double r24 = med([&](int i) { call(i, 2.4, nullptr); });  // policy-only range (radius)
   printf("{\"flag_spin_us\": %.2f, \"query_spin_us\": %.2f, \"launch_only_us\": %.2f, ", e2, e3, e4);
   printf("{\"empty_1x32_us\": %.2f, \"empty_256x256_us\": %.2f, \"abi_range0_us\": %.2f, "
-         "\"abi_range10_us\": %.2f, \"abi_range0_stream_us\": %.2f, \"abi_range10_stream_us\": %.2f}\n",
-         e0, e1, r0, r10, r0s, r10s);
+         "\"abi_range10_us\": %.2f, \"abi_range0_stream_us\": %.2f, \"abi_range10_stream_us\": %.2f, "
+         "\"abi_range2.4_us\": %.2f}\n",
+         e0, e1, r0, r10, r0s, r10s, r24);
   return 0;
 }
