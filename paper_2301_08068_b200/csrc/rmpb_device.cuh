@@ -302,11 +302,12 @@ __device__ __forceinline__ void cell_fix(int nm2, int& i, double& f) {
   }
 }
 
-// interp with exdiv + cell_floor / cell_fix: bit-identical to interp() above.
+// Cell of a point (the reference's clamp + floor + fraction, before the
+// boundary fix): exdiv2 / origin-0 forms per accessor type.
 template <class G>
-__device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, double px,
-                                              double py, double pz, int& ix, int& iy, int& iz) {
-  double fx, fy, fz;
+__device__ __forceinline__ void locate(const GridGeom& g, double px, double py, double pz,
+                                       int& ix, int& iy, int& iz, double& fx, double& fy,
+                                       double& fz) {
   if constexpr (origin0<G>::value) {
     cell_floor(exdiv2(px, g.rhi, g.rlo), ix, fx);
     cell_floor(exdiv2(py, g.rhi, g.rlo), iy, fy);
@@ -320,14 +321,35 @@ __device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, 
     cell_floor(exdiv(py - g.oy, g.res, g.rhi, g.rlo), iy, fy);
     cell_floor(exdiv(pz - g.oz, g.res, g.rhi, g.rlo), iz, fz);
   }
+}
+__device__ __forceinline__ bool out_of_cells(const GridGeom& g, int ix, int iy, int iz) {
+  return ((unsigned)ix > (unsigned)g.nxm2) | ((unsigned)iy > (unsigned)g.nym2) |
+         ((unsigned)iz > (unsigned)g.nzm2);
+}
+// The reference's trilinear interpolation order (_ckern.pyx:126-135).
+__device__ __forceinline__ double lerp8(const Corners& c, double fx, double fy, double fz) {
+  double c00 = c.v000 + fz * (c.v001 - c.v000);
+  double c01 = c.v010 + fz * (c.v011 - c.v010);
+  double c10 = c.v100 + fz * (c.v101 - c.v100);
+  double c11 = c.v110 + fz * (c.v111 - c.v110);
+  double c0 = c00 + fy * (c01 - c00);
+  double c1 = c10 + fy * (c11 - c10);
+  return c0 + fx * (c1 - c0);
+}
+
+// interp with exdiv + cell_floor / cell_fix: bit-identical to interp() above.
+template <class G>
+__device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, double px,
+                                              double py, double pz, int& ix, int& iy, int& iz) {
+  double fx, fy, fz;
+  locate<G>(g, px, py, pz, ix, iy, iz, fx, fy, fz);
 #if RMPB_SPEC_LOAD
   // The gather issues right after the floor, with the indices clamped into
   // the map (unsigned min: in bounds whatever they are); only a step outside
   // the clamp range -- the map boundary, rare -- fixes the cell (reference
   // clamps) and gathers again.  Keeps the boundary test's compare + branch
   // off the dependent chain in front of the L2 gather.
-  const bool oob = ((unsigned)ix > (unsigned)g.nxm2) | ((unsigned)iy > (unsigned)g.nym2) |
-                   ((unsigned)iz > (unsigned)g.nzm2);
+  const bool oob = out_of_cells(g, ix, iy, iz);
   Corners c = grid.load((int)min((unsigned)ix, (unsigned)g.nxm2),
                         (int)min((unsigned)iy, (unsigned)g.nym2),
                         (int)min((unsigned)iz, (unsigned)g.nzm2));
@@ -339,21 +361,14 @@ __device__ __forceinline__ double interp_fast(const G& grid, const GridGeom& g, 
   }
 #else
   // one (rarely taken) branch for all three boundary clamps
-  if (((unsigned)ix > (unsigned)g.nxm2) | ((unsigned)iy > (unsigned)g.nym2) |
-      ((unsigned)iz > (unsigned)g.nzm2)) {
+  if (out_of_cells(g, ix, iy, iz)) {
     cell_fix(g.nxm2, ix, fx);
     cell_fix(g.nym2, iy, fy);
     cell_fix(g.nzm2, iz, fz);
   }
   Corners c = grid.load(ix, iy, iz);
 #endif
-  double c00 = c.v000 + fz * (c.v001 - c.v000);
-  double c01 = c.v010 + fz * (c.v011 - c.v010);
-  double c10 = c.v100 + fz * (c.v101 - c.v100);
-  double c11 = c.v110 + fz * (c.v111 - c.v110);
-  double c0 = c00 + fy * (c01 - c00);
-  double c1 = c10 + fy * (c11 - c10);
-  return c0 + fx * (c1 - c0);
+  return lerp8(c, fx, fy, fz);
 }
 
 // ---------------------------------------------------------------------------

@@ -538,6 +538,87 @@ __device__ __forceinline__ void policy_flush(SM& sm, int warp, int lane, bool va
 #define RMPB_LANE_COUNT 1  // lane-private hit count (no per-round ballot)
 #endif
 
+// Prepare the warp's next 32-ray chunk into its shared buffer: direction,
+// slab interval [t0, t1] (max_range applied), shared-first-step start, ray
+// id with the closing / first-step flags; rays that miss the map retire here.
+template <class G, bool RAYOUT, bool INSIDE, int NW>
+__device__ __forceinline__ void prep_chunk(K2Smem<NW>& sm, const GridGeom& g, const Bundle& b,
+                                           const PoseIO& io, const RayOut& ro, int pose, int begin,
+                                           int end, int lane, int warp, unsigned lt, double sx,
+                                           double sy, double sz, double max_range, bool skip1,
+                                           double t1s, int& chunk, int& pcount, int& phead) {
+  const unsigned FULL = 0xffffffffu;
+  const int r = begin + (chunk << 5) + lane;
+  chunk += NW;
+  bool ok = r < end, first = false;
+  double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
+  if (ok) {
+    ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
+    if (INSIDE) {
+      const RecipDir q = b.recip(r);
+      double thi = CUDART_INF;
+      if (ex != 0.0) {
+        const double tb = slab_div((ex > 0.0 ? g.hx : g.ox) - sx, ex, q.hx, q.lx);
+        thi = tb < thi ? tb : thi;
+      }
+      if (ey != 0.0) {
+        const double tb = slab_div((ey > 0.0 ? g.hy : g.oy) - sy, ey, q.hy, q.ly);
+        thi = tb < thi ? tb : thi;
+      }
+      if (ez != 0.0) {
+        const double tb = slab_div((ez > 0.0 ? g.hz : g.oz) - sz, ez, q.hz, q.lz);
+        thi = tb < thi ? tb : thi;
+      }
+      t0 = 0.0;
+      t1 = thi < max_range ? thi : max_range;
+      ok = !(t0 > t1);
+      // shared first step: rays with a finite direction start at t1s
+      // (1 step done); those with t1s > t_end end there (a miss)
+      if (skip1 && ok && isfinite(ex) && isfinite(ey) && isfinite(ez)) {
+        t0 = t1s;
+        first = true;
+        ok = t1s <= t1;  // !(t > t_end): NaN ends the ray
+      }
+    } else {
+      ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, b.recip(r), t0,
+                         t1);
+      if (ok) {
+        t0 = t0 > 0.0 ? t0 : 0.0;
+        t1 = t1 < max_range ? t1 : max_range;
+        ok = !(t0 > t1);
+      }
+    }
+    if (RAYOUT && !ok && ro.t) {
+      const int o = b.perm ? b.perm[r] : r;
+      ro.t[o] = CUDART_INF;
+      if (ro.cell) { ro.cell[3 * o] = -1; ro.cell[3 * o + 1] = -1; ro.cell[3 * o + 2] = -1; }
+      if (ro.steps) ro.steps[o] = first ? 1 : 0;
+    }
+  }
+  const unsigned m = __ballot_sync(FULL, ok);
+  if (ok) {
+    const int pos = __popc(m & lt);
+    RMPB_CHECK(pos < kPrep && r >= begin && r < end && r < b.n);
+    sm.pt[warp][pos] = t0; sm.pe[warp][pos] = t1;
+    sm.px[warp][pos] = ex; sm.py[warp][pos] = ey; sm.pz[warp][pos] = ez;
+#if RMPB_TOWARD_FILTER
+    // policy_accumulate adds nothing for toward <= 0 (_ckern.pyx:295-299):
+    // flag the ray (sign bit) so only closing hits are queued.  Same
+    // expression and rounding as policy_accumulate's test.
+    double vx, vy, vz;
+    io.vel(pose, vx, vy, vz);
+    const double toward = ex * vx + ey * vy + ez * vz;
+    sm.pr[warp][pos] = (int)((unsigned)r | (toward > 0.0 ? 0x80000000u : 0u) |
+                             (first ? 0x40000000u : 0u));
+#else
+    sm.pr[warp][pos] = (int)((unsigned)r | (first ? 0x40000000u : 0u));
+#endif
+  }
+  pcount = __popc(m);
+  phead = 0;
+  __syncwarp();
+}
+
 // RAYOUT: per-ray parity outputs (t, cell, steps) and the step counter.
 // FAST: fp32 march (opt-in, not reference-exact; see interp_f).
 // INSIDE: the pose lies inside the map domain (CTA-uniform: one pose per
@@ -594,75 +675,8 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem<NW>& sm, const G& grid, 
     if ((__popc(need) < RMPB_REFILL && need != FULL) || drained) need = 0u;
     while (need != 0u && (pcount > 0 || chunk < nchunks)) {
       if (pcount == 0) {
-        const int r = begin + (chunk << 5) + lane;
-        chunk += NW;
-        bool ok = r < end, first = false;
-        double ex = 0, ey = 0, ez = 0, t0 = 0, t1 = 0;
-        if (ok) {
-          ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
-          if (INSIDE) {
-            const RecipDir q = b.recip(r);
-            double thi = CUDART_INF;
-            if (ex != 0.0) {
-              const double tb = slab_div((ex > 0.0 ? g.hx : g.ox) - sx, ex, q.hx, q.lx);
-              thi = tb < thi ? tb : thi;
-            }
-            if (ey != 0.0) {
-              const double tb = slab_div((ey > 0.0 ? g.hy : g.oy) - sy, ey, q.hy, q.ly);
-              thi = tb < thi ? tb : thi;
-            }
-            if (ez != 0.0) {
-              const double tb = slab_div((ez > 0.0 ? g.hz : g.oz) - sz, ez, q.hz, q.lz);
-              thi = tb < thi ? tb : thi;
-            }
-            t0 = 0.0;
-            t1 = thi < max_range ? thi : max_range;
-            ok = !(t0 > t1);
-            // shared first step: rays with a finite direction start at t1s
-            // (1 step done); those with t1s > t_end end there (a miss)
-            if (skip1 && ok && isfinite(ex) && isfinite(ey) && isfinite(ez)) {
-              t0 = t1s;
-              first = true;
-              ok = t1s <= t1;  // !(t > t_end): NaN ends the ray
-            }
-          } else {
-            ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, b.recip(r), t0,
-                               t1);
-            if (ok) {
-              t0 = t0 > 0.0 ? t0 : 0.0;
-              t1 = t1 < max_range ? t1 : max_range;
-              ok = !(t0 > t1);
-            }
-          }
-          if (RAYOUT && !ok && ro.t) {
-            const int o = b.perm ? b.perm[r] : r;
-            ro.t[o] = CUDART_INF;
-            if (ro.cell) { ro.cell[3 * o] = -1; ro.cell[3 * o + 1] = -1; ro.cell[3 * o + 2] = -1; }
-            if (ro.steps) ro.steps[o] = first ? 1 : 0;
-          }
-        }
-        const unsigned m = __ballot_sync(FULL, ok);
-        if (ok) {
-          const int pos = __popc(m & lt);
-          RMPB_CHECK(pos < kPrep && r >= begin && r < end && r < b.n);
-          sm.pt[warp][pos] = t0; sm.pe[warp][pos] = t1;
-          sm.px[warp][pos] = ex; sm.py[warp][pos] = ey; sm.pz[warp][pos] = ez;
-#if RMPB_TOWARD_FILTER
-          // policy_accumulate adds nothing for toward <= 0 (_ckern.pyx:295-299):
-          // flag the ray (sign bit) so only closing hits are queued.  Same
-          // expression and rounding as policy_accumulate's test.
-          double vx, vy, vz;
-          io.vel(pose, vx, vy, vz);
-          const double toward = ex * vx + ey * vy + ez * vz;
-          sm.pr[warp][pos] = (int)((unsigned)r | (toward > 0.0 ? 0x80000000u : 0u) |
-                                   (first ? 0x40000000u : 0u));
-#else
-          sm.pr[warp][pos] = (int)((unsigned)r | (first ? 0x40000000u : 0u));
-#endif
-        }
-        pcount = __popc(m);
-        phead = 0;
-        __syncwarp();
+        prep_chunk<G, RAYOUT, INSIDE, NW>(sm, g, b, io, ro, pose, begin, end, lane, warp, lt, sx,
+                                          sy, sz, max_range, skip1, t1s, chunk, pcount, phead);
         continue;
       }
       const int rank = __popc(need & lt);
