@@ -662,9 +662,24 @@ def c5_config(dev, stream, steps=20):
         e1.record(stream)
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
+    # the same poses through a policy-only engine (rays stop at the 2.4 m
+    # activation radius; the same sums -- the partial RMP sums are what the
+    # ray split exchanges)
+    eng_po = RayPolicyEngine(brick, eng.bundle, PARAMS, MAX_RANGE, policy_only=True)
+    ts_po = []
+    for k in range(steps):
+        ep[0] += 1
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        eng_po.exchange(xs[k % 8], vs[k % 8], mb, ep[0], 0, n)
+        e1.record(stream)
+        e1.synchronize()
+        ts_po.append(e0.elapsed_time(e1))
     mb.close()
     ms = statistics.median(ts)
     return {"rays_per_pose": n, "map": "1000x1000x200 @0.05 m TSDF (tau 0.2 m), BRICK 8^3 f32",
+            "policy_only_ms_per_pose_median": round(statistics.median(ts_po), 4),
             "bricks_allocated": info["bricks_allocated"], "brick_bytes": info["brick_bytes"],
             "ms_per_pose_median": round(ms, 4), "ms_per_pose_best": round(min(ts), 4),
             "rays_per_s": round(n / (ms * 1e-3), 1), "hz": round(1e3 / ms, 1),
