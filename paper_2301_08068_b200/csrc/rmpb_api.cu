@@ -337,6 +337,17 @@ extern "C" int rmpb_device_count(int* n) {
   return RMPB_OK;
 }
 
+#ifdef RMPB_DBG_TIMELINE
+// (timing probe builds only) read and reset the lean kernel's timeline
+extern "C" RMPB_EXPORT int rmpb_debug_timeline(unsigned long long out[8]) {
+  CK(cudaDeviceSynchronize());
+  CK(cudaMemcpyFromSymbol(out, g_tl, 8 * sizeof(unsigned long long)));
+  unsigned long long init[8] = {~0ull, 0, 0, 0, 0, 0, 0, 0};
+  CK(cudaMemcpyToSymbol(g_tl, init, sizeof init));
+  return RMPB_OK;
+}
+#endif
+
 extern "C" int rmpb_set_option(const char* name, int64_t value) {
   if (!name) return fail(RMPB_ERR_INVALID, "name is NULL");
   if (!strcmp(name, "seg_rays")) {

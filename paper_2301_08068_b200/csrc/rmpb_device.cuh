@@ -712,25 +712,28 @@ __device__ __forceinline__ void jacobi3(double a[3][3], double V[3][3]) {
   }
 }
 
-// Fast path: when every Cholesky pivot of the (PSD) metric is >= 0.1 x its
-// trace, lambda_min >= 1e-3 lambda_max (the pivots bound det from below), so
-// pinv_psd's 1e-8 cutoff drops nothing and pinv(M) f = M^-1 f: a Cholesky
-// solve (~30 dependent fp64 ops instead of Jacobi sweeps).  Returns false when
-// the metric is not that well conditioned (rank-deficient ones included).
+// Fast path: a Cholesky solve when the (PSD) metric is provably far from the
+// pinv_psd cutoff.  Every pivot d_i is positive and at most tr (d_i <= m_ii),
+// and det = d0 d1 d2 = l0 l1 l2; so det >= 1e-6 tr^3 gives
+//   lambda_min >= det / (l_mid l_max) >= det / tr^2 >= 1e-6 tr >= 1e-6 lambda_max,
+// 100x above pinv_psd's 1e-8 * lambda_max cutoff: nothing is dropped and
+// pinv(M) f = M^-1 f, which the solve gives to ~cond(M) * 2^-53 <= 1e-10
+// relative (~30 dependent fp64 ops instead of Jacobi sweeps: 4.4 -> ~1 us on
+// one pose's final CTA).  Returns false otherwise (rank-deficient or badly
+// conditioned metrics: the Jacobi path).
 __device__ inline bool chol_solve3(const double m[9], const double f[3], double out[3]) {
   const double tr = m[0] + m[4] + m[8];
-  if (!(tr > 0.0)) return false;
-  const double tau = 0.1 * tr;
+  if (!(tr > 1e-90) || !(tr < 1e90)) return false;  // (tr^3 and det stay normal)
   const double d0 = m[0];
-  if (!(d0 >= tau)) return false;
+  if (!(d0 > 0.0)) return false;
   const double l00 = sqrt(d0);
   const double l10 = m[3] / l00, l20 = m[6] / l00;
   const double d1 = m[4] - l10 * l10;
-  if (!(d1 >= tau)) return false;
+  if (!(d1 > 0.0)) return false;
   const double l11 = sqrt(d1);
   const double l21 = (m[7] - l20 * l10) / l11;
   const double d2 = m[8] - l20 * l20 - l21 * l21;
-  if (!(d2 >= tau)) return false;
+  if (!(d2 > 0.0) || !(d0 * d1 * d2 >= 1e-6 * tr * tr * tr)) return false;
   const double l22 = sqrt(d2);
   const double y0 = f[0] / l00;
   const double y1 = (f[1] - l10 * y0) / l11;

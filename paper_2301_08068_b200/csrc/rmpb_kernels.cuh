@@ -136,6 +136,17 @@ __device__ __forceinline__ double fold8(const double* p, int n, int stride) {
   return v[0];
 }
 
+#ifdef RMPB_DBG_TIMELINE
+// (timing probe builds only) [0] min CTA start, [1] max trace end, [2] last
+// CTA after the ticket, [3] after the fold, [4] after write_slot
+__device__ unsigned long long g_tl[8];
+#define RMPB_TL_MIN(k) atomicMin(&g_tl[k], globaltimer_ns())
+#define RMPB_TL_MAX(k) atomicMax(&g_tl[k], globaltimer_ns())
+#else
+#define RMPB_TL_MIN(k)
+#define RMPB_TL_MAX(k)
+#endif
+
 struct ExArgs {  // per-call exchange arguments (kernel parameter of the lean kernel)
   const PeerEx* ex;
   unsigned long long epoch;
@@ -202,6 +213,7 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
   __shared__ double sm[NW * kAcc];
   __shared__ int s_last;
   block_reduce<NW>(acc, sm);
+  if (threadIdx.x == 0) RMPB_TL_MAX(1);
   if (io.seg_out && threadIdx.x == 0) acc_to_arr(acc, io.seg_out + (size_t)(pose * segs + seg) * kAcc);
   if (segs == 1) {
     if (EX) {  // warp 0 runs the exchange (lane 0 holds the total)
@@ -224,6 +236,7 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
     const unsigned prev = ticket_add_release(io.tickets + pose);
     s_last = (prev == (unsigned)(segs - 1));
     if (s_last) fence_acquire_gpu();  // the other segments' partials are visible
+    if (s_last) RMPB_TL_MAX(2);
   }
   __syncthreads();
   if (!s_last) return false;
@@ -251,8 +264,10 @@ __device__ __forceinline__ bool finish_unit(Acc& acc, const PoseIO& io, int pose
     return false;
   }
   if (threadIdx.x == 0) {
+    RMPB_TL_MAX(3);
     io.tickets[pose] = 0u;  // self-reset: graph replays / next call start clean
     write_slot(f, io.slot + (size_t)pose * 13, io.accel ? io.accel + (size_t)pose * 3 : nullptr);
+    RMPB_TL_MAX(4);
     return true;
   }
   return false;
@@ -341,6 +356,7 @@ __device__ __forceinline__ bool lean_unit(const G& grid, const GridGeom& g, cons
                                           int segs, int seg_rays, const RayOut& ro, int unit,
                                           const ExArgs* xa) {
   const int pose = unit / segs, seg = unit - pose * segs;
+  if (threadIdx.x == 0) RMPB_TL_MIN(0);
   double sx, sy, sz, vx, vy, vz;
   io.pose(pose, sx, sy, sz);
   io.vel(pose, vx, vy, vz);

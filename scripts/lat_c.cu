@@ -59,6 +59,17 @@ int main() {
   double r0s = med([&](int i) { call(i, 1e-6, s); });
   double r10s = med([&](int i) { call(i, 10.0, s); });
   double r24 = med([&](int i) { call(i, 2.4, nullptr); });  // policy-only range (radius)
+  rmpb_set_option("l2_window", 0);
+  double r24w = med([&](int i) { call(i, 2.4, nullptr); });
+  double r0w = med([&](int i) { call(i, 1e-6, nullptr); });
+  rmpb_set_option("l2_window", 1);
+  rmpb_set_option("seg_rays", 512);
+  double r24s = med([&](int i) { call(i, 2.4, nullptr); });
+  rmpb_set_option("seg_rays", 1024);
+  double r24s2 = med([&](int i) { call(i, 2.4, nullptr); });
+  rmpb_set_option("seg_rays", 0);
+  printf("{\"abi_range2.4_no_l2window_us\": %.2f, \"abi_range0_no_l2window_us\": %.2f, "
+         "\"abi_range2.4_seg512_us\": %.2f, \"abi_range2.4_seg1024_us\": %.2f}\n", r24w, r0w, r24s, r24s2);
   printf("{\"flag_spin_us\": %.2f, \"query_spin_us\": %.2f, \"launch_only_us\": %.2f, ", e2, e3, e4);
   printf("{\"empty_1x32_us\": %.2f, \"empty_256x256_us\": %.2f, \"abi_range0_us\": %.2f, "
          "\"abi_range10_us\": %.2f, \"abi_range0_stream_us\": %.2f, \"abi_range10_stream_us\": %.2f, "
