@@ -563,6 +563,52 @@ __device__ __forceinline__ TraceResult trace_ray_fast(const G& grid, const GridG
   return r;
 }
 
+// trace_ray_fast for a start inside the node domain, given the pose's first
+// step (d0 = interp at the start, shared by every ray of the pose): the
+// entry side drops out (t0 = 0 exactly) and, with `skip1` (d0 >= eps and no
+// -0.0 coordinate, as k_ray_policy2), a ray with a finite direction starts
+// at t = 0 + step * d0 with one step counted -- bitwise trace_ray_fast.
+template <class G>
+__device__ __forceinline__ TraceResult trace_ray_inside(const G& grid, const GridGeom& g,
+                                                        double sx, double sy, double sz,
+                                                        double dx, double dy, double dz,
+                                                        const RecipDir& q, double max_range,
+                                                        double eps, double step_scale, bool skip1,
+                                                        double t1s) {
+  TraceResult r;
+  r.t = CUDART_INF; r.cx = r.cy = r.cz = -1; r.steps = 0;
+  double thi = CUDART_INF;
+  if (dx != 0.0) {
+    const double tb = slab_div((dx > 0.0 ? g.hx : g.ox) - sx, dx, q.hx, q.lx);
+    thi = tb < thi ? tb : thi;
+  }
+  if (dy != 0.0) {
+    const double tb = slab_div((dy > 0.0 ? g.hy : g.oy) - sy, dy, q.hy, q.ly);
+    thi = tb < thi ? tb : thi;
+  }
+  if (dz != 0.0) {
+    const double tb = slab_div((dz > 0.0 ? g.hz : g.oz) - sz, dz, q.hz, q.lz);
+    thi = tb < thi ? tb : thi;
+  }
+  const double t_end = thi < max_range ? thi : max_range;
+  double t = 0.0;
+  if (t > t_end) return r;
+  if (skip1 && isfinite(dx) && isfinite(dy) && isfinite(dz)) {
+    r.steps = 1;
+    t = t1s;
+    if (!(t <= t_end)) return r;
+  }
+  int ix, iy, iz;
+  while (true) {
+    const double d = interp_fast(grid, g, sx + t * dx, sy + t * dy, sz + t * dz, ix, iy, iz);
+    ++r.steps;
+    if (d < eps) { r.t = t; r.cx = ix; r.cy = iy; r.cz = iz; break; }
+    t += step_scale * d;
+    if (!(t <= t_end)) break;
+  }
+  return r;
+}
+
 // ---------------------------------------------------------------------------
 // Per-ray obstacle policy (rmpnav/_kernels/_ckern.pyx:290-316).  `dir` is the
 // cast direction; r = -dir points away from the obstacle (policies.py:550-552).

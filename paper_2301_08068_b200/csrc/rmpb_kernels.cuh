@@ -366,10 +366,26 @@ __device__ __forceinline__ bool lean_unit(const G& grid, const GridGeom& g, cons
   const int end = min(begin + seg_rays, b.n);
   int my_steps = 0;
   if (io.active && !io.active[pose]) return false;
+  // a pose inside the domain: its first step (t = 0) is shared by all rays
+  // (k_ray_policy2's shared first step), one dependent step off every chain
+  const bool inside =
+      sx >= g.ox && sx <= g.hx && sy >= g.oy && sy <= g.hy && sz >= g.oz && sz <= g.hz;
+  bool skip1 = false;
+  double t1s = 0.0;
+  if (inside) {
+    int cx, cy, cz;
+    const double d0 = interp_fast(grid, g, sx, sy, sz, cx, cy, cz);
+    const bool negz = (sx == 0.0 && signbit(sx)) || (sy == 0.0 && signbit(sy)) ||
+                      (sz == 0.0 && signbit(sz));
+    skip1 = !(d0 < eps) && !negz;
+    t1s = 0.0 + step_scale * d0;
+  }
   for (int i = begin + threadIdx.x; i < end; i += kBlock) {
     const double dx = b.dx[i], dy = b.dy[i], dz = b.dz[i];
-    TraceResult r = trace_ray_fast(grid, g, sx, sy, sz, dx, dy, dz, b.recip(i), max_range, eps,
-                                   step_scale);
+    TraceResult r = inside ? trace_ray_inside(grid, g, sx, sy, sz, dx, dy, dz, b.recip(i),
+                                              max_range, eps, step_scale, skip1, t1s)
+                           : trace_ray_fast(grid, g, sx, sy, sz, dx, dy, dz, b.recip(i),
+                                            max_range, eps, step_scale);
     policy_accumulate(acc, dx, dy, dz, r.t, vx, vy, vz, p);
     my_steps += r.steps;
     if (ro.t) {
