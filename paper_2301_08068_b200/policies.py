@@ -32,7 +32,7 @@ import numpy as np
 
 from ._kernels import get_backend
 from .core import Policy, RobotState
-from .geometry import EsdfGrid, Scene
+from .geometry import EsdfGrid
 from .rays import (DEFAULT_MAX_RANGE, GRID_STEP_SCALE, RangeScan, RayBundle, policy_range,
                    raycast_many)
 

@@ -2,7 +2,7 @@
 4096 poses x 65536 rays, C1 map, L2 flushed between reps; prints one line."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 from paper_2301_08068_b200 import synth
 from paper_2301_08068_b200.device import RayPolicyEngine
 import paper_2301_08068_b200 as P

@@ -2,7 +2,7 @@
 without the map's L2 access-policy window (option l2_window)."""
 import sys, os, json
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 from paper_2301_08068_b200 import synth, _lib
 from paper_2301_08068_b200.device import RayPolicyEngine
 import paper_2301_08068_b200 as P

@@ -3,7 +3,7 @@ speed) as the partial kernel and as the K4 fused exchange kernel (world-1
 mailbox), 5 launches each, for the launch list's device durations."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 from paper_2301_08068_b200 import synth
 from paper_2301_08068_b200._kernels import b200
 from paper_2301_08068_b200.device import RayPolicyEngine, PeerMailbox

@@ -2,7 +2,7 @@
 pinv (accel output NULL), at max range ~0 (fixed cost only) and 10 m."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 from paper_2301_08068_b200 import synth, _lib as L
 from paper_2301_08068_b200.device import RayPolicyEngine
 import paper_2301_08068_b200 as P

@@ -1,7 +1,7 @@
 """ncu target: a 1-robot closed-loop rollout on the C1 map, 32 ticks."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 import paper_2301_08068_b200 as P
 from paper_2301_08068_b200 import synth
 from paper_2301_08068_b200.rollout import BatchRolloutConfig, RolloutBatch

@@ -2,7 +2,7 @@
 5 single-pose launches, of k_ray_policy2 on the C1 map."""
 import sys, os
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-import numpy as np, torch
+import torch
 from paper_2301_08068_b200 import synth
 from paper_2301_08068_b200.device import RayPolicyEngine
 import paper_2301_08068_b200 as P
