@@ -592,8 +592,12 @@ def _params_cached(params):
     """(array, pointer) of the 7 params; LRU-cached for hashable params.
     The CALLER must keep the returned array alive until the C call returns
     (the pointer alone does not own the buffer)."""
-    key = tuple(params) if not isinstance(params, np.ndarray) else None
+    key = (params if type(params) is tuple else tuple(params)) \
+        if not isinstance(params, np.ndarray) else None
     if key is not None:
+        hit = _param_cache.get(key)  # (a dict lookup is atomic: no lock on a hit)
+        if hit is not None:
+            return hit
         with _lock:
             hit = _param_cache.get(key)
             if hit is None:

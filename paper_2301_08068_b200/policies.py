@@ -145,6 +145,7 @@ def esdf_policy(state: RobotState, grid: EsdfGrid, p: ObstacleParams) -> Policy:
 
 
 _SYM_SAFE = 8.98e307  # 0.5 * (m + m.T) overflows above DBL_MAX / 2
+_F64 = np.dtype(np.float64)
 
 
 def _policy_from_slot(slot, accel) -> Policy:
@@ -153,12 +154,13 @@ def _policy_from_slot(slot, accel) -> Policy:
     returns it unchanged whenever it cannot overflow: such slots take a
     check-only path (~2 us instead of ~15 us of small NumPy ops); anything
     else goes through Policy's own construction (and its ValueError)."""
-    if type(slot) is np.ndarray and type(accel) is np.ndarray and slot.dtype == np.float64 \
-            and accel.dtype == np.float64 and slot.ndim == 1 and accel.shape == (3,):
+    if type(slot) is np.ndarray and type(accel) is np.ndarray and slot.dtype is _F64 \
+            and accel.dtype is _F64 and slot.ndim == 1 and accel.shape == (3,):
         lm = slot.tolist()
-        # sum(|x|) < bound: every |x| below it, and NaN / inf fail the test
-        if (len(lm) >= 9 and lm[1] == lm[3] and lm[2] == lm[6] and lm[5] == lm[7]
-                and sum(map(abs, lm[:9])) < _SYM_SAFE and sum(map(abs, accel.tolist())) < math.inf):
+        m9 = lm[:9]
+        tot = sum(m9) + sum(accel.tolist())  # NaN / inf (or an overflowing sum) -> not finite
+        if (len(lm) >= 9 and tot - tot == 0.0 and lm[1] == lm[3] and lm[2] == lm[6]
+                and lm[5] == lm[7] and max(m9) < _SYM_SAFE and min(m9) > -_SYM_SAFE):
             return Policy._trusted(accel, slot[0:9].reshape(3, 3))
     return Policy(np.asarray(accel, dtype=float), np.asarray(slot[0:9], dtype=float).reshape(3, 3))
 
