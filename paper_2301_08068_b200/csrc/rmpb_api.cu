@@ -242,16 +242,26 @@ static int with_grid(const rmpb_grid* g, F&& f) {
                           (unsigned)(g->nx * g->ny * g->nz)};
     return f(a);
   }
+  const bool o0 = G.ox == 0.0 && G.oy == 0.0 && G.oz == 0.0 && !std::signbit(G.ox) &&
+                  !std::signbit(G.oy) && !std::signbit(G.oz);  // +0.0 only: p - (+0) == p
   if (g->layout == LAYOUT_PAIR64) {
-    PairGridF64 a{(const double2*)g->d_values, G.nz - 1, G.ny * (G.nz - 1),
+    PairGridF64 a{(const double2*)g->d_values, G.nz - 1, G.ny * (G.nz - 1), 1, G.nz - 1,
                   (unsigned)(g->nx * g->ny * (g->nz - 1))};
+    if (G.div2 && o0) {
+      PairGridF64Div2O0 a3;
+      static_cast<PairGridF64&>(a3) = a;
+      return f(a3);
+    }
+    if (G.div2) {
+      PairGridF64Div2 a2;
+      static_cast<PairGridF64&>(a2) = a;
+      return f(a2);
+    }
     return f(a);
   }
   if (g->layout == LAYOUT_QUAD) {  // f32 storage only (grid_build)
     QuadGridF32 a{(const float4*)g->d_values, G.nz - 1, G.nx,
                   (unsigned)(g->nx * (g->ny - 1) * (g->nz - 1))};
-    const bool o0 = G.ox == 0.0 && G.oy == 0.0 && G.oz == 0.0 && !std::signbit(G.ox) &&
-                    !std::signbit(G.oy) && !std::signbit(G.oz);  // +0.0 only: p - (+0) == p
     if (G.div2 && o0) {  // + origin at (+0, +0, +0): the subtraction leaves the chain
       QuadGridF32Div2O0 a3;
       static_cast<QuadGridF32&>(a3) = a;

@@ -191,12 +191,13 @@ struct origin0<G, decltype((void)G::kOrigin0)> { static constexpr bool value = G
 struct PairGridF64 {
   static constexpr bool kDiv2 = false;
   const double2* __restrict__ q;
-  int py, px;  // strides in pairs: (nz-1), ny*(nz-1)
-  unsigned lim;  // pair count (RMPB_CHECKED builds)
+  int py, px, pz;  // strides in pairs: y nz-1, x ny*(nz-1), z 1
+  int nzm1;        // nz - 1 (RMPB_CHECKED builds)
+  unsigned lim;    // pair count (RMPB_CHECKED builds)
   __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
-    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && iz < py &&
-               (unsigned)(ix * px + iy * py + iz) + (unsigned)(px + py) < lim);
-    const double2* b = q + (unsigned)(ix * px + iy * py + iz);
+    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 && iz < nzm1 &&
+               (unsigned)(ix * px + iy * py + iz * pz) + (unsigned)(px + py) < lim);
+    const double2* b = q + (unsigned)(ix * px + iy * py + iz * pz);
     double2 a0 = __ldg(b), a1 = __ldg(b + (unsigned)py);
     double2 c0 = __ldg(b + (unsigned)px), c1 = __ldg(b + (unsigned)(px + py));
     Corners k;
@@ -204,6 +205,14 @@ struct PairGridF64 {
     k.v100 = c0.x; k.v101 = c0.y; k.v110 = c1.x; k.v111 = c1.y;
     return k;
   }
+};
+// f64 maps whose resolution passes div2_exact() / with the origin at +0: the
+// same 2-op division and origin-0 forms as the QUAD accessors.
+struct PairGridF64Div2 : PairGridF64 {
+  static constexpr bool kDiv2 = true;
+};
+struct PairGridF64Div2O0 : PairGridF64Div2 {
+  static constexpr bool kOrigin0 = true;
 };
 
 // Block-hashed sparse grid: bricks of B^3 nodes; brick (bi,bj,bk) ->

@@ -22,7 +22,12 @@ states = synth.bench_states(scene, count=PB, seed=123)
 x_h, v_h = synth.states_arrays(states)
 bundle = P.sample_directions(65536)
 MR = float(os.environ.get("MAX_RANGE", "10.0"))
-eng = RayPolicyEngine(grid, bundle, P.preset("static_map").obstacle.as_tuple(), MR)
+gsrc = grid
+if os.environ.get("LAYOUT"):  # e.g. 4 = PAIR64 (librmpb LAYOUT_*)
+    from paper_2301_08068_b200._kernels import b200
+    gsrc = b200.DeviceGrid(grid.values, grid.origin, grid.resolution,
+                           storage=_lib.STORE_F64, layout=int(os.environ["LAYOUT"]))
+eng = RayPolicyEngine(gsrc, bundle, P.preset("static_map").obstacle.as_tuple(), MR)
 x = torch.from_numpy(x_h).cuda(); v = torch.from_numpy(v_h).cuda()
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
 s0, a0 = eng.evaluate(x, v); torch.cuda.synchronize()
@@ -37,7 +42,7 @@ print(json.dumps({"lib": os.path.basename(os.environ.get("RMPB_LIBRARY", "") or 
                   "l2_window": os.environ.get("L2_WINDOW", "default"),
                   "seg_rays": os.environ.get("SEG_RAYS", "auto"),
                   "carveout": os.environ.get("CARVEOUT", "default"),
-                  "trace_warps": os.environ.get("TRACE_WARPS", "8"), "max_range": MR,
+                  "trace_warps": os.environ.get("TRACE_WARPS", "8"), "max_range": MR, "layout": os.environ.get("LAYOUT", "auto"),
                   "ms_min": round(min(ts), 3), "ms_med": round(sorted(ts)[len(ts) // 2], 3),
                   "hits": int(sl[:, 12].sum()), "sum_a00": float(sl[:, 0].sum()),
                   "sum_b0": float(sl[:, 9].sum())}), flush=True)
