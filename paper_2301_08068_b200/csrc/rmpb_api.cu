@@ -274,9 +274,19 @@ static int with_grid(const rmpb_grid* g, F&& f) {
     }
     return f(a);
   }
-  if (g->storage == RMPB_STORE_F32) {
-    BrickGrid<float> a{(const float*)g->d_values, g->d_table, g->bny, g->bnz, (float)g->fill,
-                       (unsigned)(g->bnx * g->bny * g->bnz), (unsigned)g->bricks};
+  if (g->storage == RMPB_STORE_F32) {  // apron-QUAD bricks (brickq_build)
+    BrickQuadF32 a{(const float4*)g->d_values, g->d_table, g->bny, g->bnz, (float)g->fill,
+                   (unsigned)(g->bnx * g->bny * g->bnz), (unsigned)g->bricks};
+    if (G.div2 && o0) {
+      BrickQuadF32Div2O0 a3;
+      static_cast<BrickQuadF32&>(a3) = a;
+      return f(a3);
+    }
+    if (G.div2) {
+      BrickQuadF32Div2 a2;
+      static_cast<BrickQuadF32&>(a2) = a;
+      return f(a2);
+    }
     return f(a);
   }
   BrickGrid<double> a{(const double*)g->d_values, g->d_table, g->bny, g->bnz, g->fill,
@@ -585,6 +595,43 @@ static int brick_build_t(rmpb_grid* g, const T* d_lin, T fill, cudaStream_t st) 
   return RMPB_OK;
 }
 
+// f32 bricks as apron-QUAD records (BrickQuadF32).
+static int brickq_build(rmpb_grid* g, const float* d_lin, float fill, cudaStream_t st) {
+  const int nx = (int)g->nx, ny = (int)g->ny, nz = (int)g->nz;
+  const int bnx = (nx + 7) / 8, bny = (ny + 7) / 8, bnz = (nz + 7) / 8;
+  const int nb = bnx * bny * bnz;
+  int *flag = nullptr, *slot = nullptr;
+  CK(cudaMalloc((void**)&flag, (size_t)(nb + 1) * sizeof(int)));
+  CK(cudaMalloc((void**)&slot, (size_t)(nb + 1) * sizeof(int)));
+  k_brickq_flags<<<nb, 512, 0, st>>>(d_lin, nx, ny, nz, fill, flag);
+  CKL();
+  CK(cudaMemsetAsync(flag + nb, 0, sizeof(int), st));
+  size_t tmpb = 0;
+  CK(cub::DeviceScan::ExclusiveSum(nullptr, tmpb, flag, slot, nb + 1, st));
+  void* tmp = nullptr;
+  CK(cudaMalloc(&tmp, tmpb));
+  CK(cub::DeviceScan::ExclusiveSum(tmp, tmpb, flag, slot, nb + 1, st));
+  g_launches.fetch_add(1);
+  int count = 0;
+  CK(cudaMemcpyAsync(&count, slot + nb, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  rfree(tmp);
+  const size_t pool_b = (size_t)(count > 0 ? count : 1) * 576 * sizeof(float4);
+  CK(cudaMalloc(&g->d_values, pool_b));
+  CK(cudaMalloc((void**)&g->d_table, (size_t)nb * sizeof(int32_t)));
+  k_brickq_fill<<<nb, 576, 0, st>>>(d_lin, nx, ny, nz, fill, flag, slot, g->d_table,
+                                    (float4*)g->d_values);
+  CKL();
+  CK(cudaStreamSynchronize(st));
+  rfree(flag);
+  rfree(slot);
+  g->layout = LAYOUT_BRICK;
+  g->bnx = bnx; g->bny = bny; g->bnz = bnz;
+  g->bricks = count;
+  g->bytes = (int64_t)(pool_b + (size_t)nb * sizeof(int32_t));
+  return RMPB_OK;
+}
+
 // d_src: device linear values (dtype); resolves storage like grid_build.
 static int brick_build(rmpb_grid* g, const void* d_src, int dtype, double fill, int storage,
                        cudaStream_t st) {
@@ -613,12 +660,12 @@ static int brick_build(rmpb_grid* g, const void* d_src, int dtype, double fill, 
   g->storage = store;
   g->fill = fill;
   if (store == RMPB_STORE_F64) return brick_build_t<double>(g, (const double*)d_src, fill, st);
-  if (dtype == RMPB_F32) return brick_build_t<float>(g, (const float*)d_src, (float)fill, st);
+  if (dtype == RMPB_F32) return brickq_build(g, (const float*)d_src, (float)fill, st);
   float* lin = nullptr;
   CK(cudaMalloc((void**)&lin, n * sizeof(float)));
   k_to_f32<<<grid_blocks(n), 256, 0, st>>>(n, (const double*)d_src, lin);
   CKL();
-  int rc = brick_build_t<float>(g, lin, (float)fill, st);
+  int rc = brickq_build(g, lin, (float)fill, st);
   rfree(lin);
   return rc;
 }
@@ -1123,8 +1170,9 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
   if (units >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many CTA units");
   // one ray per thread -> the lean kernel (nothing to refill); else lane refill
   const int64_t kopt = g_opt_kernel.load();
-  // the K4 exchange epilogue lives in the lean kernel only
-  const bool v2 = !xa && (kopt == 2 || (kopt == 0 && seg_rays > kBlock) || mode == RMPB_MODE_FAST);
+  // (the K4 exchange epilogue: either kernel, exact mode)
+  const bool v2 = kopt == 2 || (kopt == 0 && seg_rays > kBlock) || mode == RMPB_MODE_FAST;
+  if (xa && mode != RMPB_MODE_EXACT) return fail(RMPB_ERR_UNSUPPORTED, "exchange: exact mode only");
   const ExArgs xv = xa ? *xa : ExArgs{nullptr, 0ull, 0};
   return with_grid(g, [&](auto acc) -> int {
     using G = decltype(acc);
@@ -1138,6 +1186,7 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
       }
       apply_carveout(k_ray_policy2<G, true>);
       apply_carveout(k_ray_policy2<G, false>);
+      apply_carveout(k_ray_policy2<G, false, false, kTraceWarps, true>);
     }
     cudaError_t le = cudaSuccess;
     const unsigned nb = (unsigned)units;
@@ -1148,24 +1197,28 @@ static int launch_ray_policy(const rmpb_grid* g, const rmpb_bundle* b, PoseIO io
     } else if (!v2) {
       le = launch_mapped(g, k_ray_policy<G>, nb, kBlock, st, acc, g->geom, bv, io, pp, max_range,
                          eps, step_scale, segs, seg_rays, ro, xv);
+    } else if (xa) {
+      le = launch_mapped_smem(g, k_ray_policy2<G, false, false, kTraceWarps, true>, nb,
+                              kTraceWarps * 32, sm8, st, acc, g->geom, bv, io, pp, max_range, eps,
+                              step_scale, segs, seg_rays, ro, xv);
     } else if (mode == RMPB_MODE_FAST) {
       if constexpr (kFastOk) {
         if (ro.step_total)
           le = launch_mapped_smem(g, k_ray_policy2<G, true, true>, nb, kTraceWarps * 32, sm8, st, acc,
                                   g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays,
-                                  ro);
+                                  ro, xv);
         else
           le = launch_mapped_smem(g, k_ray_policy2<G, false, true>, nb, kTraceWarps * 32, sm8, st, acc,
                                   g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays,
-                                  ro);
+                                  ro, xv);
       }
     } else if (ro.t || ro.step_total) {
       le = launch_mapped_smem(g, k_ray_policy2<G, true>, nb, kTraceWarps * 32, sm8, st, acc, g->geom, bv,
-                              io, pp, max_range, eps, step_scale, segs, seg_rays, ro);
+                              io, pp, max_range, eps, step_scale, segs, seg_rays, ro, xv);
     } else {
       le = launch_mapped_smem(g, k_ray_policy2<G, false>, nb, kTraceWarps * 32, sm8, st, acc,
                               g->geom, bv, io, pp, max_range, eps, step_scale, segs, seg_rays,
-                              ro);
+                              ro, xv);
     }
     CK(le);
     CKL();

@@ -441,6 +441,45 @@ k_brick_fill(const T* __restrict__ v, int nx, int ny, int nz, T fill, const int*
   pool[(long long)slot[bid] * 512 + ((li << 6) | (lj << 3) | lk)] = x;
 }
 
+// Apron-QUAD bricks (BrickQuadF32): a brick is needed when any node of its
+// 9^3 box [8b, 8b+9) (clipped to the map) differs from fill.
+__global__ void __launch_bounds__(512)
+k_brickq_flags(const float* __restrict__ v, int nx, int ny, int nz, float fill,
+               int* __restrict__ flag) {
+  const int bnz = (nz + 7) >> 3, bny = (ny + 7) >> 3;
+  const int bid = blockIdx.x;
+  const int bk = bid % bnz, bj = (bid / bnz) % bny, bi = bid / (bnz * bny);
+  bool diff = false;
+  for (int t = threadIdx.x; t < 729; t += 512) {
+    const int i = bi * 8 + t / 81, j = bj * 8 + (t / 9) % 9, k = bk * 8 + t % 9;
+    if (i < nx && j < ny && k < nz) diff |= !(v[((long long)i * ny + j) * nz + k] == fill);
+  }
+  const int any = __syncthreads_or(diff);
+  if (threadIdx.x == 0) flag[bid] = any ? 1 : 0;
+}
+
+// Record (lj*8 + lk)*9 + li of brick bid: the QUAD record of node
+// 8 (bi, bj, bk) + (li, lj, lk); nodes outside the map read fill (no cell
+// inside the map reaches them).
+__global__ void __launch_bounds__(576)
+k_brickq_fill(const float* __restrict__ v, int nx, int ny, int nz, float fill,
+              const int* __restrict__ flag, const int* __restrict__ slot,
+              int* __restrict__ table, float4* __restrict__ pool) {
+  const int bnz = (nz + 7) >> 3, bny = (ny + 7) >> 3;
+  const int bid = blockIdx.x;
+  const int bk = bid % bnz, bj = (bid / bnz) % bny, bi = bid / (bnz * bny);
+  if (threadIdx.x == 0) table[bid] = flag[bid] ? slot[bid] : -1;
+  if (!flag[bid]) return;
+  const int r = threadIdx.x;  // 0..575
+  const int li = r % 9, lk = (r / 9) & 7, lj = r / 72;
+  const int i = bi * 8 + li, j = bj * 8 + lj, k = bk * 8 + lk;
+  auto at = [&](int a, int b, int c) -> float {
+    return (a < nx && b < ny && c < nz) ? v[((long long)a * ny + b) * nz + c] : fill;
+  };
+  pool[(long long)slot[bid] * 576 + r] =
+      make_float4(at(i, j, k), at(i, j, k + 1), at(i, j + 1, k), at(i, j + 1, k + 1));
+}
+
 // Node values back out of any layout (test / export path): node (i,j,k) is
 // corner v000 of cell (i,j,k), or a v1xx / vx1x / vxx1 corner at the far faces.
 template <class G>

@@ -262,6 +262,47 @@ struct BrickGrid {
   }
 };
 
+// Block-hashed f32 map, bricks of 8^3 CELLS stored as QUAD records with a
+// one-node apron: brick (bi, bj, bk) holds, for li in 0..8 and lj, lk in
+// 0..7, the record {v[i,j,k], v[i,j,k+1], v[i,j+1,k], v[i,j+1,k+1]} of node
+// (i, j, k) = 8 (bi, bj, bk) + (li, lj, lk) at (lj*8 + lk)*9 + li -- so every
+// cell whose base lies in the brick reads its 8 corners as two adjacent
+// 16-B records of ONE brick: a table lookup + 2 gathers per step (the
+// scalar-pool layout needed a lookup + 8 gathers, and 8 lookups at brick
+// faces).  A brick is allocated when any node of its 9^3 apron box differs
+// from `fill`, so an unallocated brick's cells have every corner == fill.
+struct BrickQuadF32 {
+  static constexpr bool kDiv2 = false;
+  const float4* __restrict__ pool;    // slot * 576 + (lj*8 + lk)*9 + li
+  const int32_t* __restrict__ table;  // (bi*bny + bj)*bnz + bk -> slot or -1
+  int bny, bnz;
+  float fill;
+  unsigned tlim, plim;  // table entries, allocated bricks (RMPB_CHECKED builds)
+  __device__ __forceinline__ Corners load(int ix, int iy, int iz) const {
+    RMPB_CHECK(ix >= 0 && iy >= 0 && iz >= 0 &&
+               (unsigned)(((ix >> 3) * bny + (iy >> 3)) * bnz + (iz >> 3)) < tlim);
+    const int sl = __ldg(table + ((ix >> 3) * bny + (iy >> 3)) * bnz + (iz >> 3));
+    RMPB_CHECK(sl < (int)plim);
+    Corners k;
+    if (sl < 0) {
+      const double f = (double)fill;
+      k.v000 = k.v001 = k.v010 = k.v011 = k.v100 = k.v101 = k.v110 = k.v111 = f;
+      return k;
+    }
+    const float4* b = pool + (size_t)sl * 576 + ((((iy & 7) << 3) | (iz & 7)) * 9 + (ix & 7));
+    const float4 a = __ldg(b), c = __ldg(b + 1);
+    k.v000 = a.x; k.v001 = a.y; k.v010 = a.z; k.v011 = a.w;
+    k.v100 = c.x; k.v101 = c.y; k.v110 = c.z; k.v111 = c.w;
+    return k;
+  }
+};
+struct BrickQuadF32Div2 : BrickQuadF32 {
+  static constexpr bool kDiv2 = true;
+};
+struct BrickQuadF32Div2O0 : BrickQuadF32Div2 {
+  static constexpr bool kOrigin0 = true;
+};
+
 // ---------------------------------------------------------------------------
 // Exact interpolation (rmpnav/_kernels/_ckern.pyx:92-135).
 template <class G>

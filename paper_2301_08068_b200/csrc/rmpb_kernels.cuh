@@ -656,13 +656,14 @@ __device__ __forceinline__ void prep_chunk(K2Smem<NW>& sm, const GridGeom& g, co
 // INSIDE: the pose lies inside the map domain (CTA-uniform: one pose per
 // CTA), so the body is compiled without the per-refill domain test
 // (13.78 -> 13.55 ms per 4096-pose C1 step).
-template <class G, bool RAYOUT, bool FAST, bool INSIDE, int NW>
+template <class G, bool RAYOUT, bool FAST, bool INSIDE, int NW, bool EX = false>
 __device__ __forceinline__ void ray_policy2_body(K2Smem<NW>& sm, const G& grid, const GridGeom& g,
                                                  const Bundle& b, const PoseIO& io,
                                                  const PolicyParams& p, double max_range,
                                                  double eps, double step_scale, int segs,
                                                  int seg_rays, const RayOut& ro, int pose, int seg,
-                                                 double sx, double sy, double sz) {
+                                                 double sx, double sy, double sz,
+                                                 const ExArgs* xa = nullptr) {
   using real = typename std::conditional<FAST, float, double>::type;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const unsigned FULL = 0xffffffffu;
@@ -824,7 +825,7 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem<NW>& sm, const G& grid, 
     acc.b0 = sm.acc[warp][6]; acc.b1 = sm.acc[warp][7]; acc.b2 = sm.acc[warp][8];
     acc.cnt = cnt;  // warp-uniform count: contributed once per warp
   }
-  finish_unit<false, NW>(acc, io, pose, seg, segs);
+  finish_unit<EX, NW>(acc, io, pose, seg, segs, xa);
 }
 
 // NW warps per CTA (kTraceWarps): one (pose, ray segment) unit per CTA.
@@ -838,10 +839,11 @@ __device__ __forceinline__ void ray_policy2_body(K2Smem<NW>& sm, const G& grid, 
 #define RMPB_TRACE_MINB (RMPB_MINB * kWarps / RMPB_NW)
 #endif
 constexpr int kTraceWarps = RMPB_NW;
-template <class G, bool RAYOUT, bool FAST = false, int NW = kTraceWarps>
+// EX: with the K4 peer-exchange epilogue (config C5 ray split; exact only).
+template <class G, bool RAYOUT, bool FAST = false, int NW = kTraceWarps, bool EX = false>
 __global__ void __launch_bounds__(NW * 32, RMPB_TRACE_MINB)
 k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double max_range,
-              double eps, double step_scale, int segs, int seg_rays, RayOut ro) {
+              double eps, double step_scale, int segs, int seg_rays, RayOut ro, ExArgs xa) {
   // dynamic: sizeof(K2Smem<32>) = 72 KB exceeds the 48 KB static limit
   extern __shared__ __align__(16) unsigned char k2_dsm[];
   K2Smem<NW>& sm = *reinterpret_cast<K2Smem<NW>*>(k2_dsm);
@@ -859,13 +861,13 @@ k_ray_policy2(G grid, GridGeom g, Bundle b, PoseIO io, PolicyParams p, double ma
   if (lane < 9) sm.acc[warp][lane] = 0.0;
   __syncthreads();
   if (inside)
-    ray_policy2_body<G, RAYOUT, FAST, true, NW>(sm, grid, g, b, io, p, max_range, eps,
+    ray_policy2_body<G, RAYOUT, FAST, true, NW, EX>(sm, grid, g, b, io, p, max_range, eps,
                                                 step_scale, segs, seg_rays, ro, pose, seg, sx, sy,
-                                                sz);
+                                                sz, &xa);
   else
-    ray_policy2_body<G, RAYOUT, FAST, false, NW>(sm, grid, g, b, io, p, max_range, eps,
+    ray_policy2_body<G, RAYOUT, FAST, false, NW, EX>(sm, grid, g, b, io, p, max_range, eps,
                                                  step_scale, segs, seg_rays, ro, pose, seg, sx,
-                                                 sy, sz);
+                                                 sy, sz, &xa);
 }
 
 // K2: LiDAR-direct policy (policies.py:195-205, rays.py:172-173).  Beam k of

@@ -48,10 +48,20 @@ def timed(fn, reps=7):
     return round(statistics.median(ts), 4)
 
 
-out = {"exchange_lean": [], "batch_lean": [], "batch_k2": []}
+if os.environ.get("C5_SWEEP"):  # kernel x seg_rays sweep of the batch path (median over poses)
+    for kern in (1, 2):
+        for sr in (256, 512, 1024, 2048, 4096, 8192):
+            _lib.set_option("kernel", kern)
+            _lib.set_option("seg_rays", sr)
+            v = [timed(lambda: eng.evaluate(xs[k], vs[k]), reps=5) for k in range(8)]
+            print(json.dumps({"kernel": kern, "seg_rays": sr, "median": statistics.median(v)}), flush=True)
+    _lib.set_option("kernel", 0)
+    _lib.set_option("seg_rays", 0)
+    sys.exit(0)
+out = {"exchange_auto": [], "batch_lean": [], "batch_k2": []}
 slots = {}
 for k in range(8):
-    out["exchange_lean"].append(timed(lambda: ex(k)))
+    out["exchange_auto"].append(timed(lambda: ex(k)))
     for name, kern in (("batch_lean", 1), ("batch_k2", 2)):
         _lib.set_option("kernel", kern)
         out[name].append(timed(lambda: eng.evaluate(xs[k], vs[k])))

@@ -44,7 +44,18 @@ def baseline(eng, x, v, world):
     return eng.resolve(torch.stack(parts))
 
 
-def test_exchange_world1_equals_partial_fold(world_small, oracle):
+@pytest.fixture(params=[0, 1, 2], ids=["auto", "lean", "refill"])
+def kernel_opt(request):
+    """Run with librmpb option `kernel` = auto / the lean kernel / the refill
+    kernel k_ray_policy2: the K4 epilogue is compiled into both."""
+    from paper_2301_08068_b200 import _lib
+
+    _lib.set_option("kernel", request.param)
+    yield request.param
+    _lib.set_option("kernel", 0)
+
+
+def test_exchange_world1_equals_partial_fold(world_small, oracle, kernel_opt):
     from paper_2301_08068_b200.device import PeerMailbox
 
     eng, x, v, vals, dirs = world_small
@@ -64,7 +75,7 @@ def test_exchange_world1_equals_partial_fold(world_small, oracle):
 
 
 @pytest.mark.parametrize("world", [2, 3, 8])
-def test_exchange_same_process_ranks_sequential(world_small, world):
+def test_exchange_same_process_ranks_sequential(world_small, world, kernel_opt):
     from paper_2301_08068_b200.device import EX_POST, EX_WAIT, PeerMailbox
     from paper_2301_08068_b200.parallel import balanced_range
 
