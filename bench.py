@@ -332,7 +332,7 @@ def run_b200(args):
             "l2_stream_peak_GBps": l2.get("stream"),
             "frac_of_l2_stream_peak": (round(achieved / l2["stream"], 4)
                                        if l2.get("stream") else None),
-            "kernel": "k_ray_policy2<QuadGridF32>",
+            "kernel": "k_ray_policy2<QuadGridF32Div2O0>",
             "algorithmic_bytes_per_launch": algo_bytes,
             "voxel_steps_per_launch": vox_steps,
             "note": "bytes = voxel-steps x 8 corners x 4 B (f32 map); map is L2-resident"}
@@ -678,12 +678,14 @@ def c5_config(dev, stream, steps=20):
         ts_po.append(e0.elapsed_time(e1))
     mb.close()
     ms = statistics.median(ts)
-    return {"rays_per_pose": n, "map": "1000x1000x200 @0.05 m TSDF (tau 0.2 m), BRICK 8^3 f32",
+    return {"rays_per_pose": n,
+            "map": "1000x1000x200 @0.05 m TSDF (tau 0.2 m), BRICK 8^3 f32 (apron-QUAD records)",
             "policy_only_ms_per_pose_median": round(statistics.median(ts_po), 4),
             "bricks_allocated": info["bricks_allocated"], "brick_bytes": info["brick_bytes"],
             "ms_per_pose_median": round(ms, 4), "ms_per_pose_best": round(min(ts), 4),
             "rays_per_s": round(n / (ms * 1e-3), 1), "hz": round(1e3 / ms, 1),
-            "kernel": "k_ray_policy<BrickGrid<float>, EX> (K4 exchange epilogue, world 1)"}
+            "kernel": "k_ray_policy2<BrickQuadF32*, EX> (K4 exchange epilogue, world 1; the "
+                      "kernel the batch path selects for 512-ray segments)"}
 
 
 def run_c5(args):
@@ -783,7 +785,7 @@ def run_c5(args):
                "config": {"workload": "C5: one pose x 1 M Halton rays, 1000x1000x200 @0.05 m "
                                       "block-hashed TSDF (tau 0.2 m), max range 10 m, rays "
                                       f"split over {world} GPU(s)",
-                          "rays_per_pose": n, "map": "BRICK 8^3, f32", **info,
+                          "rays_per_pose": n, "map": "BRICK 8^3, f32 apron-QUAD records", **info,
                           "build_s": round(build_s, 2),
                           "parallelism": f"ray-split x{world} (K4 peer-mailbox exchange)"},
                "hz": round(1e3 / ms_fused, 1),
