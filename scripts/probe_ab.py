@@ -26,7 +26,8 @@ gsrc = grid
 if os.environ.get("LAYOUT"):  # e.g. 4 = PAIR64 (librmpb LAYOUT_*)
     from paper_2301_08068_b200._kernels import b200
     gsrc = b200.DeviceGrid(grid.values, grid.origin, grid.resolution,
-                           storage=_lib.STORE_F64, layout=int(os.environ["LAYOUT"]))
+                           storage=int(os.environ.get("STORAGE", "0")),
+                           layout=int(os.environ["LAYOUT"]))
 eng = RayPolicyEngine(gsrc, bundle, P.preset("static_map").obstacle.as_tuple(), MR)
 x = torch.from_numpy(x_h).cuda(); v = torch.from_numpy(v_h).cuda()
 flush = torch.empty(64 * 1024 * 1024, dtype=torch.float32, device="cuda")
