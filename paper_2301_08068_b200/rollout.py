@@ -22,7 +22,7 @@ from . import _lib as L
 from ._kernels import b200
 from .geometry import EsdfGrid, Scene
 from .policies import PolicyParams
-from .rays import DEFAULT_MAX_RANGE, RayBundle
+from .rays import DEFAULT_MAX_RANGE, RayBundle, policy_range
 
 OUTCOMES = {0: "RUNNING", 1: "SUCCESS", 2: "COLLISION", 3: "TIMEOUT", 4: "STUCK"}
 
@@ -41,6 +41,9 @@ class BatchRolloutConfig:
     stuck_speed: float = 0.01
     max_range: float = DEFAULT_MAX_RANGE
     hold_mode: bool = False
+    # beyond the reference: rays stop at the activation radius (the same
+    # obstacle policy up to the summation order; rays.policy_range)
+    policy_only: bool = False
 
     def __post_init__(self):
         if self.dt <= 0:
@@ -78,8 +81,10 @@ class RolloutBatch:
         ap = cfg.params.attractor
         att = np.array([ap.alpha, ap.beta, ap.c], dtype=np.float64)
         prm = np.ascontiguousarray(cfg.params.obstacle.as_tuple(), dtype=np.float64)
+        mr = policy_range(cfg.max_range, cfg.params.obstacle.radius) if cfg.policy_only \
+            else cfg.max_range
         c = np.array([cfg.dt, cfg.max_time, cfg.robot_radius, cfg.goal_tolerance, cfg.max_accel,
-                      cfg.stuck_window, cfg.stuck_speed, cfg.max_range,
+                      cfg.stuck_window, cfg.stuck_speed, mr,
                       1.0 if cfg.hold_mode else 0.0], dtype=np.float64)
         h = ctypes.c_void_p()
         L.call("rmpb_rollout_create", self.grid.handle, self.bundle.handle, self.scene.handle,

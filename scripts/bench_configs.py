@@ -329,6 +329,18 @@ def c4loop(args, out):
            "still_running": left,
            "outcomes": {k: res.outcome.count(k) for k in set(res.outcome)},
            "note": "wall clock around rmpb_rollout_run (3 launches per tick, polled every 16)"}
+    # the same robots with policy_only rays (stopped at the activation radius)
+    import dataclasses
+    cfg_po = dataclasses.replace(cfg, policy_only=True)
+    rbp = RolloutBatch(scene, grid, bundle, starts, goals, cfg_po)
+    rbp.run(2)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    rbp.run(ticks)
+    torch.cuda.synchronize()
+    el_po = time.perf_counter() - t0
+    rec["policy_only_s_per_tick"] = round(el_po / ticks, 5)
+    rec["policy_only_robot_steps_per_s"] = round(n_rob * ticks / el_po, 1)
     # small batches are launch-bound: ticks replayed from a captured CUDA graph
     # (16 per graph launch) vs eager launches
     from paper_2301_08068_b200 import _lib as L

@@ -494,10 +494,13 @@ def _golden_scene(g):
     return P.Scene(P.Aabb(lo, hi), prims)
 
 
-def test_batched_rollout_vs_reference_golden(be, gworld, golden):
+@pytest.mark.parametrize("policy_only", [False, True])
+def test_batched_rollout_vs_reference_golden(be, gworld, golden, policy_only):
     """Row f1: closed-loop rollouts on device reproduce the reference's
     sim.rollout trajectories (ray planner): outcome, clamp count, every
-    (x, v, command) sample of the trajectory."""
+    (x, v, command) sample of the trajectory -- also with the opt-in
+    policy_only rays (stopped at the activation radius: the same policy up
+    to the summation order)."""
     import paper_2301_08068_b200 as P
     from paper_2301_08068_b200.rollout import BatchRolloutConfig, RolloutBatch
 
@@ -507,7 +510,8 @@ def test_batched_rollout_vs_reference_golden(be, gworld, golden):
     grid = P.EsdfGrid(g["grid_origin"], float(g["grid_res"]), tuple(g["grid_dims"]), vals)
     for k in (0, 1):
         cfg = BatchRolloutConfig(params=P.preset("static_map"), dt=0.01, max_time=1.5,
-                                 max_accel=float(g[f"roll{k}_maxacc"]), max_range=10.0)
+                                 max_accel=float(g[f"roll{k}_maxacc"]), max_range=10.0,
+                                 policy_only=policy_only)
         n_rec = g[f"roll{k}_pos"].shape[0] - 1
         # 3 identical robots: lockstep batches must not interfere
         starts = np.repeat(g["roll_start"][None], 3, axis=0)
