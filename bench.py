@@ -556,6 +556,18 @@ def c3_config(dev, stream, hbm_peak, flush, cpu=True, S=1024):
                         "unit": "GB/s", "frac": round(gbs / hbm_peak, 4),
                         "bytes_per_beam": 9, "kernel": "k_lidar_warp<LatticeSrc>"},
            "single_scan_public_api_us_median": round(statistics.median(lat) * 1e6, 1)}
+    # opt-in fast mode (fp32 per-beam policy math, the same contributing
+    # beams; sums within ~1e-7 of the exact mode): not the headline
+    bf, _mf = _ev_ms(lambda: lidar_policy_batch_device(dirs, R, rg, vl, v, lp, 0.3, mode="fast"),
+                     stream, flush)
+    s_ex, _ = lidar_policy_batch_device(dirs, R, rg, vl, v, lp, 0.3)
+    s_fa, _ = lidar_policy_batch_device(dirs, R, rg, vl, v, lp, 0.3, mode="fast")
+    s_ex, s_fa = s_ex.cpu().numpy(), s_fa.cpu().numpy()
+    rec["fast_mode"] = {"ms_per_launch_best": round(bf, 4),
+                        "hbm_frac": round(S * n * 9 / (bf * 1e-3) / 1e9 / hbm_peak, 4),
+                        "max_rel_sums_vs_exact": float(np.abs(s_fa[:, :12] - s_ex[:, :12]).max()
+                                                       / np.abs(s_ex[:, :12]).max()),
+                        "n_hits_equal": bool(np.array_equal(s_fa[:, 12], s_ex[:, 12]))}
     if cpu:
         sys.path.insert(0, os.path.join(ROOT, "oracle"))
         import oracle as O

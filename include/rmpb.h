@@ -255,6 +255,16 @@ RMPB_EXPORT int rmpb_lidar_policy_batch_device(const double* d_dirs, const doubl
                                    const uint8_t* d_valid, int64_t n, int64_t S, const double* d_v,
                                    const double params[7], double min_range, double* d_slot,
                                    double* d_accel, void* stream);
+/* Same with a mode: RMPB_MODE_EXACT, or RMPB_MODE_FAST = the per-beam policy
+ * math (exp / log1p / divisions) in fp32 with fp64 accumulation -- the same
+ * beams contribute (the count / radius / closing tests stay fp64), each with
+ * ~1e-7 relative error (north_star's bar for the sums: 1e-5); opt-in, NOT
+ * reference-exact. */
+RMPB_EXPORT int rmpb_lidar_policy_batch_device_mode(const double* d_dirs, const double* d_R,
+                                   const double* d_ranges, const uint8_t* d_valid, int64_t n,
+                                   int64_t S, const double* d_v, const double params[7],
+                                   double min_range, double* d_slot, double* d_accel, void* stream,
+                                   int mode);
 /* Raw sensor-frame points (f32 xyz, S x n x 3): dir = p/|p|, range = |p|;
  * zero or non-finite points are invalid. */
 RMPB_EXPORT int rmpb_lidar_points(const float* xyz, const double* R, int64_t n, const double v[3],
@@ -263,6 +273,10 @@ RMPB_EXPORT int rmpb_lidar_points(const float* xyz, const double* R, int64_t n, 
 RMPB_EXPORT int rmpb_lidar_points_batch_device(const float* d_xyz, const double* d_R, int64_t n, int64_t S,
                                    const double* d_v, const double params[7], double min_range,
                                    double* d_slot, double* d_accel, void* stream);
+RMPB_EXPORT int rmpb_lidar_points_batch_device_mode(const float* d_xyz, const double* d_R, int64_t n,
+                                   int64_t S, const double* d_v, const double params[7],
+                                   double min_range, double* d_slot, double* d_accel, void* stream,
+                                   int mode);
 
 /* ---- unfused protocol entries (parity) ---------------------------------- */
 RMPB_EXPORT int rmpb_grid_trace(const rmpb_grid* g, const double* dirs, int64_t n, const double start[3],

@@ -84,6 +84,10 @@ _SIGS = {
                                             _vp, _vp]),
     "rmpb_lidar_points": (_i, [_vp, _vp, _i64, _vp, _vp, _d, _vp, _vp, _vp]),
     "rmpb_lidar_points_batch_device": (_i, [_vp, _vp, _i64, _i64, _vp, _vp, _d, _vp, _vp, _vp]),
+    "rmpb_lidar_policy_batch_device_mode": (_i, [_vp, _vp, _vp, _vp, _i64, _i64, _vp, _vp, _d,
+                                                 _vp, _vp, _vp, _i]),
+    "rmpb_lidar_points_batch_device_mode": (_i, [_vp, _vp, _i64, _i64, _vp, _vp, _d, _vp, _vp,
+                                                 _vp, _i]),
     "rmpb_grid_trace": (_i, [_vp, _vp, _i64, _vp, _d, _d, _d, _vp, _vp, _vp, _vp]),
     "rmpb_policy_reduce": (_i, [_vp, _vp, _i64, _vp, _vp, _d, _vp, _vp]),
     "rmpb_pinv_psd": (_i, [_vp, _i64, _vp, _vp]),

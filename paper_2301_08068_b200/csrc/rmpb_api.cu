@@ -1787,7 +1787,8 @@ extern "C" int rmpb_fold_resolve_device(const double* d_slots, int64_t n, double
 template <class Src>
 static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, double v0[3],
                              const PolicyParams& pp, double* d_slot, double* d_accel,
-                             Workspace* ws, cudaStream_t st) {
+                             Workspace* ws, cudaStream_t st,
+                             int mode = RMPB_MODE_EXACT) {
   const int64_t target = g_opt_lidar_warps.load();
   int64_t wps = (target + S_ - 1) / S_;
   wps = std::min<int64_t>(wps, 1024);
@@ -1827,19 +1828,25 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
   std::call_once(once[dev & 63], [&] {
     cudaFuncSetAttribute(k_lidar_warp<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)smem);
+    cudaFuncSetAttribute(k_lidar_warp<Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
   });
-  k_lidar_warp<Src><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps, (int)seg,
-                                                             nunits, sched);
+  if (mode == RMPB_MODE_FAST)
+    k_lidar_warp<Src, true><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps,
+                                                                     (int)seg, nunits, sched);
+  else
+    k_lidar_warp<Src><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps, (int)seg,
+                                                               nunits, sched);
   CKL();
   return RMPB_OK;
 }
 
 static int lidar_launch(ScanIO sc, int64_t S_, const double* d_v, double v0[3],
                         const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
-                        cudaStream_t st) {
+                        cudaStream_t st, int mode = RMPB_MODE_EXACT) {
   LatticeSrc src{};
   src.sc = sc;
-  return launch_lidar_warp(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+  return launch_lidar_warp(src, S_, sc.n, d_v, v0, pp, d_slot, d_accel, ws, st, mode);
 }
 
 static int lidar_host(const double* d_dirs_or_null, const double* dirs, const double* R,
@@ -1915,6 +1922,18 @@ extern "C" int rmpb_lidar_policy_batch_device(const double* d_dirs, const double
                                               int64_t n, int64_t S_, const double* d_v,
                                               const double params[7], double min_range,
                                               double* d_slot, double* d_accel, void* stream) {
+  return rmpb_lidar_policy_batch_device_mode(d_dirs, d_R, d_ranges, d_valid, n, S_, d_v, params,
+                                             min_range, d_slot, d_accel, stream, RMPB_MODE_EXACT);
+}
+
+extern "C" int rmpb_lidar_policy_batch_device_mode(const double* d_dirs, const double* d_R,
+                                                   const double* d_ranges, const uint8_t* d_valid,
+                                                   int64_t n, int64_t S_, const double* d_v,
+                                                   const double params[7], double min_range,
+                                                   double* d_slot, double* d_accel, void* stream,
+                                                   int mode) {
+  if (mode != RMPB_MODE_EXACT && mode != RMPB_MODE_FAST)
+    return fail(RMPB_ERR_INVALID, "bad mode %d", mode);
   TRY(check_params(params));
   if (!d_dirs || !d_ranges || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
   if (n < 1 || n >= (1LL << 31) || S_ < 1) return fail(RMPB_ERR_INVALID, "bad n / S");
@@ -1924,15 +1943,15 @@ extern "C" int rmpb_lidar_policy_batch_device(const double* d_dirs, const double
   std::lock_guard<std::mutex> lk(ws->mu);
   ScanIO sc{d_dirs, d_R, d_ranges, d_valid, (int)n};
   return lidar_launch(sc, S_, d_v, nullptr, make_params(params, min_range), d_slot, d_accel, ws,
-                      S(stream));
+                      S(stream), mode);
 }
 
 static int points_launch(PointsIO pt, int64_t S_, const double* d_v, double v0[3],
                          const PolicyParams& pp, double* d_slot, double* d_accel, Workspace* ws,
-                         cudaStream_t st) {
+                         cudaStream_t st, int mode = RMPB_MODE_EXACT) {
   PointSrc src{};
   src.pt = pt;
-  return launch_lidar_warp(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st);
+  return launch_lidar_warp(src, S_, pt.n, d_v, v0, pp, d_slot, d_accel, ws, st, mode);
 }
 
 extern "C" int rmpb_lidar_points(const float* xyz, const double* R, int64_t n, const double v[3],
@@ -1966,6 +1985,17 @@ extern "C" int rmpb_lidar_points_batch_device(const float* d_xyz, const double* 
                                               int64_t S_, const double* d_v,
                                               const double params[7], double min_range,
                                               double* d_slot, double* d_accel, void* stream) {
+  return rmpb_lidar_points_batch_device_mode(d_xyz, d_R, n, S_, d_v, params, min_range, d_slot,
+                                             d_accel, stream, RMPB_MODE_EXACT);
+}
+
+extern "C" int rmpb_lidar_points_batch_device_mode(const float* d_xyz, const double* d_R,
+                                                   int64_t n, int64_t S_, const double* d_v,
+                                                   const double params[7], double min_range,
+                                                   double* d_slot, double* d_accel, void* stream,
+                                                   int mode) {
+  if (mode != RMPB_MODE_EXACT && mode != RMPB_MODE_FAST)
+    return fail(RMPB_ERR_INVALID, "bad mode %d", mode);
   TRY(check_params(params));
   if (!d_xyz || !d_v || !d_slot) return fail(RMPB_ERR_INVALID, "NULL device pointer");
   if (n < 1 || n >= (1LL << 31) || S_ < 1) return fail(RMPB_ERR_INVALID, "bad n / S");
@@ -1975,7 +2005,7 @@ extern "C" int rmpb_lidar_points_batch_device(const float* d_xyz, const double* 
   std::lock_guard<std::mutex> lk(ws->mu);
   PointsIO pt{d_xyz, d_R, (int)n};
   return points_launch(pt, S_, d_v, nullptr, make_params(params, min_range), d_slot, d_accel, ws,
-                       S(stream));
+                       S(stream), mode);
 }
 
 // ---------------------------------------------------------------------------

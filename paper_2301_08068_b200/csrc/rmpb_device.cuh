@@ -709,6 +709,35 @@ __device__ __forceinline__ void policy_accumulate(Acc& acc, double dx, double dy
   }
 }
 
+// policy_accumulate with the per-beam transcendental math in fp32 (opt-in
+// LiDAR "fast" mode, NOT reference-exact): the counted / in-radius /
+// closing decisions are the fp64 ones, so the same beams contribute; each
+// contribution carries ~1e-7 relative error (north_star's bar for the sums
+// is 1e-5 relative in fp32) and is accumulated in fp64.
+__device__ __forceinline__ void policy_accumulate_f32(Acc& acc, double dx, double dy, double dz,
+                                                      double d, double vx, double vy, double vz,
+                                                      const PolicyParams& p) {
+  if (d != d || d == CUDART_INF || d < p.min_range) return;
+  acc.cnt += 1;
+  const double toward = dx * vx + dy * vy + dz * vz;
+  if (!(d < p.radius) || !(toward > 0.0)) return;
+  const float df = (float)d, gf = (float)toward;
+  const float frep = (float)p.eta_rep * __expf(-df * (float)p.rnr_h);
+  const float fdamp = __fdividef((float)p.eta_damp, df * (float)p.rnd_h + (float)p.eps_p) * gf * gf;
+  const float x = 1.0f - df * (float)p.rr_h;  // w = (1 - d/r)^2
+  const float w = x * x;
+  const float cf = (float)p.c;
+  const float smag = __fdividef(fdamp, fdamp + cf * log1pf(__expf(-2.0f * cf * fdamp)));
+  const float a = w * smag * smag;
+  if (a != 0.0f) {
+    const double ad = (double)a, rx = -dx, ry = -dy, rz = -dz;
+    acc.a00 += ad * rx * rx; acc.a01 += ad * rx * ry; acc.a02 += ad * rx * rz;
+    acc.a11 += ad * ry * ry; acc.a12 += ad * ry * rz; acc.a22 += ad * rz * rz;
+    const double bf = (double)(a * (frep + fdamp));
+    acc.b0 += bf * rx; acc.b1 += bf * ry; acc.b2 += bf * rz;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // Deterministic block reduction: butterfly shuffles inside each warp (fixed
 // pairing), then warp partials summed in warp order.  The result does not

@@ -1055,7 +1055,7 @@ __device__ __forceinline__ void lidar_unit_finish(const Acc& a, const PoseIO& io
 #ifndef RMPB_LIDAR_MINB
 #define RMPB_LIDAR_MINB 4
 #endif
-template <class Src>
+template <class Src, bool F32 = false>
 __device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const PolicyParams& p,
                                                 int wps, int seg, long long unit,
                                                 LidarWarpSmem& w) {
@@ -1145,7 +1145,12 @@ __device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const
         a.zero();
         if (lane < t2) {
           const int e = (h2 + lane) & (kRing2 - 1);
-          policy_accumulate(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2], p);
+          if constexpr (F32)
+            policy_accumulate_f32(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2],
+                                  p);
+          else
+            policy_accumulate(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2],
+                              p);
         }
         h2 = (h2 + t2) & (kRing2 - 1);
         q2n -= t2;
@@ -1172,7 +1177,8 @@ __device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const
   lidar_unit_finish(a, io, scan, wu, wps, lane);
 }
 
-template <class Src>
+// F32: the opt-in fp32 policy math (policy_accumulate_f32).
+template <class Src, bool F32 = false>
 __global__ void __launch_bounds__(kBlock, RMPB_LIDAR_MINB)
 k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits,
              unsigned long long* __restrict__ sched) {
@@ -1181,7 +1187,7 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (sched == nullptr) {  // one unit per warp (the hardware block scheduler balances)
     const long long unit = (long long)blockIdx.x * kWarps + warp;
-    if (unit < nunits) lidar_warp_unit(src, io, p, wps, seg, unit, smw[warp]);
+    if (unit < nunits) lidar_warp_unit<Src, F32>(src, io, p, wps, seg, unit, smw[warp]);
     return;
   }
   // Persistent warps claiming units from a counter (sched[0]); a unit's
@@ -1193,7 +1199,7 @@ k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nun
     if (lane == 0) u = atomicAdd(sched, 1ull);
     u = __shfl_sync(0xffffffffu, u, 0);
     if ((long long)u >= nunits) break;
-    lidar_warp_unit(src, io, p, wps, seg, (long long)u, smw[warp]);
+    lidar_warp_unit<Src, F32>(src, io, p, wps, seg, (long long)u, smw[warp]);
   }
   if (lane == 0) {
     const unsigned long long W = (unsigned long long)gridDim.x * kWarps;

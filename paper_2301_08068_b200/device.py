@@ -250,10 +250,20 @@ class DdaPolicyEngine:
         return out_slot, out_accel
 
 
-def lidar_policy_batch_device(dirs, R, ranges, valid, v, params, min_range=0.3, stream=None):
+def _lidar_mode(mode):
+    if mode not in ("exact", "fast"):
+        raise ValueError("mode must be 'exact' or 'fast'")
+    return L.MODE_FAST if mode == "fast" else L.MODE_EXACT
+
+
+def lidar_policy_batch_device(dirs, R, ranges, valid, v, params, min_range=0.3, stream=None,
+                              mode: str = "exact"):
     """S scans sharing the lattice ``dirs`` (n x 3 f64, CUDA): R (S x 9 or
     None), ranges (S x n f64), valid (S x n uint8 / bool or None), v (S x 3).
-    Returns (slots S x 13, accels S x 3) CUDA tensors."""
+    Returns (slots S x 13, accels S x 3) CUDA tensors.  ``mode="fast"``
+    (opt-in, NOT reference-exact): the per-beam policy math in fp32, the
+    same contributing beams, sums within ~1e-7 relative."""
+    m = _lidar_mode(mode)
     torch = _torch()
     if not isinstance(ranges, torch.Tensor) or ranges.dim() != 2:
         raise ValueError("ranges must be a (S, n) float64 CUDA tensor")
@@ -275,15 +285,18 @@ def lidar_policy_batch_device(dirs, R, ranges, valid, v, params, min_range=0.3, 
     p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
     slots = torch.empty((S, 13), dtype=torch.float64, device=ranges.device)
     accels = torch.empty((S, 3), dtype=torch.float64, device=ranges.device)
-    L.call("rmpb_lidar_policy_batch_device", dirs.data_ptr(), None if R is None else R.data_ptr(),
-           ranges.data_ptr(), None if valid is None else valid.data_ptr(), n, S, v.data_ptr(),
-           p.ctypes.data, float(min_range), slots.data_ptr(), accels.data_ptr(),
-           _stream_ptr(stream))
+    L.call("rmpb_lidar_policy_batch_device_mode", dirs.data_ptr(),
+           None if R is None else R.data_ptr(), ranges.data_ptr(),
+           None if valid is None else valid.data_ptr(), n, S, v.data_ptr(), p.ctypes.data,
+           float(min_range), slots.data_ptr(), accels.data_ptr(), _stream_ptr(stream), m)
     return slots, accels
 
 
-def lidar_points_batch_device(xyz, R, v, params, min_range=0.3, stream=None):
-    """Raw points: xyz (S x n x 3 f32 CUDA), R (S x 9 or None), v (S x 3)."""
+def lidar_points_batch_device(xyz, R, v, params, min_range=0.3, stream=None,
+                              mode: str = "exact"):
+    """Raw points: xyz (S x n x 3 f32 CUDA), R (S x 9 or None), v (S x 3);
+    ``mode`` as lidar_policy_batch_device."""
+    m = _lidar_mode(mode)
     torch = _torch()
     if xyz.dtype != torch.float32 or not xyz.is_cuda or xyz.dim() != 3:
         raise ValueError("xyz must be a (S, n, 3) float32 CUDA tensor")
@@ -300,9 +313,9 @@ def lidar_points_batch_device(xyz, R, v, params, min_range=0.3, stream=None):
     p = np.ascontiguousarray(np.asarray(params, dtype=np.float64).reshape(7))
     slots = torch.empty((S, 13), dtype=torch.float64, device=xyz.device)
     accels = torch.empty((S, 3), dtype=torch.float64, device=xyz.device)
-    L.call("rmpb_lidar_points_batch_device", xyz.data_ptr(), None if R is None else R.data_ptr(),
+    L.call("rmpb_lidar_points_batch_device_mode", xyz.data_ptr(), None if R is None else R.data_ptr(),
            n, S, v.data_ptr(), p.ctypes.data, float(min_range), slots.data_ptr(),
-           accels.data_ptr(), _stream_ptr(stream))
+           accels.data_ptr(), _stream_ptr(stream), m)
     return slots, accels
 
 

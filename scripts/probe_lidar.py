@@ -32,13 +32,15 @@ for arg in sys.argv[1:] or ["38000"]:
     t = int(t)
     _lib.call("rmpb_set_option", b"lidar_warps", t)
     _lib.call("rmpb_set_option", b"lidar_persist", int(pers or 1))
-    sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3)
+    MODE = os.environ.get("LIDAR_MODE", "exact")
+    sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3, mode=MODE)
     torch.cuda.synchronize()
     ts = []
     for _ in range(7):
         flush.zero_()
         e0 = torch.cuda.Event(enable_timing=True); e1 = torch.cuda.Event(enable_timing=True)
-        e0.record(); sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3); e1.record()
+        e0.record(); sl, ac = lidar_policy_batch_device(dirs, R, rg, vl, v, LIDAR, 0.3, mode=MODE)
+        e1.record()
         e1.synchronize()
         ts.append(e0.elapsed_time(e1))
     s_np = sl.cpu().numpy()
@@ -46,6 +48,8 @@ for arg in sys.argv[1:] or ["38000"]:
     print(json.dumps({"target_units": t, "persist": int(pers or 1), "ms_min": round(ms, 4),
                       "ms_med": round(sorted(ts)[3], 4),
                       "hbm_frac": round(9 * 131072 * S / (ms * 1e-3) / 1e9 / peak, 4),
-                      "hits": int(s_np[:, 12].sum())}), flush=True)
+                      "hits": int(s_np[:, 12].sum()), "mode": MODE,
+                      "sum_a00": float(s_np[:, 0].sum()), "sum_b0": float(s_np[:, 9].sum())}),
+          flush=True)
 _lib.call("rmpb_set_option", b"lidar_warps", 38000)
 _lib.call("rmpb_set_option", b"lidar_persist", 1)

@@ -934,3 +934,44 @@ def test_c5_full_size_properties(be, oracle):
                                  10.0, 0.5 * synth.C5_RES, 0.9, with_cells=True, workers=8)
     assert np.array_equal(t, t_r) and np.array_equal(c, c_r)
     assert np.isfinite(t).mean() > 0.3
+
+
+@pytest.mark.parametrize("n,S", [(131072, 2), (4096, 8), (131, 3)])
+def test_lidar_fast_mode_within_north_star_tolerance(be, oracle, n, S):
+    """Opt-in LiDAR mode="fast" (per-beam policy math in fp32, fp64
+    accumulation): the same beams counted (n_hits exact) and the sums
+    within north_star's 1e-5 relative bar (measured ~1e-7), lattice scans and
+    raw points."""
+    import torch
+
+    from paper_2301_08068_b200.device import lidar_points_batch_device, lidar_policy_batch_device
+
+    rng = np.random.default_rng(n + S)
+    dirs = rng.standard_normal((n, 3))
+    dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
+    ranges = rng.uniform(0.0, 3.0, (S, n))
+    ranges[:, ::17] = np.inf
+    valid = rng.random((S, n)) < 0.8
+    v = rng.standard_normal((S, 3))
+    Rs = np.stack([np.linalg.qr(rng.standard_normal((3, 3)))[0] for _ in range(S)])
+    sl, ac = lidar_policy_batch_device(torch.from_numpy(dirs).cuda(),
+                                       torch.from_numpy(Rs.reshape(S, 9).copy()).cuda(),
+                                       torch.from_numpy(ranges).cuda(),
+                                       torch.from_numpy(valid.astype(np.uint8)).cuda(),
+                                       torch.from_numpy(v).cuda(), LIDAR, 0.3, mode="fast")
+    sl = sl.cpu().numpy()
+    for s in range(S):
+        slot_r, _ = oracle.lidar_policy(dirs @ Rs[s].T, ranges[s], valid[s], v[s], LIDAR, 0.3)
+        assert sl[s][12] == slot_r[12]
+        assert rel_err(sl[s][:12], slot_r[:12]) <= 1e-5
+    pts = rng.uniform(-3.0, 3.0, (S, n, 3)).astype(np.float32)
+    sp, _ = lidar_points_batch_device(torch.from_numpy(pts).cuda(), None,
+                                      torch.from_numpy(v).cuda(), LIDAR, 0.3, mode="fast")
+    se, _ = lidar_points_batch_device(torch.from_numpy(pts).cuda(), None,
+                                      torch.from_numpy(v).cuda(), LIDAR, 0.3)
+    sp, se = sp.cpu().numpy(), se.cpu().numpy()
+    assert np.array_equal(sp[:, 12], se[:, 12])
+    assert rel_err(sp[:, :12], se[:, :12]) <= 1e-5
+    with pytest.raises(ValueError):
+        lidar_points_batch_device(torch.from_numpy(pts).cuda(), None, torch.from_numpy(v).cuda(),
+                                  LIDAR, 0.3, mode="fp16")
