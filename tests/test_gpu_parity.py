@@ -252,21 +252,34 @@ def test_layouts_and_storage_identical(be, oracle, c1):
         assert np.array_equal(t, t_ref), kw
 
 
-def test_brick_grid_identical_to_dense(be, oracle):
-    """Block-hashed TSDF: a truncated field whose far bricks are uniform +tau."""
+@pytest.mark.parametrize("dims,f64", [((64, 48, 40), False), ((61, 45, 37), False),
+                                      ((9, 17, 10), False), ((61, 45, 37), True)])
+def test_brick_grid_identical_to_dense(be, oracle, dims, f64):
+    """Block-hashed TSDF: a truncated field whose far bricks are uniform
+    +tau -- f32 apron-QUAD bricks (dims that are not multiples of 8: bricks
+    clipped at the far faces) and f64 scalar bricks; node readback and the
+    trace bit-identical to the dense oracle."""
     rng = np.random.default_rng(3)
-    nx, ny, nz = 64, 48, 40
+    nx, ny, nz = dims
     res, tau = 0.05, 0.2
     ii, jj, kk = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
     p = np.stack([ii, jj, kk], -1) * res
-    c = np.array([1.5, 1.2, 1.0])
-    sd = np.linalg.norm(p - c, axis=-1) - 0.6
-    vals = np.clip(sd, -tau, tau).astype(np.float32).astype(np.float64)
-    dg = be.DeviceGrid(vals, np.zeros(3), res, brick_fill=float(np.float32(tau)))
-    assert dg.layout == "brick" and 0 < dg.bricks < (8 * 6 * 5)
+    ext = np.array(dims) * res
+    c = np.array([1.5, 1.2, 1.0]) if nx >= 40 else 0.45 * ext
+    rad = 0.6 if nx >= 40 else 0.3 * ext.min()
+    sd = np.linalg.norm(p - c, axis=-1) - rad
+    vals = np.clip(sd, -tau, tau)
+    if not f64:
+        vals = vals.astype(np.float32).astype(np.float64)
+    fill = float(np.float32(tau)) if not f64 else tau
+    dg = be.DeviceGrid(vals, np.zeros(3), res, brick_fill=fill)
+    nb = ((nx + 7) // 8) * ((ny + 7) // 8) * ((nz + 7) // 8)
+    assert dg.layout == "brick" and 0 < dg.bricks <= nb
+    assert dg.storage == ("f64" if f64 else "f32")
+    assert np.array_equal(dg.values(), vals)
     dirs = rng.normal(size=(4096, 3))
     dirs /= np.linalg.norm(dirs, axis=1, keepdims=True)
-    start = np.array([0.4, 0.4, 0.3])
+    start = np.array([0.4, 0.4, 0.3]) if nx >= 40 else 0.1 * ext
     t, cells, _ = be.grid_trace_ex(dg, np.zeros(3), res, start, dirs, 5.0, 0.5 * res, 0.9,
                                    with_cells=True)
     t_r, c_r = oracle.grid_trace(vals, np.zeros(3), res, start, dirs, 5.0, 0.5 * res, 0.9,
