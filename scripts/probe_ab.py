@@ -11,6 +11,8 @@ PB = int(os.environ.get("PROBE_P", "4096"))
 from paper_2301_08068_b200 import _lib
 if os.environ.get("SEG_RAYS"):
     _lib.call("rmpb_set_option", b"seg_rays", int(os.environ["SEG_RAYS"]))
+if os.environ.get("KERNEL"):
+    _lib.call("rmpb_set_option", b"kernel", int(os.environ["KERNEL"]))
 if os.environ.get("CARVEOUT"):
     _lib.call("rmpb_set_option", b"carveout", int(os.environ["CARVEOUT"]))
 if os.environ.get("TRACE_WARPS"):
@@ -43,7 +45,7 @@ print(json.dumps({"lib": os.path.basename(os.environ.get("RMPB_LIBRARY", "") or 
                   "l2_window": os.environ.get("L2_WINDOW", "default"),
                   "seg_rays": os.environ.get("SEG_RAYS", "auto"),
                   "carveout": os.environ.get("CARVEOUT", "default"),
-                  "trace_warps": os.environ.get("TRACE_WARPS", "8"), "max_range": MR, "layout": os.environ.get("LAYOUT", "auto"),
+                  "trace_warps": os.environ.get("TRACE_WARPS", "8"), "max_range": MR, "layout": os.environ.get("LAYOUT", "auto"), "kernel": os.environ.get("KERNEL", "0"),
                   "ms_min": round(min(ts), 3), "ms_med": round(sorted(ts)[len(ts) // 2], 3),
                   "hits": int(sl[:, 12].sum()), "sum_a00": float(sl[:, 0].sum()),
                   "sum_b0": float(sl[:, 9].sum())}), flush=True)
