@@ -166,12 +166,20 @@ def run_b200(args):
     world = _env_int("WORLD_SIZE", 1)
     rank = _env_int("RANK", 0)
     local = _env_int("LOCAL_RANK", 0)
+    # (RMPB_BENCH_BACKEND=gloo: a code-path check of the N > 1 flow with
+    # several ranks sharing the visible GPUs -- never a measurement)
+    backend = os.environ.get("RMPB_BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local = local % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     if world > 1:
         # communicator-init lines on stderr (the driver's rank check reads them)
         os.environ.setdefault("NCCL_DEBUG", "INFO")
         os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(backend)
     os.environ["RMPNAV_DEVICE"] = str(local)
 
     from paper_2301_08068_b200 import _lib, synth
