@@ -1809,13 +1809,14 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
   io.tickets = (unsigned*)ws->tickets.p;
   long long blocks = (nunits + kWarps - 1) / kWarps;
   if (blocks >= (1LL << 31)) return fail(RMPB_ERR_INVALID, "too many scans");
-  const size_t smem = sizeof(LidarWarpSmem) * kWarps;
+  const bool fast = mode == RMPB_MODE_FAST;
+  const size_t smem = (fast ? sizeof(LidarWarpSmemT<true>) : sizeof(LidarWarpSmemT<false>)) * kWarps;
   unsigned long long* sched = nullptr;
   if (g_opt_lidar_persist.load()) {  // persistent warps: one full wave of CTAs
     int sms = 0, dv = 0;
     CK(cudaGetDevice(&dv));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dv));
-    const long long full = (long long)sms * RMPB_LIDAR_MINB;
+    const long long full = (long long)sms * (fast ? RMPB_LIDAR_MINB_FAST : RMPB_LIDAR_MINB);
     if (blocks > full) {
       blocks = full;
       TRY(ws->ensure_sched());
@@ -1827,9 +1828,9 @@ static int launch_lidar_warp(Src src, int64_t S_, int64_t n, const double* d_v, 
   CK(cudaGetDevice(&dev));
   std::call_once(once[dev & 63], [&] {
     cudaFuncSetAttribute(k_lidar_warp<Src>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+                         (int)(sizeof(LidarWarpSmemT<false>) * kWarps));
     cudaFuncSetAttribute(k_lidar_warp<Src, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+                         (int)(sizeof(LidarWarpSmemT<true>) * kWarps));
   });
   if (mode == RMPB_MODE_FAST)
     k_lidar_warp<Src, true><<<(unsigned)blocks, kBlock, smem, st>>>(src, io, pp, (int)wps,

@@ -895,13 +895,23 @@ struct ScanIO {
 // data-determined: bitwise reproducible.
 constexpr int kRing1 = 32 + 4 * 32;  // < 32 left + one group's pushes (4 beams x 32 lanes)
 constexpr int kRing2 = 64;
-struct LidarWarpSmem {
+template <bool F32>
+struct LidarQ2 {  // stage-2 ring: range + world direction of the closing beams
+  double d[kRing2], x[kRing2], y[kRing2], z[kRing2];
+};
+template <>
+struct LidarQ2<true> {  // fast mode: the policy math is fp32 anyway (1 KB less per warp)
+  float4 e[kRing2];     // (d, x, y, z)
+};
+template <bool F32 = false>
+struct LidarWarpSmemT {
   double acc[9][32];  // per-lane running sums (lane l owns column l)
   double R[9], v[3];  // this warp's scan orientation (row-major) and velocity
   double q1d[kRing1];
   int q1i[kRing1];
-  double q2d[kRing2], q2x[kRing2], q2y[kRing2], q2z[kRing2];
+  LidarQ2<F32> q2;
 };
+using LidarWarpSmem = LidarWarpSmemT<false>;
 
 // K2b: raw sensor-frame points (no map, no lattice): the
 // beam direction is p/|p| and its range |p|; zero / non-finite points are
@@ -1058,7 +1068,7 @@ __device__ __forceinline__ void lidar_unit_finish(const Acc& a, const PoseIO& io
 template <class Src, bool F32 = false>
 __device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const PolicyParams& p,
                                                 int wps, int seg, long long unit,
-                                                LidarWarpSmem& w) {
+                                                LidarWarpSmemT<F32>& w) {
   const int lane = threadIdx.x & 31;
   const unsigned FULL = 0xffffffffu, lt = (1u << lane) - 1u;
   const int scan = (int)(unit / wps), wu = (int)(unit - (long long)scan * wps);
@@ -1133,7 +1143,11 @@ __device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const
       if (keep) {
         const int pos = (h2 + q2n + __popc(km & lt)) & (kRing2 - 1);
         RMPB_CHECK(q2n + __popc(km) <= kRing2);
-        w.q2d[pos] = d; w.q2x[pos] = wx; w.q2y[pos] = wy; w.q2z[pos] = wz;
+        if constexpr (F32)
+          w.q2.e[pos] = make_float4((float)d, (float)wx, (float)wy, (float)wz);
+        else {
+          w.q2.d[pos] = d; w.q2.x[pos] = wx; w.q2.y[pos] = wy; w.q2.z[pos] = wz;
+        }
       }
       q2n += __popc(km);
       __syncwarp();
@@ -1145,12 +1159,13 @@ __device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const
         a.zero();
         if (lane < t2) {
           const int e = (h2 + lane) & (kRing2 - 1);
-          if constexpr (F32)
-            policy_accumulate_f32(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2],
-                                  p);
-          else
-            policy_accumulate(a, w.q2x[e], w.q2y[e], w.q2z[e], w.q2d[e], w.v[0], w.v[1], w.v[2],
-                              p);
+          if constexpr (F32) {
+            const float4 q = w.q2.e[e];
+            policy_accumulate_f32(a, q.y, q.z, q.w, q.x, w.v[0], w.v[1], w.v[2], p);
+          } else {
+            policy_accumulate(a, w.q2.x[e], w.q2.y[e], w.q2.z[e], w.q2.d[e], w.v[0], w.v[1],
+                              w.v[2], p);
+          }
         }
         h2 = (h2 + t2) & (kRing2 - 1);
         q2n -= t2;
@@ -1178,12 +1193,15 @@ __device__ __forceinline__ void lidar_warp_unit(Src src, const PoseIO& io, const
 }
 
 // F32: the opt-in fp32 policy math (policy_accumulate_f32).
+#ifndef RMPB_LIDAR_MINB_FAST
+#define RMPB_LIDAR_MINB_FAST 5  // fast mode: smaller rings -> 5 CTAs of 8 warps per SM
+#endif
 template <class Src, bool F32 = false>
-__global__ void __launch_bounds__(kBlock, RMPB_LIDAR_MINB)
+__global__ void __launch_bounds__(kBlock, F32 ? RMPB_LIDAR_MINB_FAST : RMPB_LIDAR_MINB)
 k_lidar_warp(Src src, PoseIO io, PolicyParams p, int wps, int seg, long long nunits,
              unsigned long long* __restrict__ sched) {
-  extern __shared__ __align__(16) unsigned char lidar_dsm[];  // kWarps x LidarWarpSmem
-  LidarWarpSmem* smw = reinterpret_cast<LidarWarpSmem*>(lidar_dsm);
+  extern __shared__ __align__(16) unsigned char lidar_dsm[];  // kWarps x LidarWarpSmemT<F32>
+  LidarWarpSmemT<F32>* smw = reinterpret_cast<LidarWarpSmemT<F32>*>(lidar_dsm);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (sched == nullptr) {  // one unit per warp (the hardware block scheduler balances)
     const long long unit = (long long)blockIdx.x * kWarps + warp;
