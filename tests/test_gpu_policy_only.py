@@ -119,3 +119,34 @@ def be_lib():
     _lib.load()
     assert _lib.device_count() >= 1
     return _lib
+
+
+def test_policy_only_outside_poses_and_exchange(be_lib, oracle, c1):
+    """Poses outside the map (INSIDE=false body) and the K4 exchange path
+    (world-1 mailbox) with policy_only engines: the full-range oracle
+    policy, n_hits = the oracle's hits within the radius."""
+    import torch
+
+    from paper_2301_08068_b200._kernels import b200
+    from paper_2301_08068_b200.device import PeerMailbox, RayPolicyEngine
+
+    scene, grid, states = c1
+    dirs = oracle.sample_directions(16384)
+    eng = RayPolicyEngine(grid, b200.DeviceBundle(dirs), STATIC_MAP, 10.0, policy_only=True)
+    xs = np.array([[-1.5, 5.0, 3.0], [10.0, 21.0, 4.0], [5.0, 5.0, 11.0], [19.9, 19.9, 9.9]]
+                  + [s.position for s in states[:4]])
+    vs = np.tile([[0.4, -0.3, 0.2]], (len(xs), 1))
+    s, a = eng.evaluate(torch.from_numpy(xs).cuda(), torch.from_numpy(vs).cuda())
+    s, a = s.cpu().numpy(), a.cpu().numpy()
+    mb = PeerMailbox(1, 0)
+    mb.open([mb.ipc_handle])
+    try:
+        for k in range(len(xs)):
+            slot_r, acc_r, t_full = _full(oracle, grid, xs[k], vs[k], dirs)
+            _check_vs_full(s[k], a[k], slot_r, acc_r, t_full)
+            xs_t = torch.from_numpy(xs[k].copy()).cuda()
+            vs_t = torch.from_numpy(vs[k].copy()).cuda()
+            se, ae = eng.exchange(xs_t, vs_t, mb, k + 1, 0, eng.n_rays)
+            _check_vs_full(se.cpu().numpy(), ae.cpu().numpy(), slot_r, acc_r, t_full)
+    finally:
+        mb.close()
