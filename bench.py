@@ -449,6 +449,24 @@ def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n
         e1.synchronize()
         if i >= 20:
             k_us.append(e0.elapsed_time(e1) * 1e3)
+    # the same launch with max range ~0: the fixed part (launch, ray prep,
+    # first step, CTA reduce, ticket, fold, solve); the rest is the rays' tail
+    from paper_2301_08068_b200.device import RayPolicyEngine
+
+    eng0 = RayPolicyEngine(eng.grid, eng.bundle, eng.params, 1e-6)
+    k0_us = []
+    for i in range(n // 2 + 20):
+        x1 = x_all[i % 64:i % 64 + 1]
+        v1 = v_all[i % 64:i % 64 + 1]
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        torch.cuda._sleep(200000)
+        e0.record()
+        eng0.evaluate(x1, v1)
+        e1.record()
+        e1.synchronize()
+        if i >= 20:
+            k0_us.append(e0.elapsed_time(e1) * 1e3)
     # the platform floor: one empty-ish kernel launch + stream sync (host clock)
     z = torch.zeros(1, device=dev)
     f_us = []
@@ -463,13 +481,18 @@ def latency_breakdown(grid, bundle, params, states, eng, dev, lat_py, lat_srv, n
     return {"python_ray_policy_us": round(lat_py * 1e6, 2),
             "c_abi_rmpb_ray_policy_us": round(c_med, 2),
             "device_kernel_us": round(k_med, 2),
+            "device_kernel_fixed_us": round(statistics.median(k0_us), 2),
+            "device_kernel_ray_tail_us": round(k_med - statistics.median(k0_us), 2),
             "python_overhead_us": round(lat_py * 1e6 - c_med, 2),
             "host_launch_sync_readback_us": round(c_med - k_med, 2),
             "latency_server_us": round(lat_srv * 1e6, 2), "max_range_m": mr,
             "empty_kernel_launch_sync_us": round(statistics.median(f_us), 2),
             "note": "medians of 200 calls; device_kernel_us = CUDA events around one "
                     "device-resident P=1 launch (segments of 256 rays: the pose's longest "
-                    "ray is the floor)"}
+                    "ray is the floor); device_kernel_fixed_us = the same launch at max "
+                    "range ~0 (launch, prep, CTA reduce, ticket, fold, solve; includes the "
+                    "~6 us event-timing floor of any kernel); device timeline of the parts: "
+                    "profiles/README.md (scripts/lat_tl.cu)"}
 
 
 def parity_check(grid, x_h, v_h, dirs, slots, accels, poses=8):
