@@ -265,7 +265,7 @@ RMPB_EXPORT int rmpb_lidar_policy_batch_device_mode(const double* d_dirs, const 
                                    int64_t S, const double* d_v, const double params[7],
                                    double min_range, double* d_slot, double* d_accel, void* stream,
                                    int mode);
-/* Raw sensor-frame points (f32 xyz, S x n x 3): dir = p/|p|, range = |p|;
+/* Raw sensor-frame points (f32 xyz, S x n x 3): dir = p * (1/|p|), range = |p|;
  * zero or non-finite points are invalid. */
 RMPB_EXPORT int rmpb_lidar_points(const float* xyz, const double* R, int64_t n, const double v[3],
                       const double params[7], double min_range, double out_slot[13],

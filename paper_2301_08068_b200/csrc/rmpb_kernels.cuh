@@ -914,7 +914,7 @@ struct LidarWarpSmemT {
 using LidarWarpSmem = LidarWarpSmemT<false>;
 
 // K2b: raw sensor-frame points (no map, no lattice): the
-// beam direction is p/|p| and its range |p|; zero / non-finite points are
+// beam direction is p * (1/|p|) and its range |p|; zero / non-finite points are
 // invalid.  Float32 xyz as delivered by the sensor driver.
 struct PointsIO {
   const float* __restrict__ xyz;  // [S][N][3]
@@ -1011,8 +1011,11 @@ struct PointSrc {
       }
     }
   }
+  // direction p * (1/|p|): one fp64 division per point instead of three
+  // (within 1 ulp of p / |p|; C3 points 0.74 -> 0.69 ms)
   __device__ __forceinline__ void dir(int i, double d, double& ex, double& ey, double& ez) const {
-    ex = (double)P[3 * i] / d; ey = (double)P[3 * i + 1] / d; ez = (double)P[3 * i + 2] / d;
+    const double r = 1.0 / d;
+    ex = (double)P[3 * i] * r; ey = (double)P[3 * i + 1] * r; ez = (double)P[3 * i + 2] * r;
   }
   __device__ __forceinline__ void prefetch(int i0, int end) const {
     if (!vec || i0 + 128 > end) return;

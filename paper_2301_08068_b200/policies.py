@@ -247,7 +247,8 @@ def lidar_policy_points(velocity, points, p: ObstacleParams, orientation=None,
                         min_range: float = DEFAULT_LIDAR_MIN_RANGE,
                         backend: str | None = None) -> Policy:
     """LiDAR-direct policy from raw sensor-frame points (N x 3): beam
-    direction p/|p|, range |p|; zero / non-finite points are invalid."""
+    direction p * (1/|p|) (within 1 ulp of p/|p|), range |p|; zero / non-finite points
+    are invalid."""
     be = get_backend(backend)
     slot, accel = be.lidar_points_fused(points, orientation, np.asarray(velocity, dtype=float),
                                         p.as_tuple(), min_range)
