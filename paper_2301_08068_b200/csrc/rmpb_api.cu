@@ -216,8 +216,6 @@ struct rmpb_bundle {
   double* d_dy = nullptr;
   double* d_dz = nullptr;
   int* d_perm = nullptr;   // stored -> original (null when identity)
-  double* d_rcp = nullptr; // [6][n] double-double reciprocals of dx, dy, dz
-  int64_t rs = 0;          // row stride of d_rcp (full size; differs for range views)
   double* d_aos = nullptr; // original order AoS (for LiDAR use / download)
 };
 
@@ -927,8 +925,6 @@ static int bundle_finish(rmpb_bundle* b, cudaStream_t st) {
   CK(cudaMalloc((void**)&b->d_dx, n * sizeof(double)));
   CK(cudaMalloc((void**)&b->d_dy, n * sizeof(double)));
   CK(cudaMalloc((void**)&b->d_dz, n * sizeof(double)));
-  CK(cudaMalloc((void**)&b->d_rcp, 6 * (size_t)n * sizeof(double)));
-  b->rs = n;
   if (b->order == RMPB_ORDER_MORTON) {
     unsigned *k_in, *k_out;
     int* i_in;
@@ -947,8 +943,7 @@ static int bundle_finish(rmpb_bundle* b, cudaStream_t st) {
     CK(cudaStreamSynchronize(st));
     rfree(tmp); rfree(k_in); rfree(k_out); rfree(i_in);
   }
-  k_gather_dirs<<<grid_blocks(n), 256, 0, st>>>(n, b->d_aos, b->d_perm, b->d_dx, b->d_dy, b->d_dz,
-                                                b->d_rcp);
+  k_gather_dirs<<<grid_blocks(n), 256, 0, st>>>(n, b->d_aos, b->d_perm, b->d_dx, b->d_dy, b->d_dz);
   CKL();
   CK(cudaStreamSynchronize(st));
   return RMPB_OK;
@@ -1001,7 +996,7 @@ static int bundle_new(const double* dirs, int64_t n, int order, int device, bool
   cudaStreamDestroy(st);
   if (rc != RMPB_OK) {
     rmpb_bundle* p = b.release();
-    rfree(p->d_aos); rfree(p->d_dx); rfree(p->d_dy); rfree(p->d_dz); rfree(p->d_perm); rfree(p->d_rcp);
+    rfree(p->d_aos); rfree(p->d_dx); rfree(p->d_dy); rfree(p->d_dz); rfree(p->d_perm);
     delete p;
     return rc;
   }
@@ -1041,7 +1036,6 @@ extern "C" int rmpb_bundle_destroy(rmpb_bundle* b) {
   if (!b) return RMPB_OK;
   DeviceGuard dg(b->device);
   rfree(b->d_aos); rfree(b->d_dx); rfree(b->d_dy); rfree(b->d_dz);
-  rfree(b->d_rcp);
   if (b->d_perm) rfree(b->d_perm);
   delete b;
   return RMPB_OK;
@@ -1050,7 +1044,6 @@ extern "C" int rmpb_bundle_destroy(rmpb_bundle* b) {
 static Bundle bundle_view(const rmpb_bundle* b) {
   Bundle v;
   v.dx = b->d_dx; v.dy = b->d_dy; v.dz = b->d_dz; v.perm = b->d_perm; v.n = (int)b->n;
-  v.rcp = b->d_rcp; v.rs = (int)b->rs;
   return v;
 }
 
@@ -1398,7 +1391,6 @@ extern "C" int rmpb_ray_policy_range_device(const rmpb_grid* g, const rmpb_bundl
   sub.d_dx = b->d_dx + ray_begin;
   sub.d_dy = b->d_dy + ray_begin;
   sub.d_dz = b->d_dz + ray_begin;
-  sub.d_rcp = b->d_rcp + ray_begin;  // row stride stays b->rs
   sub.d_perm = nullptr;
   sub.n = ray_end - ray_begin;
   if (sub.n == 0) {
@@ -1752,7 +1744,6 @@ extern "C" int rmpb_ray_policy_range_exchange(const rmpb_grid* g, const rmpb_bun
   sub.d_dx = b->d_dx + ray_begin;
   sub.d_dy = b->d_dy + ray_begin;
   sub.d_dz = b->d_dz + ray_begin;
-  sub.d_rcp = b->d_rcp + ray_begin;
   sub.d_perm = nullptr;
   sub.n = ray_end - ray_begin;
   int segs, seg_rays;

@@ -91,28 +91,16 @@ __global__ void k_morton_keys(int n, const double* __restrict__ dirs_aos, unsign
   idx[i] = i;
 }
 
-// Stored-order SoA directions + double-double reciprocals (exdiv divisors).
+// Stored-order SoA directions.
 __global__ void k_gather_dirs(int n, const double* __restrict__ dirs_aos, const int* __restrict__ perm,
                               double* __restrict__ dx, double* __restrict__ dy,
-                              double* __restrict__ dz, double* __restrict__ rcp) {
+                              double* __restrict__ dz) {
   int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   int o = perm ? perm[i] : i;
-  double c[3] = {dirs_aos[3 * o], dirs_aos[3 * o + 1], dirs_aos[3 * o + 2]};
-  dx[i] = c[0];
-  dy[i] = c[1];
-  dz[i] = c[2];
-  for (int a = 0; a < 3; ++a) {
-    double hi = 0.0, lo = 0.0;
-    // |d| < 2^-1000 (subnormal included): 1/d overflows or exdiv's error
-    // analysis fails -> NaN reciprocal = "divide with IEEE /" (slab_div)
-    if (c[a] != 0.0) {
-      if (fabs(c[a]) < 0x1p-1000) hi = lo = CUDART_NAN;
-      else recip_dd(c[a], hi, lo);
-    }
-    rcp[(2 * a) * n + i] = hi;
-    rcp[(2 * a + 1) * n + i] = lo;
-  }
+  dx[i] = dirs_aos[3 * o];
+  dy[i] = dirs_aos[3 * o + 1];
+  dz[i] = dirs_aos[3 * o + 2];
 }
 
 __global__ void k_soa_to_aos(int n, const double* __restrict__ dx, const double* __restrict__ dy,

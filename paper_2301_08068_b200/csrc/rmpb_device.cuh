@@ -475,30 +475,21 @@ __device__ __forceinline__ float interp_f(const G& grid, const GeomF& g, float p
   return __fmaf_rn(fx, c1 - c0, c0);
 }
 
-// Per-ray reciprocal of a direction component (0 -> unused; NaN -> the
-// component is below 2^-1000: use IEEE division).
-struct RecipDir { double hx, lx, hy, ly, hz, lz; };
-
-// Slab quotient (bound - s) / d with the per-ray reciprocal.  exdiv equals
-// IEEE `/` for |a| >= 2^-960 and a normal divisor of moderate size; outside
-// that (a tiny numerator, |d| < 2^-1000 flagged by a NaN reciprocal, a
-// quotient that overflows -> exdiv NaN) the rare branch divides with IEEE
-// `/`, so the slab interval -- and the MISS decisions built on it -- stay
-// bit-identical to the reference's _box_span (_ckern.pyx:171-212) for every
-// input, subnormal direction components included.
-__device__ __forceinline__ double slab_div(double a, double d, double hi, double lo) {
-  double q = exdiv(a, d, hi, lo);
-  if (!(fabs(a) >= 0x1p-960) || q != q) q = a / d;
-  return q;
-}
+// Slab quotient (bound - s) / d: the reference's IEEE division
+// (_ckern.pyx:171-212), bit-identical for every input (tiny numerators,
+// subnormal direction components, overflowing quotients included).
+// (r2: a per-ray double-double reciprocal with exdiv and an IEEE fallback
+// branch was SLOWER than the native division here -- 12.19 vs 11.3 ms per
+// 4096-pose step; it is once per ray, off the step chain.)
+__device__ __forceinline__ double slab_div(double a, double d) { return a / d; }
 
 // box_span with exdiv by the per-ray reciprocals: bit-identical to box_span.
 __device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, double sy, double sz,
-                                              double dx, double dy, double dz, const RecipDir& q,
+                                              double dx, double dy, double dz,
                                               double& t0, double& t1) {
   double tlo = -CUDART_INF, thi = CUDART_INF, ta, tb, tmp;
   if (dx != 0.0) {
-    ta = slab_div(g.ox - sx, dx, q.hx, q.lx); tb = slab_div(g.hx - sx, dx, q.hx, q.lx);
+    ta = slab_div(g.ox - sx, dx); tb = slab_div(g.hx - sx, dx);
     if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
     if (ta > tlo) tlo = ta;
     if (tb < thi) thi = tb;
@@ -506,7 +497,7 @@ __device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, doub
     return false;
   }
   if (dy != 0.0) {
-    ta = slab_div(g.oy - sy, dy, q.hy, q.ly); tb = slab_div(g.hy - sy, dy, q.hy, q.ly);
+    ta = slab_div(g.oy - sy, dy); tb = slab_div(g.hy - sy, dy);
     if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
     if (ta > tlo) tlo = ta;
     if (tb < thi) thi = tb;
@@ -514,7 +505,7 @@ __device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, doub
     return false;
   }
   if (dz != 0.0) {
-    ta = slab_div(g.oz - sz, dz, q.hz, q.lz); tb = slab_div(g.hz - sz, dz, q.hz, q.lz);
+    ta = slab_div(g.oz - sz, dz); tb = slab_div(g.hz - sz, dz);
     if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
     if (ta > tlo) tlo = ta;
     if (tb < thi) thi = tb;
@@ -587,18 +578,17 @@ __device__ __forceinline__ TraceResult trace_ray(const G& grid, const GridGeom& 
   return r;
 }
 
-// Sphere trace with the exact fast arithmetic (exdiv slab interval with the
-// per-ray reciprocals, interp_fast): bit-identical to trace_ray.
+// Sphere trace with the exact fast arithmetic (interp_fast): bit-identical
+// to trace_ray.
 template <class G>
 __device__ __forceinline__ TraceResult trace_ray_fast(const G& grid, const GridGeom& g, double sx,
                                                       double sy, double sz, double dx, double dy,
-                                                      double dz, const RecipDir& q,
-                                                      double max_range, double eps,
+                                                      double dz, double max_range, double eps,
                                                       double step_scale) {
   TraceResult r;
   r.t = CUDART_INF; r.cx = r.cy = r.cz = -1; r.steps = 0;
   double t0, t1;
-  if (!box_span_fast(g, sx, sy, sz, dx, dy, dz, q, t0, t1)) return r;
+  if (!box_span_fast(g, sx, sy, sz, dx, dy, dz, t0, t1)) return r;
   double t = t0 > 0.0 ? t0 : 0.0;
   const double t_end = t1 < max_range ? t1 : max_range;
   if (t > t_end) return r;
@@ -622,22 +612,22 @@ template <class G>
 __device__ __forceinline__ TraceResult trace_ray_inside(const G& grid, const GridGeom& g,
                                                         double sx, double sy, double sz,
                                                         double dx, double dy, double dz,
-                                                        const RecipDir& q, double max_range,
+                                                        double max_range,
                                                         double eps, double step_scale, bool skip1,
                                                         double t1s) {
   TraceResult r;
   r.t = CUDART_INF; r.cx = r.cy = r.cz = -1; r.steps = 0;
   double thi = CUDART_INF;
   if (dx != 0.0) {
-    const double tb = slab_div((dx > 0.0 ? g.hx : g.ox) - sx, dx, q.hx, q.lx);
+    const double tb = slab_div((dx > 0.0 ? g.hx : g.ox) - sx, dx);
     thi = tb < thi ? tb : thi;
   }
   if (dy != 0.0) {
-    const double tb = slab_div((dy > 0.0 ? g.hy : g.oy) - sy, dy, q.hy, q.ly);
+    const double tb = slab_div((dy > 0.0 ? g.hy : g.oy) - sy, dy);
     thi = tb < thi ? tb : thi;
   }
   if (dz != 0.0) {
-    const double tb = slab_div((dz > 0.0 ? g.hz : g.oz) - sz, dz, q.hz, q.lz);
+    const double tb = slab_div((dz > 0.0 ? g.hz : g.oz) - sz, dz);
     thi = tb < thi ? tb : thi;
   }
   const double t_end = thi < max_range ? thi : max_range;

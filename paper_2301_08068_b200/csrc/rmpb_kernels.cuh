@@ -185,16 +185,8 @@ struct Bundle {
   const double* __restrict__ dx;
   const double* __restrict__ dy;
   const double* __restrict__ dz;
-  const double* __restrict__ rcp;  // [6][n]: hi/lo reciprocal of dx, dy, dz (exdiv)
   const int* __restrict__ perm;    // stored index -> original index (null = identity)
   int n;
-  int rs;                          // row stride of rcp (the full bundle size)
-  __device__ __forceinline__ RecipDir recip(int i) const {
-    RecipDir q;
-    q.hx = rcp[i]; q.lx = rcp[rs + i]; q.hy = rcp[2 * rs + i];
-    q.ly = rcp[3 * rs + i]; q.hz = rcp[4 * rs + i]; q.lz = rcp[5 * rs + i];
-    return q;
-  }
 };
 
 __device__ __forceinline__ void acc_to_arr(const Acc& a, double* o) {
@@ -382,10 +374,10 @@ __device__ __forceinline__ bool lean_unit(const G& grid, const GridGeom& g, cons
   }
   for (int i = begin + threadIdx.x; i < end; i += kBlock) {
     const double dx = b.dx[i], dy = b.dy[i], dz = b.dz[i];
-    TraceResult r = inside ? trace_ray_inside(grid, g, sx, sy, sz, dx, dy, dz, b.recip(i),
-                                              max_range, eps, step_scale, skip1, t1s)
-                           : trace_ray_fast(grid, g, sx, sy, sz, dx, dy, dz, b.recip(i),
-                                            max_range, eps, step_scale);
+    TraceResult r = inside ? trace_ray_inside(grid, g, sx, sy, sz, dx, dy, dz, max_range, eps,
+                                              step_scale, skip1, t1s)
+                           : trace_ray_fast(grid, g, sx, sy, sz, dx, dy, dz, max_range, eps,
+                                            step_scale);
     policy_accumulate(acc, dx, dy, dz, r.t, vx, vy, vz, p);
     my_steps += r.steps;
     if (ro.t) {
@@ -587,18 +579,17 @@ __device__ __forceinline__ void prep_chunk(K2Smem<NW>& sm, const GridGeom& g, co
   if (ok) {
     ex = b.dx[r]; ey = b.dy[r]; ez = b.dz[r];
     if (INSIDE) {
-      const RecipDir q = b.recip(r);
       double thi = CUDART_INF;
       if (ex != 0.0) {
-        const double tb = slab_div((ex > 0.0 ? g.hx : g.ox) - sx, ex, q.hx, q.lx);
+        const double tb = slab_div((ex > 0.0 ? g.hx : g.ox) - sx, ex);
         thi = tb < thi ? tb : thi;
       }
       if (ey != 0.0) {
-        const double tb = slab_div((ey > 0.0 ? g.hy : g.oy) - sy, ey, q.hy, q.ly);
+        const double tb = slab_div((ey > 0.0 ? g.hy : g.oy) - sy, ey);
         thi = tb < thi ? tb : thi;
       }
       if (ez != 0.0) {
-        const double tb = slab_div((ez > 0.0 ? g.hz : g.oz) - sz, ez, q.hz, q.lz);
+        const double tb = slab_div((ez > 0.0 ? g.hz : g.oz) - sz, ez);
         thi = tb < thi ? tb : thi;
       }
       t0 = 0.0;
@@ -612,8 +603,7 @@ __device__ __forceinline__ void prep_chunk(K2Smem<NW>& sm, const GridGeom& g, co
         ok = t1s <= t1;  // !(t > t_end): NaN ends the ray
       }
     } else {
-      ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, b.recip(r), t0,
-                         t1);
+      ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, t0, t1);
       if (ok) {
         t0 = t0 > 0.0 ? t0 : 0.0;
         t1 = t1 < max_range ? t1 : max_range;
