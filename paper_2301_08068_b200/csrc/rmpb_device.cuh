@@ -483,39 +483,6 @@ __device__ __forceinline__ float interp_f(const G& grid, const GeomF& g, float p
 // 4096-pose step; it is once per ray, off the step chain.)
 __device__ __forceinline__ double slab_div(double a, double d) { return a / d; }
 
-// box_span with exdiv by the per-ray reciprocals: bit-identical to box_span.
-__device__ __forceinline__ bool box_span_fast(const GridGeom& g, double sx, double sy, double sz,
-                                              double dx, double dy, double dz,
-                                              double& t0, double& t1) {
-  double tlo = -CUDART_INF, thi = CUDART_INF, ta, tb, tmp;
-  if (dx != 0.0) {
-    ta = slab_div(g.ox - sx, dx); tb = slab_div(g.hx - sx, dx);
-    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
-    if (ta > tlo) tlo = ta;
-    if (tb < thi) thi = tb;
-  } else if (sx < g.ox || sx > g.hx) {
-    return false;
-  }
-  if (dy != 0.0) {
-    ta = slab_div(g.oy - sy, dy); tb = slab_div(g.hy - sy, dy);
-    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
-    if (ta > tlo) tlo = ta;
-    if (tb < thi) thi = tb;
-  } else if (sy < g.oy || sy > g.hy) {
-    return false;
-  }
-  if (dz != 0.0) {
-    ta = slab_div(g.oz - sz, dz); tb = slab_div(g.hz - sz, dz);
-    if (tb < ta) { tmp = ta; ta = tb; tb = tmp; }
-    if (ta > tlo) tlo = ta;
-    if (tb < thi) thi = tb;
-  } else if (sz < g.oz || sz > g.hz) {
-    return false;
-  }
-  t0 = tlo; t1 = thi;
-  return true;
-}
-
 // Slab interval against the node domain (rmpnav/_kernels/_ckern.pyx:171-212).
 __device__ __forceinline__ bool box_span(const GridGeom& g, double sx, double sy, double sz,
                                          double dx, double dy, double dz, double& t0, double& t1) {
@@ -588,7 +555,7 @@ __device__ __forceinline__ TraceResult trace_ray_fast(const G& grid, const GridG
   TraceResult r;
   r.t = CUDART_INF; r.cx = r.cy = r.cz = -1; r.steps = 0;
   double t0, t1;
-  if (!box_span_fast(g, sx, sy, sz, dx, dy, dz, t0, t1)) return r;
+  if (!box_span(g, sx, sy, sz, dx, dy, dz, t0, t1)) return r;
   double t = t0 > 0.0 ? t0 : 0.0;
   const double t_end = t1 < max_range ? t1 : max_range;
   if (t > t_end) return r;

@@ -497,7 +497,8 @@ k_ray_server(G grid, GridGeom g, Bundle b, PolicyParams p, double max_range, dou
 
 // K1/K3 v2: the production trace kernel.
 //
-// * exact arithmetic via interp_fast / box_span_fast (no MUFU, no F2I/I2F);
+// * exact arithmetic via interp_fast (no MUFU, no F2I/I2F on the step) and
+//   the reference's IEEE slab divisions;
 // * work split: a unit's rays are cut into 32-ray chunks (consecutive in the
 //   Morton-ordered bundle) dealt round-robin to the CTA's warps, which keeps
 //   the warps' total march lengths balanced;
@@ -603,7 +604,7 @@ __device__ __forceinline__ void prep_chunk(K2Smem<NW>& sm, const GridGeom& g, co
         ok = t1s <= t1;  // !(t > t_end): NaN ends the ray
       }
     } else {
-      ok = box_span_fast(g, sx, sy, sz, ex, ey, ez, t0, t1);
+      ok = box_span(g, sx, sy, sz, ex, ey, ez, t0, t1);
       if (ok) {
         t0 = t0 > 0.0 ? t0 : 0.0;
         t1 = t1 < max_range ? t1 : max_range;
